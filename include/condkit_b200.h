@@ -1,0 +1,162 @@
+/*
+ * condkit_b200.h -- C ABI of the B200-native Projected-Adam kappa_2 estimator.
+ *
+ * Drop-in boundary for the reference estimator / error-bound interface
+ * (condkit, /root/reference/proj/include/condkit). Every entry point names the
+ * reference symbol (file:line) it replaces. Plain pointers and sizes only; no
+ * C++ or torch types cross this boundary and no exception escapes it.
+ *
+ * Conventions
+ *  - Every function returns a ck_status; on failure ck_last_error() returns a
+ *    thread-local message. Status values map 1:1 onto the reference's
+ *    exception types (see ck_status).
+ *  - Matrices are CSR: int64 row offsets (nrows+1, starting at 0), int32 column
+ *    indices strictly increasing within a row, finite double values -- the
+ *    invariants of SparseMatrix (sparse.hpp:47-52, validated at 129-145).
+ *  - Vectors passed as `const double*` / `double*` are HOST buffers unless the
+ *    name ends in `_dev`. Host buffers may be registered with
+ *    ck_host_register() so transfers run at pinned-memory speed.
+ *  - A handle is bound to the device current at its creation and owns one
+ *    CUDA stream. Calls on distinct handles are thread-safe; calls on one
+ *    handle must be serialised by the caller (the reference's objects are
+ *    likewise single-threaded per run).
+ */
+#ifndef CONDKIT_B200_H
+#define CONDKIT_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CK_OK = 0,
+  CK_ERR_DIMENSION = 1,        /* DimensionMismatch          sparse.hpp:25-27 */
+  CK_ERR_INVALID_ARGUMENT = 2, /* std::invalid_argument      condest.hpp:187,303 */
+  CK_ERR_LOGIC = 3,            /* std::logic_error (witness)  condest.hpp:286-289 */
+  CK_ERR_STRUCT_SINGULAR = 4,  /* StructurallySingular        lu.hpp:24-30 */
+  CK_ERR_NUM_SINGULAR = 5,     /* NumericallySingular         lu.hpp:32-40 */
+  CK_ERR_ZERO_RHS = 6,         /* ZeroRHS                     error_bounds.hpp:33-35 */
+  CK_ERR_ZERO_SOLUTION = 7,    /* ZeroSolution                error_bounds.hpp:37-39 */
+  CK_ERR_CUDA = 20,            /* CUDA runtime failure (no reference analogue) */
+  CK_ERR_NO_DEVICE = 21,       /* no sm_100 device visible */
+  CK_ERR_UNSUPPORTED = 22,     /* input outside this build's limits (e.g. nnz >= 2^32) */
+  CK_ERR_OUT_OF_MEMORY = 23
+} ck_status;
+
+/* AdamConfig, condest.hpp:39-48 (same fields, same defaults via ck_adam_default). */
+typedef struct {
+  double alpha, beta1, beta2, eps_stab;
+  uint64_t max_iter, seed;
+  double rel_tol;
+  uint64_t patience;
+} ck_adam_cfg;
+
+/* NormEstimate, condest.hpp:69-74 (the witness is returned through a separate buffer). */
+typedef struct {
+  double value;
+  uint64_t iterations;
+  int32_t converged;
+  int32_t _pad;
+} ck_norm_result;
+
+/* Per-iteration scalars of AdamStepInfo (condest.hpp:61-65) plus the AdamState
+ * scalars (condest.hpp:51-56) for observer mode. */
+typedef struct {
+  uint64_t t;
+  double loss, loss_min;
+  double x_dot_delta, delta_norm;
+  int32_t phase; /* 0 running, 1 restarted this step, 2 finished */
+  int32_t _pad;
+} ck_step_info;
+
+typedef struct {
+  int64_t nrows, ncols, nnz;
+  int64_t sell_entries_a, sell_entries_at; /* stored entries incl. slice padding */
+  int64_t device_bytes;
+  int32_t device;
+  int32_t _pad;
+} ck_matrix_info;
+
+typedef struct ck_matrix_s* ck_matrix;
+typedef struct ck_session_s* ck_session;
+
+/* ----------------------------------------------------------------- runtime */
+const char* ck_last_error(void);
+int32_t ck_abi_version(void);
+ck_status ck_device_count(int32_t* count);
+/* Select the device for handles created by this thread (cudaSetDevice). */
+ck_status ck_set_device(int32_t device);
+ck_status ck_device_synchronize(void);
+ck_status ck_host_register(void* ptr, uint64_t bytes);
+ck_status ck_host_unregister(void* ptr);
+void ck_adam_default(ck_adam_cfg* cfg);
+
+/* --------------------------------------------------- rng.hpp mirror (host) */
+/* mix_seed, rng.hpp:23-28 */
+uint64_t ck_mix_seed(uint64_t base, uint64_t stream);
+/* `count` successive random_unit_vector(n, gen) draws from one mt19937_64(seed),
+ * rng.hpp:68-77; bit-identical to the reference. */
+ck_status ck_random_unit_vectors(uint64_t seed, int64_t n, int64_t count, double* out);
+
+/* ------------------------------------------ error_bounds.hpp scalar formulas */
+ck_status ck_loose_bounds(double residual_norm, double b_norm, double kappa, double* lower,
+                          double* upper);                               /* :59-68 */
+ck_status ck_tight_bounds(double residual_norm, double a_norm, double xhat_norm, double kappa,
+                          double* lower, double* upper);                /* :71-80 */
+ck_status ck_propagate_bound(double eps_tight, double* out);           /* :84-88 */
+ck_status ck_singularity_bound(double kappa, double eps_mach, double* out); /* :93-99 */
+
+/* --------------------------------------------------- device-resident operator */
+/* Uploads A (SparseMatrix, sparse.hpp:52-152) and builds, on the device, the
+ * sliced-ELL layouts of A and A^T used by every kernel. Validates the CSR
+ * invariants like SparseMatrix::validate (sparse.hpp:129-145). */
+ck_status ck_matrix_upload(int64_t nrows, int64_t ncols, const int64_t* row_offsets,
+                           const int32_t* col_indices, const double* values, ck_matrix* out);
+ck_status ck_matrix_free(ck_matrix a);
+ck_status ck_matrix_get_info(ck_matrix a, ck_matrix_info* info);
+/* y = A x, matvec sparse.hpp:212-226 (stored-order row sums: bit-identical). */
+ck_status ck_spmv(ck_matrix a, const double* x, double* y);
+/* y = A^T x, transpose_matvec sparse.hpp:230-242 (increasing-row accumulation per
+ * output: bit-identical). */
+ck_status ck_spmv_t(ck_matrix a, const double* x, double* y);
+/* ||A x - b||, ||x||, ||b|| (verify_solution residual, error_bounds.hpp:176-183). */
+ck_status ck_residual_norms(ck_matrix a, const double* x, const double* b, double* r_norm,
+                            double* x_norm, double* b_norm);
+/* loss_explicit / grad_explicit (condest.hpp:88-107) on the device. */
+ck_status ck_loss_explicit(ck_matrix a, const double* x, double* loss);
+ck_status ck_grad_explicit(ck_matrix a, const double* x, double* g);
+
+/* ------------------------------------------ Projected Adam (ExplicitOracle) */
+/* projected_adam(ExplicitOracle(A), cfg), condest.hpp:184-297 and norm2 :315-317.
+ * witness (ncols doubles) may be NULL. */
+ck_status ck_projected_adam(ck_matrix a, const ck_adam_cfg* cfg, ck_norm_result* res,
+                            double* witness);
+/* estimate_norm(ExplicitOracle(A), cfg, restarts), condest.hpp:301-312. The
+ * restarts run concurrently as columns of one multi-vector iteration; each is
+ * bit-identical to running it alone. */
+ck_status ck_estimate_norm(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts,
+                           ck_norm_result* res, double* witness);
+
+/* Session: the device-resident loop with explicit control (bench, observer).
+ * `ncols` independent runs with seeds[c]; each follows projected_adam exactly. */
+ck_status ck_session_create(ck_matrix a, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                            int32_t ncols, ck_session* out);
+/* Runs until every column finished (max_steps == 0) or for at most max_steps
+ * loop trips. *finished = 1 when all columns are done. */
+ck_status ck_session_run(ck_session s, uint64_t max_steps, int32_t* finished);
+/* One loop trip with per-step scalars for column 0 (AdamObserver mode). */
+ck_status ck_session_step_observed(ck_session s, ck_step_info* info, double* x, double* x_min);
+/* Device-timed steps (CUDA events on the session stream): runs `steps` loop trips.
+ * mode 0: one event between every kernel -> total plus per-kernel milliseconds;
+ * mode 1: CUDA-graph chunks, total only (per-kernel outputs set to -1).
+ * Columns must not finish inside the timed region (max_iter/patience large enough). */
+ck_status ck_session_time(ck_session s, uint64_t steps, int32_t mode, double* ms_total,
+                          double* ms_apply, double* ms_transpose);
+ck_status ck_session_result(ck_session s, int32_t column, ck_norm_result* res, double* witness);
+ck_status ck_session_free(ck_session s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,25 @@
+"""condkit-b200: B200-native Projected-Adam kappa_2 estimator (arXiv 2409.11515).
+
+Drop-in for the reference's estimator / error-bound interface
+(condkit/condest.hpp, error_bounds.hpp, sparse.hpp). Every numeric operation
+runs in ``libcondkit_b200.so`` (sm_100a kernels behind a C ABI,
+include/condkit_b200.h); there is no CPU fallback.
+"""
+from .condest import (AdamConfig, AdamState, AdamStepInfo, ExplicitOracle, GradientOracle,
+                      NormEstimate, Session, estimate_norm, grad_explicit, loss_explicit, norm2,
+                      projected_adam)
+from .errors import (CondkitError, DegenerateDirection, DeviceUnavailable, DimensionMismatch,
+                     InvalidArgument, LogicError, NativeLibraryMissing, NumericallySingular,
+                     StructurallySingular, ZeroRHS, ZeroSolution)
+from .rng import mix_seed, random_unit_vector, random_unit_vectors
+from .sparse import DeviceMatrix, SparseMatrix, matvec, transpose_matvec
+
+__all__ = [
+    "AdamConfig", "AdamState", "AdamStepInfo", "ExplicitOracle", "GradientOracle",
+    "NormEstimate", "Session", "estimate_norm", "grad_explicit", "loss_explicit", "norm2",
+    "projected_adam", "CondkitError", "DegenerateDirection", "DeviceUnavailable",
+    "DimensionMismatch", "InvalidArgument", "LogicError", "NativeLibraryMissing",
+    "NumericallySingular", "StructurallySingular", "ZeroRHS", "ZeroSolution", "mix_seed",
+    "random_unit_vector", "random_unit_vectors", "DeviceMatrix", "SparseMatrix", "matvec",
+    "transpose_matvec",
+]

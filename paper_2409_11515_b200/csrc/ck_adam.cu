@@ -1,0 +1,751 @@
+// Device-resident Projected Adam (condest.hpp:184-297) for the explicit
+// operator (ExplicitOracle, condest.hpp:125-135).
+//
+// One loop trip ("step") is two kernels over HBM-resident state:
+//
+//   k_apply<R>      x~ = x - (delta - r x)          (tangent step, :231-240)
+//                   y' = A x~                        (sliced-ELL SpMV; loss at
+//                                                     x_{t+1} = x~/||x~||, :249-251)
+//                   reduce ||x~|| (double-double, the compensated norm :241)
+//                   and ||y'|| (one-pass scaled sum of squares, two_norm)
+//                   -> last CTA: loss, patience, best-tracking, next iteration
+//                      scalars (:221-224, :257-275)
+//   k_transpose<R>  x_{t+1} = x~/||x~|| materialised into a free buffer,
+//                   z = A^T y' / ||x~||              (grad, :96-107)
+//                   g, m, v, delta (Adam, :225-229), reduce r = x.delta (:231)
+//                   -> last CTA: radial scalar for the next k_apply.
+//
+// A x_{t+1} is therefore computed once per iteration and serves both the loss
+// of iteration t and the gradient of iteration t+1 (the reference evaluates it
+// twice on bitwise-identical input). The best iterate is tracked by rotating
+// three iterate buffers instead of copying x_min (:264-267). R independent runs
+// (restarts, :301-312) share one sweep over the matrix as columns of a
+// multi-vector; each column's arithmetic is independent of R.
+//
+// Per-column control state lives on the device; the host only services
+// degenerate-direction restarts (which need the reference's mt19937_64 stream,
+// :199-219) at chunk boundaries.
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "ck_common.h"
+#include "ck_device.cuh"
+#include "ck_internal.h"
+#include "ck_session.h"
+
+namespace ck {
+
+constexpr int kPA = 9;  // per-column partials of k_apply
+constexpr int kPT = 1;  // per-column partials of k_transpose
+
+__device__ __forceinline__ int pick_free(int cur, int best) {
+  for (int b = 0; b < 3; ++b)
+    if (b != cur && b != best) return b;
+  return 0;
+}
+
+// DegenerateDirection handling, condest.hpp:213-219/242-256: spend one unit of
+// the 16-restart budget or stop; the host supplies the re-randomised start.
+__device__ __forceinline__ void on_degenerate(ColState& s, const Params& p) {
+  if (s.budget == 0) {
+    s.phase = PH_DONE;
+    s.converged = 0;
+    return;
+  }
+  s.budget -= 1;
+  s.phase = (s.t >= p.max_iter) ? PH_DONE : PH_WAIT;
+}
+
+__device__ __forceinline__ void begin_iteration(ColState& s, const Params& p) {
+  s.b1p = __dmul_rn(s.b1p, p.beta1);
+  s.b2p = __dmul_rn(s.b2p, p.beta2);
+  s.mc = 1.0 / (1.0 - s.b1p);
+  s.vc = 1.0 / (1.0 - s.b2p);
+}
+
+// Control step after k_apply's reductions (thread 0 of the last CTA).
+__device__ void control_apply(ColState& s, const Params& p, double N, double yn) {
+  s.xnorm = N;
+  s.ynorm = yn;
+  if (s.phase == PH_PRO) {
+    // First iteration after a (re)start: the gradient at x needs ||A x|| != 0.
+    s.t += 1;
+    if (yn == 0.0) {
+      on_degenerate(s, p);
+      return;
+    }
+    begin_iteration(s, p);
+    s.inv_x2 = 1.0 / (N * N);
+    s.inv_y2 = 1.0 / (yn * yn);
+    s.ndiv = 1.0;
+    s.mat = 0;
+    s.phase = PH_GRAD;
+    return;
+  }
+  // PH_APPLY: finish iteration t at x_{t+1} = x~/N.
+  if (N == 0.0 || !isfinite(N)) {
+    on_degenerate(s, p);
+    return;
+  }
+  double den = yn / N;  // ||A x_{t+1}||
+  if (den == 0.0) {
+    on_degenerate(s, p);
+    return;
+  }
+  double loss = -log(den);  // log||x_{t+1}|| - log||A x_{t+1}||, ||x_{t+1}|| = 1
+  s.loss = loss;
+  s.t_loss = s.t;
+  s.n_loss += 1;
+  bool improved = !isfinite(s.loss_min) || s.loss_min - loss > p.rel_tol * fabs(s.loss_min);
+  s.since = improved ? 0 : s.since + 1;
+  s.nxt = pick_free(s.cur, s.best);
+  s.ndiv = N;
+  if (loss < s.loss_min) {
+    s.loss_min = loss;
+    s.best = s.nxt;  // x_{t+1} lands there (k_transpose or the epilogue)
+    s.pend = 1;
+  }
+  if (s.since >= p.patience) {
+    s.phase = PH_DONE;
+    s.converged = 1;
+    return;
+  }
+  if (s.t >= p.max_iter) {
+    s.phase = PH_DONE;
+    return;
+  }
+  s.t += 1;
+  begin_iteration(s, p);
+  s.inv_x2 = 1.0;
+  s.inv_y2 = 1.0 / (den * den);
+  s.mat = 1;
+  s.phase = PH_GRAD;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kTile) k_apply(LoopArgs a) {
+  if (!a.hdr->needA) return;
+  const bool observe = a.hdr->observe != 0;
+  __shared__ double s_h[8], s_l[8];
+  __shared__ int s_e[8], s_f[8];
+  __shared__ double s_res[R][5];
+
+  bool act[R], pro[R];
+  double rad[R];
+  const double* xc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int ph = a.st[r].phase;
+    act[r] = ph == PH_PRO || ph == PH_APPLY;
+    pro[r] = ph == PH_PRO;
+    rad[r] = a.st[r].rad;
+    xc[r] = a.X + ((int64_t)a.st[r].cur * R + r) * a.nc_pad;
+  }
+  DD dd[R];
+  ES es[R], dn[R];
+  double xd[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    dd[r] = dd_zero();
+    es[r] = es_zero();
+    dn[r] = es_zero();
+    xd[r] = 0.0;
+  }
+  const int t0 = blockIdx.x * a.tpu_A;
+  const int t1 = min(t0 + a.tpu_A, a.tiles_A);
+  for (int tile = t0; tile < t1; ++tile) {
+    const int64_t i = (int64_t)tile * kTile + threadIdx.x;
+    if (i < a.nc) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!act[r]) continue;
+        double x = xc[r][i];
+        double xt = x;
+        if (!pro[r]) {
+          double dp = __dsub_rn(a.dl[i * R + r], __dmul_rn(rad[r], x));  // :232
+          xt = __dsub_rn(x, dp);                                          // :240
+          if (observe) {
+            xd[r] = __fma_rn(x, dp, xd[r]);
+            es_add(dn[r], dp);
+          }
+        }
+        dd_add_sq(dd[r], xt);
+      }
+    }
+    if (i < a.nr_pad) {
+      const int64_t base = a.A.sp[i >> 5] + (i & 31);
+      const int L = a.A.len[i];
+      double acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < L; ++j) {
+        const int64_t k = base + (int64_t)j * kSlice;
+        const int c = ld_stream(a.A.col + k);
+        const double v = ld_stream(a.A.val + k);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!act[r]) continue;
+          double x = __ldg(xc[r] + c);
+          double xt = pro[r] ? x
+                             : __dsub_rn(x, __dsub_rn(__ldg(a.dl + (int64_t)c * R + r),
+                                                      __dmul_rn(rad[r], x)));
+          acc[r] = __dadd_rn(acc[r], __dmul_rn(v, xt));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!act[r]) continue;
+        a.y[i * R + r] = acc[r];
+        es_add(es[r], acc[r]);
+      }
+    }
+  }
+  // Per-CTA partials.
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    DD d = block_dd(dd[r], s_h, s_l);
+    ES e = block_es(es[r], s_h, s_e, s_f);
+    double x2 = 0.0;
+    ES e2 = es_zero();
+    if (observe) {
+      x2 = block_sum(xd[r], s_h);
+      e2 = block_es(dn[r], s_h, s_e, s_f);
+    }
+    if (threadIdx.x == 0) {
+      double* p = a.partA + ((int64_t)blockIdx.x * R + r) * kPA;
+      p[0] = d.hi;
+      p[1] = d.lo;
+      p[2] = e.s;
+      p[3] = (double)e.e;
+      p[4] = (double)e.flags;
+      p[5] = x2;
+      p[6] = e2.s;
+      p[7] = (double)e2.e;
+      p[8] = (double)e2.flags;
+    }
+  }
+  if (!elect_last_block(&a.hdr->cntA, (unsigned)a.units_A)) return;
+
+  // Last CTA: fixed-order merge of all partials, then the control step.
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    DD d = dd_zero();
+    ES e = es_zero(), e2 = es_zero();
+    double x2 = 0.0;
+    for (int u = threadIdx.x; u < a.units_A; u += kTile) {
+      const double* p = a.partA + ((int64_t)u * R + r) * kPA;
+      dd_merge(d, DD{__ldcg(p), __ldcg(p + 1)});
+      es_merge(e, ES{__ldcg(p + 2), (int)__ldcg(p + 3), (int)__ldcg(p + 4)});
+      x2 = __dadd_rn(x2, __ldcg(p + 5));
+      es_merge(e2, ES{__ldcg(p + 6), (int)__ldcg(p + 7), (int)__ldcg(p + 8)});
+    }
+    d = block_dd(d, s_h, s_l);
+    e = block_es(e, s_h, s_e, s_f);
+    x2 = block_sum(x2, s_h);
+    e2 = block_es(e2, s_h, s_e, s_f);
+    if (threadIdx.x == 0) {
+      s_res[r][0] = sqrt(__dadd_rn(d.hi, d.lo));
+      s_res[r][1] = es_norm(e);
+      s_res[r][2] = x2;
+      s_res[r][3] = es_norm(e2);
+    }
+  }
+  if (threadIdx.x == 0) {
+    int needT = 0, nwait = 0, ndone = 0;
+    for (int r = 0; r < R; ++r) {
+      ColState s = a.st[r];
+      if (s.phase == PH_PRO || s.phase == PH_APPLY) {
+        if (s.phase == PH_APPLY && observe) {
+          s.obs_xd = s_res[r][2];
+          s.obs_dn = s_res[r][3];
+        }
+        control_apply(s, a.prm, s_res[r][0], s_res[r][1]);
+        a.st[r] = s;
+      }
+      needT |= s.phase == PH_GRAD;
+      nwait += s.phase == PH_WAIT;
+      ndone += s.phase == PH_DONE;
+    }
+    a.hdr->needT = needT;
+    a.hdr->needA = 0;
+    a.hdr->nwait = nwait;
+    a.hdr->ndone = ndone;
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kTile) k_transpose(LoopArgs a) {
+  if (!a.hdr->needT) return;
+  __shared__ double s_h[8];
+  __shared__ double s_res[R];
+  const Params p = a.prm;
+  bool act[R], mat[R];
+  double rad[R], ndiv[R], ix2[R], iy2[R], mc[R], vc[R];
+  const double* xc[R];
+  double* xn_out[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const ColState& s = a.st[r];
+    act[r] = s.phase == PH_GRAD;
+    mat[r] = s.mat != 0;
+    rad[r] = s.rad;
+    ndiv[r] = s.ndiv;
+    ix2[r] = s.inv_x2;
+    iy2[r] = s.inv_y2;
+    mc[r] = s.mc;
+    vc[r] = s.vc;
+    xc[r] = a.X + ((int64_t)s.cur * R + r) * a.nc_pad;
+    xn_out[r] = a.X + ((int64_t)s.nxt * R + r) * a.nc_pad;
+  }
+  const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
+  double dot[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) dot[r] = 0.0;
+  const int t0 = blockIdx.x * a.tpu_T;
+  const int t1 = min(t0 + a.tpu_T, a.tiles_T);
+  for (int tile = t0; tile < t1; ++tile) {
+    const int64_t j = (int64_t)tile * kTile + threadIdx.x;
+    const int64_t base = a.AT.sp[j >> 5] + (j & 31);
+    const int L = a.AT.len[j];
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll 4
+    for (int q = 0; q < L; ++q) {
+      const int64_t k = base + (int64_t)q * kSlice;
+      const int c = ld_stream(a.AT.col + k);
+      const double v = ld_stream(a.AT.val + k);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v, __ldg(a.y + (int64_t)c * R + r)));
+    }
+    if (j < a.nc) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!act[r]) continue;
+        const int64_t e = j * R + r;
+        double xo = xc[r][j];
+        double xn = xo;
+        if (mat[r]) {
+          double dp = __dsub_rn(a.dl[e], __dmul_rn(rad[r], xo));
+          xn = __ddiv_rn(__dsub_rn(xo, dp), ndiv[r]);  // :240-247
+          xn_out[r][j] = xn;
+        }
+        double z = __ddiv_rn(acc[r], ndiv[r]);  // A^T A x_{t+1}
+        double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(z, iy2[r]));  // :105
+        double mm = __dadd_rn(__dmul_rn(p.beta1, a.m[e]), __dmul_rn(om1, g));  // :226
+        double vv = __dadd_rn(__dmul_rn(p.beta2, a.v[e]), __dmul_rn(__dmul_rn(om2, g), g));  // :227
+        double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
+                             __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));  // :228
+        a.m[e] = mm;
+        a.v[e] = vv;
+        a.dl[e] = d;
+        dot[r] = __fma_rn(xn, d, dot[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double s = block_sum(dot[r], s_h);
+    if (threadIdx.x == 0) a.partT[(int64_t)blockIdx.x * R + r] = s;
+  }
+  if (!elect_last_block(&a.hdr->cntT, (unsigned)a.units_T)) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double s = 0.0;
+    for (int u = threadIdx.x; u < a.units_T; u += kTile)
+      s = __dadd_rn(s, __ldcg(a.partT + (int64_t)u * R + r));
+    s = block_sum(s, s_h);
+    if (threadIdx.x == 0) s_res[r] = s;
+  }
+  if (threadIdx.x == 0) {
+    int needA = 0;
+    for (int r = 0; r < R; ++r) {
+      ColState s = a.st[r];
+      if (s.phase == PH_GRAD) {
+        s.rad = s_res[r];
+        if (s.mat) {
+          s.cur = s.nxt;
+          s.pend = 0;
+        }
+        s.phase = PH_APPLY;
+        a.st[r] = s;
+      }
+      needA |= s.phase == PH_APPLY;
+    }
+    a.hdr->needA = needA;
+    a.hdr->needT = 0;
+  }
+}
+
+// x_{t+1} = (x - (delta - r x)) / N into `out` (epilogue materialisation).
+__global__ void k_materialise(int64_t nc, int R, int col, const double* __restrict__ x,
+                              const double* __restrict__ dl, double rad, double ndiv,
+                              double* out) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nc) return;
+  double xo = x[j];
+  double dp = __dsub_rn(dl[j * R + col], __dmul_rn(rad, xo));
+  out[j] = __ddiv_rn(__dsub_rn(xo, dp), ndiv);
+}
+
+__global__ void k_zero_column(int64_t n, int R, int col, double* a, double* b, double* c) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  a[j * R + col] = 0.0;
+  b[j * R + col] = 0.0;
+  c[j * R + col] = 0.0;
+}
+
+}  // namespace ck
+
+namespace ck {
+
+static void launch_step(ck_session_s* s, cudaStream_t st) {
+  const LoopArgs& a = s->args;
+  switch (s->R) {
+    case 1: k_apply<1><<<a.units_A, kTile, 0, st>>>(a); k_transpose<1><<<a.units_T, kTile, 0, st>>>(a); break;
+    case 2: k_apply<2><<<a.units_A, kTile, 0, st>>>(a); k_transpose<2><<<a.units_T, kTile, 0, st>>>(a); break;
+    case 3: k_apply<3><<<a.units_A, kTile, 0, st>>>(a); k_transpose<3><<<a.units_T, kTile, 0, st>>>(a); break;
+    default: k_apply<4><<<a.units_A, kTile, 0, st>>>(a); k_transpose<4><<<a.units_T, kTile, 0, st>>>(a); break;
+  }
+}
+
+static void launch_apply_only(ck_session_s* s, cudaStream_t st) {
+  const LoopArgs& a = s->args;
+  switch (s->R) {
+    case 1: k_apply<1><<<a.units_A, kTile, 0, st>>>(a); break;
+    case 2: k_apply<2><<<a.units_A, kTile, 0, st>>>(a); break;
+    case 3: k_apply<3><<<a.units_A, kTile, 0, st>>>(a); break;
+    default: k_apply<4><<<a.units_A, kTile, 0, st>>>(a); break;
+  }
+}
+
+static void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
+  const LoopArgs& a = s->args;
+  switch (s->R) {
+    case 1: k_transpose<1><<<a.units_T, kTile, 0, st>>>(a); break;
+    case 2: k_transpose<2><<<a.units_T, kTile, 0, st>>>(a); break;
+    case 3: k_transpose<3><<<a.units_T, kTile, 0, st>>>(a); break;
+    default: k_transpose<4><<<a.units_T, kTile, 0, st>>>(a); break;
+  }
+}
+
+static void pull_state(ck_session_s* s) {
+  cudaStream_t st = s->A->stream;
+  CK_CUDA(cudaMemcpyAsync(s->h_st, s->st.p, sizeof(ColState) * s->R, cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaMemcpyAsync(s->h_hdr, s->hdr.p, sizeof(Header), cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+}
+
+static void push_state(ck_session_s* s) {
+  cudaStream_t st = s->A->stream;
+  CK_CUDA(cudaMemcpyAsync(s->st.p, s->h_st, sizeof(ColState) * s->R, cudaMemcpyHostToDevice, st));
+  CK_CUDA(cudaMemcpyAsync(s->hdr.p, s->h_hdr, sizeof(Header), cudaMemcpyHostToDevice, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+}
+
+// Upload a fresh start vector for column c (original order) into buffer b.
+static void load_start(ck_session_s* s, int c, int b, const double* x) {
+  cudaStream_t st = s->A->stream;
+  int64_t nc = s->A->ncols;
+  CK_CUDA(cudaMemcpyAsync(s->tmp.p, x, sizeof(double) * nc, cudaMemcpyHostToDevice, st));
+  double* dst = s->X.p + ((int64_t)b * s->R + c) * s->args.nc_pad;
+  gather_perm(s->A->at.perm.p, s->args.nc_pad, s->tmp.p, dst, st);
+  k_zero_column<<<(unsigned)ceil_div(s->args.nc_pad, 256), 256, 0, st>>>(s->args.nc_pad, s->R, c, s->m.p, s->v.p, s->dl.p);
+  CK_CUDA(cudaGetLastError());
+  CK_CUDA(cudaStreamSynchronize(st));
+}
+
+// restart(), condest.hpp:201-207: the next vector of the column's own stream,
+// m = v = 0, bias powers reset; x_min and the patience counters are kept.
+static void service_restarts(ck_session_s* s) {
+  bool any = false;
+  for (int c = 0; c < s->R; ++c) {
+    ColState& cs = s->h_st[c];
+    if (cs.phase != PH_WAIT) continue;
+    random_unit_vector_host(&s->gens[c], s->A->ncols, s->hx.data());
+    int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
+    load_start(s, c, b, s->hx.data());
+    cs.cur = b;
+    cs.b1p = 1.0;
+    cs.b2p = 1.0;
+    cs.mat = 0;
+    cs.pend = 0;
+    cs.rad = 0.0;
+    cs.phase = PH_PRO;
+    any = true;
+  }
+  if (any) {
+    s->h_hdr->needA = 1;
+    s->h_hdr->nwait = 0;
+    push_state(s);
+  }
+}
+
+static void build_graph(ck_session_s* s, int steps) {
+  cudaStream_t st = s->A->stream;
+  cudaGraph_t g;
+  CK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < steps; ++k) launch_step(s, st);
+  CK_CUDA(cudaStreamEndCapture(st, &g));
+  CK_CUDA(cudaGraphInstantiate(&s->gexec, g, 0));
+  CK_CUDA(cudaGraphDestroy(g));
+  s->gsteps = steps;
+}
+
+void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
+                    const uint64_t* seeds, int R) {
+  if (R < 1 || R > kMaxCols) fail(CK_ERR_INVALID_ARGUMENT, "session columns must be 1..4");
+  if (A->ncols == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
+  s->A = A;
+  s->R = R;
+  s->prm = Params{cfg->alpha, cfg->beta1, cfg->beta2, cfg->eps_stab, cfg->rel_tol, cfg->max_iter,
+                  cfg->patience};
+  LoopArgs& a = s->args;
+  a.A = view(A->a);
+  a.AT = view(A->at);
+  a.nr = A->nrows;
+  a.nc = A->ncols;
+  a.nr_pad = A->a.nrows_pad;
+  a.nc_pad = A->at.nrows_pad;
+  a.tiles_A = (int)(std::max(a.nr_pad, a.nc_pad) / kTile);
+  a.tpu_A = (int)std::max<int64_t>(1, ceil_div(a.tiles_A, kTargetUnits));
+  a.units_A = (int)ceil_div(a.tiles_A, a.tpu_A);
+  a.tiles_T = (int)(a.nc_pad / kTile);
+  a.tpu_T = (int)std::max<int64_t>(1, ceil_div(a.tiles_T, kTargetUnits));
+  a.units_T = (int)ceil_div(a.tiles_T, a.tpu_T);
+  cudaStream_t st = A->stream;
+  s->X.alloc(3 * R * a.nc_pad);
+  s->m.alloc(a.nc_pad * R);
+  s->v.alloc(a.nc_pad * R);
+  s->dl.alloc(a.nc_pad * R);
+  s->y.alloc(std::max(a.nr_pad, a.nc_pad) * R);
+  s->partA.alloc((int64_t)a.units_A * R * kPA);
+  s->partT.alloc((int64_t)a.units_T * R * kPT);
+  s->tmp.alloc(std::max(a.nr_pad, a.nc_pad));
+  s->st.alloc(R);
+  s->hdr.alloc(1);
+  CK_CUDA(cudaMemsetAsync(s->X.p, 0, s->X.bytes(), st));
+  CK_CUDA(cudaMemsetAsync(s->y.p, 0, s->y.bytes(), st));
+  a.X = s->X.p;
+  a.m = s->m.p;
+  a.v = s->v.p;
+  a.dl = s->dl.p;
+  a.y = s->y.p;
+  a.partA = s->partA.p;
+  a.partT = s->partT.p;
+  a.st = s->st.p;
+  a.hdr = s->hdr.p;
+  a.prm = s->prm;
+  CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_st), sizeof(ColState) * R));
+  CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_hdr), sizeof(Header)));
+  s->hx.resize((size_t)A->ncols);
+  s->gens.clear();
+  for (int c = 0; c < R; ++c) {
+    s->gens.emplace_back(seeds[c]);
+    random_unit_vector_host(&s->gens[c], A->ncols, s->hx.data());  // x0, rng.hpp:68-77
+    load_start(s, c, 0, s->hx.data());
+    ColState cs{};
+    cs.phase = cfg->max_iter == 0 ? PH_DONE : PH_PRO;
+    cs.cur = 0;
+    cs.best = 0;  // x_min = x (condest.hpp:194)
+    cs.nxt = 1;
+    cs.budget = 16;
+    cs.b1p = cs.b2p = 1.0;
+    cs.loss_min = INFINITY;
+    cs.loss = NAN;
+    s->h_st[c] = cs;
+  }
+  Header h{};
+  h.needA = cfg->max_iter == 0 ? 0 : 1;
+  h.ncols = R;
+  h.ndone = cfg->max_iter == 0 ? R : 0;
+  *s->h_hdr = h;
+  push_state(s);
+  // chunk length: about 4 ms of work per host round trip, 4..256 steps
+  double bytes_per_step = 24.0 * (double)A->nnz * 1.0 + 100.0 * (double)A->ncols * R;
+  int steps = (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
+  build_graph(s, steps);
+}
+
+void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished) {
+  cudaStream_t st = s->A->stream;
+  uint64_t done = 0;
+  *finished = 0;
+  for (;;) {
+    pull_state(s);
+    if (s->h_hdr->ndone == s->R) {
+      *finished = 1;
+      return;
+    }
+    if (s->h_hdr->nwait > 0) service_restarts(s);
+    if (max_steps && done >= max_steps) return;
+    if (max_steps && max_steps - done < (uint64_t)s->gsteps) {
+      for (uint64_t k = done; k < max_steps; ++k) launch_step(s, st);
+      CK_CUDA(cudaGetLastError());
+      done = max_steps;
+    } else {
+      CK_CUDA(cudaGraphLaunch(s->gexec, st));
+      done += (uint64_t)s->gsteps;
+    }
+  }
+}
+
+void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_total,
+                  double* ms_apply, double* ms_transpose) {
+  cudaStream_t st = s->A->stream;
+  pull_state(s);
+  if (s->h_hdr->nwait > 0) service_restarts(s);
+  if (mode == 1) {  // whole graph chunks, no per-kernel events
+    cudaEvent_t e0, e1;
+    CK_CUDA(cudaEventCreate(&e0));
+    CK_CUDA(cudaEventCreate(&e1));
+    CK_CUDA(cudaStreamSynchronize(st));
+    CK_CUDA(cudaEventRecord(e0, st));
+    uint64_t k = 0;
+    for (; k + (uint64_t)s->gsteps <= steps; k += (uint64_t)s->gsteps) CK_CUDA(cudaGraphLaunch(s->gexec, st));
+    for (; k < steps; ++k) launch_step(s, st);
+    CK_CUDA(cudaEventRecord(e1, st));
+    CK_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_total = ms;
+    *ms_apply = -1.0;
+    *ms_transpose = -1.0;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return;
+  }
+  std::vector<cudaEvent_t> ev(2 * steps + 1);
+  for (auto& e : ev) CK_CUDA(cudaEventCreate(&e));
+  CK_CUDA(cudaStreamSynchronize(st));
+  for (uint64_t k = 0; k < steps; ++k) {
+    CK_CUDA(cudaEventRecord(ev[2 * k], st));
+    launch_apply_only(s, st);
+    CK_CUDA(cudaEventRecord(ev[2 * k + 1], st));
+    launch_transpose_only(s, st);
+  }
+  CK_CUDA(cudaEventRecord(ev[2 * steps], st));
+  CK_CUDA(cudaEventSynchronize(ev[2 * steps]));
+  CK_CUDA(cudaGetLastError());
+  double ta = 0.0, tt = 0.0;
+  for (uint64_t k = 0; k < steps; ++k) {
+    float a = 0.f, b = 0.f;
+    CK_CUDA(cudaEventElapsedTime(&a, ev[2 * k], ev[2 * k + 1]));
+    CK_CUDA(cudaEventElapsedTime(&b, ev[2 * k + 1], ev[2 * k + 2]));
+    ta += a;
+    tt += b;
+  }
+  float tot = 0.f;
+  CK_CUDA(cudaEventElapsedTime(&tot, ev[0], ev[2 * steps]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  *ms_total = tot;
+  *ms_apply = ta;
+  *ms_transpose = tt;
+}
+
+// Final NormEstimate for column c (condest.hpp:278-296).
+void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness) {
+  if (c < 0 || c >= s->R) fail(CK_ERR_INVALID_ARGUMENT, "column out of range");
+  cudaStream_t st = s->A->stream;
+  pull_state(s);
+  ColState& cs = s->h_st[c];
+  const int64_t ncp = s->args.nc_pad;
+  double* best = s->X.p + ((int64_t)cs.best * s->R + c) * ncp;
+  if (cs.pend) {  // x_{t+1} became the best but was never materialised
+    const double* cur = s->X.p + ((int64_t)cs.cur * s->R + c) * ncp;
+    k_materialise<<<(unsigned)ceil_div(ncp, 256), 256, 0, st>>>(s->A->ncols > 0 ? ncp : 0, s->R, c, cur, s->dl.p, cs.rad, cs.ndiv, best);
+    CK_CUDA(cudaGetLastError());
+    cs.pend = 0;
+    cs.cur = cs.best;
+    push_state(s);
+  }
+  res->iterations = cs.t;
+  res->converged = cs.converged;
+  res->_pad = 0;
+  if (std::isfinite(cs.loss_min)) {
+    res->value = std::exp(-cs.loss_min);
+    // witness re-check, condest.hpp:284-289
+    matrix_apply_perm(s->A, best, s->tmp.p, st);
+    double chk = device_norm(s->tmp.p, s->A->a.nrows_pad, s->A->s_red.p, st);
+    if (!(std::fabs(chk - res->value) <= 1e-12 * std::max(res->value, chk)))
+      fail(CK_ERR_LOGIC, "norm estimate does not match ||Op witness||");
+  } else {
+    res->value = 0.0;
+    res->converged = 0;
+  }
+  if (witness) {
+    scatter_perm(s->A->at.perm.p, ncp, best, s->tmp.p, st);
+    CK_CUDA(cudaMemcpyAsync(witness, s->tmp.p, sizeof(double) * s->A->ncols, cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
+// Observer mode (AdamObserver, condest.hpp:234-238, 268-271) for column 0:
+// advances until column 0 evaluates a loss (or finishes) and reports the
+// iteration's scalars and, optionally, x_{t+1} and x_min.
+void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, double* x_min) {
+  cudaStream_t st = s->A->stream;
+  pull_state(s);
+  if (!s->observe_on) {
+    s->h_hdr->observe = 1;
+    push_state(s);
+    s->observe_on = true;
+  }
+  uint64_t n0 = s->h_st[0].n_loss;
+  std::memset(info, 0, sizeof(*info));
+  for (;;) {
+    if (s->h_st[0].phase == PH_DONE) {
+      info->phase = 2;
+      info->t = s->h_st[0].t;
+      info->loss_min = s->h_st[0].loss_min;
+      return;
+    }
+    if (s->h_hdr->nwait > 0) service_restarts(s);
+    launch_apply_only(s, st);
+    CK_CUDA(cudaGetLastError());
+    pull_state(s);
+    bool reported = s->h_st[0].n_loss != n0;
+    ColState cs = s->h_st[0];
+    // k_transpose materialises x_{t+1}; when the column just finished it
+    // does not run, so materialise into scratch instead.
+    const int64_t ncp = s->args.nc_pad;
+    const double* xnext = nullptr;
+    if (reported && cs.phase == PH_DONE) {
+      const double* cur = s->X.p + ((int64_t)cs.cur * s->R) * ncp;
+      k_materialise<<<(unsigned)ceil_div(ncp, 256), 256, 0, st>>>(s->A->ncols, s->R, 0, cur, s->dl.p, cs.rad, cs.ndiv, s->tmp.p);
+      xnext = s->tmp.p;
+    }
+    launch_transpose_only(s, st);
+    CK_CUDA(cudaGetLastError());
+    pull_state(s);
+    if (!reported) continue;
+    cs = s->h_st[0];
+    info->t = cs.t_loss;
+    info->loss = cs.loss;
+    info->loss_min = cs.loss_min;
+    info->x_dot_delta = cs.obs_xd;
+    info->delta_norm = cs.obs_dn;
+    info->phase = 0;
+    if (!xnext) xnext = s->X.p + ((int64_t)cs.cur * s->R) * ncp;
+    const double* xm = cs.pend ? xnext : s->X.p + ((int64_t)cs.best * s->R) * ncp;
+    std::vector<double> tmp2;
+    if (x) {
+      scatter_perm(s->A->at.perm.p, ncp, xnext, s->A->s_out.p, st);
+      CK_CUDA(cudaMemcpyAsync(x, s->A->s_out.p, sizeof(double) * s->A->ncols, cudaMemcpyDeviceToHost, st));
+      CK_CUDA(cudaStreamSynchronize(st));
+    }
+    if (x_min) {
+      scatter_perm(s->A->at.perm.p, ncp, xm, s->A->s_out.p, st);
+      CK_CUDA(cudaMemcpyAsync(x_min, s->A->s_out.p, sizeof(double) * s->A->ncols, cudaMemcpyDeviceToHost, st));
+      CK_CUDA(cudaStreamSynchronize(st));
+    }
+    return;
+  }
+}
+
+}  // namespace ck

@@ -1,0 +1,432 @@
+// C ABI (include/condkit_b200.h): argument checking, exception -> status
+// mapping, the host RNG mirror, the scalar error-bound formulas and the
+// estimate_norm orchestration over device sessions.
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ck_common.h"
+#include "ck_internal.h"
+#include "ck_session.h"
+
+namespace ck {
+void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
+                    const uint64_t* seeds, int R);
+void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished);
+void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_total,
+                  double* ms_apply, double* ms_transpose);
+void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness);
+void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, double* x_min);
+
+static thread_local std::string g_last_error;
+
+void fail(ck_status c, const std::string& msg) { throw Error(c, msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  std::string m = std::string(what) + " failed: " + cudaGetErrorString(e) + " (" + file + ":" +
+                  std::to_string(line) + ")";
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) throw Error(CK_ERR_NO_DEVICE, m);
+  if (e == cudaErrorMemoryAllocation) throw Error(CK_ERR_OUT_OF_MEMORY, m);
+  throw Error(CK_ERR_CUDA, m);
+}
+
+template <class F>
+static ck_status guarded(F&& f) {
+  try {
+    f();
+    return CK_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return CK_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CK_ERR_LOGIC;
+  }
+}
+
+// sparse.hpp:175-186, sequential so the result is bit-identical.
+static double two_norm_seq(const double* v, int64_t n) {
+  double amax = 0.0;
+  for (int64_t i = 0; i < n; ++i) amax = std::max(amax, std::abs(v[i]));
+  if (amax == 0.0) return 0.0;
+  if (!std::isfinite(amax)) return amax;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double q = v[i] / amax;
+    s += q * q;
+  }
+  return amax * std::sqrt(s);
+}
+
+template <class F>
+static void parallel_for(int64_t n, F&& f) {
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  int64_t nt = n < (int64_t(1) << 18) ? 1 : std::min<int64_t>(hw, 64);
+  if (nt <= 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  int64_t chunk = ceil_div(n, nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    int64_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b >= e) break;
+    pool.emplace_back([&f, b, e] { f(b, e); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// random_unit_vector (rng.hpp:68-77) with standard_normal (rng.hpp:61-65) and
+// uniform01 (rng.hpp:31-33): the engine draws stay sequential (they define the
+// stream); the Box-Muller transform and the final scaling are elementwise and
+// run on all host threads; the norm is sequential as in the reference.
+void random_unit_vector_host(void* engine, int64_t n, double* out) {
+  auto& g = *static_cast<std::mt19937_64*>(engine);
+  std::vector<uint64_t> draws((size_t)(2 * n));
+  double nrm = 0.0;
+  while (nrm == 0.0) {
+    for (auto& d : draws) d = g();
+    parallel_for(n, [&](int64_t b, int64_t e) {
+      for (int64_t i = b; i < e; ++i) {
+        double u1 = 1.0 - static_cast<double>(draws[2 * i] >> 11) * 0x1.0p-53;
+        double u2 = static_cast<double>(draws[2 * i + 1] >> 11) * 0x1.0p-53;
+        out[i] = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+      }
+    });
+    nrm = two_norm_seq(out, n);
+  }
+  parallel_for(n, [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i) out[i] /= nrm;
+  });
+}
+
+static void check_cfg(const ck_adam_cfg* cfg) {
+  if (cfg == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "cfg is NULL");
+}
+
+static ck_matrix_s* M(ck_matrix a) {
+  if (a == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "matrix handle is NULL");
+  CK_CUDA(cudaSetDevice(a->device));
+  return a;
+}
+
+}  // namespace ck
+
+using namespace ck;
+
+extern "C" {
+
+const char* ck_last_error(void) { return g_last_error.c_str(); }
+
+int32_t ck_abi_version(void) { return 1; }
+
+ck_status ck_device_count(int32_t* count) {
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+      cudaGetLastError();
+      n = 0;
+    } else {
+      CK_CUDA(e);
+    }
+    *count = n;
+  });
+}
+
+ck_status ck_set_device(int32_t device) {
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail(CK_ERR_NO_DEVICE, "no CUDA device visible");
+    }
+    cudaDeviceProp p{};
+    CK_CUDA(cudaGetDeviceProperties(&p, device));
+    if (p.major != 10) fail(CK_ERR_NO_DEVICE, std::string("device is not sm_100: ") + p.name);
+    CK_CUDA(cudaSetDevice(device));
+  });
+}
+
+ck_status ck_device_synchronize(void) {
+  return guarded([&] { CK_CUDA(cudaDeviceSynchronize()); });
+}
+
+ck_status ck_host_register(void* ptr, uint64_t bytes) {
+  return guarded([&] {
+    if (bytes == 0) return;
+    CK_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  });
+}
+
+ck_status ck_host_unregister(void* ptr) {
+  return guarded([&] { CK_CUDA(cudaHostUnregister(ptr)); });
+}
+
+void ck_adam_default(ck_adam_cfg* c) {
+  c->alpha = 0.05;
+  c->beta1 = 0.9;
+  c->beta2 = 0.999;
+  c->eps_stab = 1e-8;
+  c->max_iter = 2000;
+  c->seed = 1;
+  c->rel_tol = 1e-12;
+  c->patience = 100;
+}
+
+uint64_t ck_mix_seed(uint64_t base, uint64_t stream) {
+  uint64_t z = base + 0x9E3779B97F4A7C15ull * (stream + 1);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+ck_status ck_random_unit_vectors(uint64_t seed, int64_t n, int64_t count, double* out) {
+  return guarded([&] {
+    if (n < 0 || count < 0) fail(CK_ERR_INVALID_ARGUMENT, "negative size");
+    std::mt19937_64 g(seed);
+    for (int64_t c = 0; c < count; ++c) random_unit_vector_host(&g, n, out + c * n);
+  });
+}
+
+// ---------------------------------------------- error_bounds.hpp:59-99
+ck_status ck_loose_bounds(double rn, double bn, double kappa, double* lo, double* hi) {
+  return guarded([&] {
+    if (!(rn >= 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "residual norm must be >= 0");
+    if (!(kappa >= 1.0)) fail(CK_ERR_INVALID_ARGUMENT, "kappa must be >= 1");
+    if (bn == 0.0) fail(CK_ERR_ZERO_RHS, "right-hand side has zero norm");
+    if (!(bn > 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "b norm must be >= 0");
+    double rho = rn / bn;
+    if (rho == 0.0) {
+      *lo = 0.0;
+      *hi = 0.0;
+      return;
+    }
+    *lo = rho / kappa;
+    *hi = kappa * rho;
+  });
+}
+
+ck_status ck_tight_bounds(double rn, double an, double xn, double kappa, double* lo, double* hi) {
+  return guarded([&] {
+    if (!(rn >= 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "residual norm must be >= 0");
+    if (!(kappa >= 1.0)) fail(CK_ERR_INVALID_ARGUMENT, "kappa must be >= 1");
+    if (xn == 0.0) fail(CK_ERR_ZERO_SOLUTION, "candidate solution has zero norm");
+    if (!(xn > 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "solution norm must be >= 0");
+    if (!(an > 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "operator norm must be > 0");
+    double rho = rn / (an * xn);
+    if (rho == 0.0) {
+      *lo = 0.0;
+      *hi = 0.0;
+      return;
+    }
+    *lo = rho;
+    *hi = kappa * rho;
+  });
+}
+
+ck_status ck_propagate_bound(double e, double* out) {
+  return guarded([&] {
+    if (!(e >= 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "bound must be >= 0");
+    *out = e >= 1.0 ? std::numeric_limits<double>::infinity() : e / (1.0 - e);
+  });
+}
+
+ck_status ck_singularity_bound(double kappa, double eps, double* out) {
+  return guarded([&] {
+    if (!(kappa >= 1.0)) fail(CK_ERR_INVALID_ARGUMENT, "kappa must be >= 1");
+    if (!(eps > 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "eps_mach must be > 0");
+    double ke = kappa * eps;
+    *out = ke >= 1.0 ? std::numeric_limits<double>::infinity() : 2.0 * ke / (1.0 - ke);
+  });
+}
+
+// ---------------------------------------------------------- operator
+ck_status ck_matrix_upload(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
+                           const double* va, ck_matrix* out) {
+  return guarded([&] {
+    if (out == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "out is NULL");
+    auto* m = new ck_matrix_s();
+    try {
+      matrix_upload(m, nrows, ncols, rp, ci, va);
+    } catch (...) {
+      if (m->stream) cudaStreamDestroy(m->stream);
+      delete m;
+      throw;
+    }
+    *out = m;
+  });
+}
+
+ck_status ck_matrix_free(ck_matrix a) {
+  return guarded([&] {
+    if (!a) return;
+    cudaSetDevice(a->device);
+    cudaStreamSynchronize(a->stream);
+    cudaStream_t s = a->stream;
+    delete a;
+    if (s) cudaStreamDestroy(s);
+  });
+}
+
+ck_status ck_matrix_get_info(ck_matrix a, ck_matrix_info* info) {
+  return guarded([&] {
+    M(a);
+    info->nrows = a->nrows;
+    info->ncols = a->ncols;
+    info->nnz = a->nnz;
+    info->sell_entries_a = a->a.entries;
+    info->sell_entries_at = a->at.entries;
+    auto sb = [](const Sell& s) {
+      return s.slice_ptr.bytes() + s.len.bytes() + s.col.bytes() + s.val.bytes() + s.perm.bytes() +
+             s.inv.bytes();
+    };
+    info->device_bytes = sb(a->a) + sb(a->at);
+    info->device = a->device;
+    info->_pad = 0;
+  });
+}
+
+ck_status ck_spmv(ck_matrix a, const double* x, double* y) {
+  return guarded([&] { matrix_apply_host(M(a), false, x, y); });
+}
+
+ck_status ck_spmv_t(ck_matrix a, const double* x, double* y) {
+  return guarded([&] { matrix_apply_host(M(a), true, x, y); });
+}
+
+ck_status ck_residual_norms(ck_matrix a, const double* x, const double* b, double* rn, double* xn,
+                            double* bn) {
+  return guarded([&] { residual_norms(M(a), x, b, rn, xn, bn); });
+}
+
+ck_status ck_loss_explicit(ck_matrix a, const double* x, double* loss) {
+  return guarded([&] {
+    bool deg = false;
+    double l = loss_explicit_dev(M(a), x, &deg);
+    if (deg) fail(CK_ERR_INVALID_ARGUMENT, "operator maps direction to zero (DegenerateDirection)");
+    *loss = l;
+  });
+}
+
+ck_status ck_grad_explicit(ck_matrix a, const double* x, double* g) {
+  return guarded([&] {
+    bool deg = false;
+    grad_explicit_dev(M(a), x, g, &deg);
+    if (deg) fail(CK_ERR_INVALID_ARGUMENT, "operator maps direction to zero (DegenerateDirection)");
+  });
+}
+
+// ------------------------------------------------------ sessions
+ck_status ck_session_create(ck_matrix a, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                            int32_t ncols, ck_session* out) {
+  return guarded([&] {
+    check_cfg(cfg);
+    auto* s = new ck_session_s();
+    try {
+      session_create(s, M(a), cfg, seeds, ncols);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+ck_status ck_session_run(ck_session s, uint64_t max_steps, int32_t* finished) {
+  return guarded([&] {
+    M(s->A);
+    session_run(s, max_steps, finished);
+  });
+}
+
+ck_status ck_session_step_observed(ck_session s, ck_step_info* info, double* x, double* x_min) {
+  return guarded([&] {
+    M(s->A);
+    if (s->R != 1) fail(CK_ERR_INVALID_ARGUMENT, "observer mode needs a single-column session");
+    session_step_observed(s, info, x, x_min);
+  });
+}
+
+ck_status ck_session_time(ck_session s, uint64_t steps, int32_t mode, double* ms_total,
+                          double* ms_apply, double* ms_transpose) {
+  return guarded([&] {
+    M(s->A);
+    session_time(s, steps, mode, ms_total, ms_apply, ms_transpose);
+  });
+}
+
+ck_status ck_session_result(ck_session s, int32_t column, ck_norm_result* res, double* witness) {
+  return guarded([&] {
+    M(s->A);
+    session_result(s, column, res, witness);
+  });
+}
+
+ck_status ck_session_free(ck_session s) {
+  return guarded([&] {
+    if (!s) return;
+    cudaSetDevice(s->A->device);
+    cudaStreamSynchronize(s->A->stream);
+    delete s;
+  });
+}
+
+// projected_adam / norm2, condest.hpp:184-297, 315-317
+ck_status ck_projected_adam(ck_matrix a, const ck_adam_cfg* cfg, ck_norm_result* res,
+                            double* witness) {
+  return guarded([&] {
+    check_cfg(cfg);
+    ck_session_s s;
+    uint64_t seed = cfg->seed;
+    session_create(&s, M(a), cfg, &seed, 1);
+    int32_t fin = 0;
+    session_run(&s, 0, &fin);
+    session_result(&s, 0, res, witness);
+  });
+}
+
+// estimate_norm, condest.hpp:301-312: restart r uses seed cfg.seed (r = 0) or
+// mix_seed(cfg.seed, r); the first strictly larger value wins. Up to four
+// restarts share each device sweep.
+ck_status ck_estimate_norm(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts,
+                           ck_norm_result* res, double* witness) {
+  return guarded([&] {
+    check_cfg(cfg);
+    if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
+    M(a);
+    bool have = false;
+    for (uint64_t r0 = 0; r0 < restarts; r0 += kMaxCols) {
+      int R = (int)std::min<uint64_t>(kMaxCols, restarts - r0);
+      std::vector<uint64_t> seeds(R);
+      for (int c = 0; c < R; ++c) {
+        uint64_t r = r0 + c;
+        seeds[c] = r == 0 ? cfg->seed : ck_mix_seed(cfg->seed, r);
+      }
+      ck_session_s s;
+      session_create(&s, a, cfg, seeds.data(), R);
+      int32_t fin = 0;
+      session_run(&s, 0, &fin);
+      for (int c = 0; c < R; ++c) {
+        ck_norm_result e{};
+        session_result(&s, c, &e, nullptr);
+        if (!have || e.value > res->value) {
+          *res = e;
+          have = true;
+          if (witness) session_result(&s, c, &e, witness);
+        }
+      }
+    }
+  });
+}
+
+}  // extern "C"

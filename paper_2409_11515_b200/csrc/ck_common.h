@@ -1,0 +1,108 @@
+// Internal definitions shared by the condkit-b200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "condkit_b200.h"
+
+namespace ck {
+
+// Rows handled by one CTA (one thread per row) and rows per sliced-ELL slice.
+constexpr int kTile = 256;
+constexpr int kSlice = 32;
+constexpr int kSlicesPerTile = kTile / kSlice;
+// Target number of work units (CTAs) per kernel: 148 SMs x 8 resident CTAs.
+// Fixed (not queried) so the reduction tree -- and hence every result bit --
+// is identical on every device.
+constexpr int kTargetUnits = 148 * 8;
+constexpr int kMaxCols = 4;  // restarts carried as columns of one multi-vector
+
+// Error carrying a ck_status across the C++ implementation; converted at the ABI.
+struct Error : std::runtime_error {
+  ck_status code;
+  Error(ck_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(ck_status c, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define CK_CUDA(x) ::ck::cuda_check((x), #x, __FILE__, __LINE__)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Device buffer with RAII.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  DBuf() = default;
+  explicit DBuf(int64_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    reset();
+    p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  ~DBuf() { reset(); }
+  void alloc(int64_t count) {
+    reset();
+    n = count;
+    if (count > 0) {
+      cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count));
+      if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        fail(CK_ERR_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(sizeof(T) * count) + " bytes failed");
+      }
+      CK_CUDA(e);
+    }
+  }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  int64_t bytes() const { return n * static_cast<int64_t>(sizeof(T)); }
+};
+
+// Sliced-ELL (SELL-32-256) layout of a sparse operator. Rows are permuted
+// inside each 256-row tile by descending length (stable), so every 32-row slice
+// is nearly uniform; slice s stores entry j of its lane-th row at
+// slice_ptr[s] + 32*j + lane, which makes each warp load one contiguous
+// 256-byte run of values and a 128-byte run of column indices.
+struct Sell {
+  int64_t nrows = 0;      // logical rows
+  int64_t nrows_pad = 0;  // multiple of kTile
+  int64_t entries = 0;    // stored entries including slice padding
+  DBuf<int64_t> slice_ptr;  // nrows_pad/32 + 1
+  DBuf<uint16_t> len;       // per permuted row
+  DBuf<int32_t> col;        // column index in the permuted column space
+  DBuf<double> val;
+  DBuf<int32_t> perm;       // perm[k] = original row at permuted position k (-1 = pad)
+  DBuf<int32_t> inv;        // inv[row] = permuted position
+};
+
+struct SellView {
+  const int64_t* __restrict__ sp;
+  const uint16_t* __restrict__ len;
+  const int32_t* __restrict__ col;
+  const double* __restrict__ val;
+};
+
+inline SellView view(const Sell& s) { return {s.slice_ptr.p, s.len.p, s.col.p, s.val.p}; }
+
+}  // namespace ck
+
+struct ck_matrix_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  ck::Sell a;   // rows of A in P order, columns in Q space
+  ck::Sell at;  // rows of A^T (= columns of A) in Q order, columns in P space
+  // scratch for the standalone ops
+  ck::DBuf<double> s_in, s_out, s_perm_in, s_perm_out, s_red;
+};

@@ -1,0 +1,32 @@
+// Cross-translation-unit internals (host side).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ck_common.h"
+
+namespace ck {
+
+constexpr int kNormParts = 296;  // partial blocks of the standalone norm (2 x 148 SMs)
+
+void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* rp,
+                   const int32_t* ci, const double* va);
+void matrix_apply_host(ck_matrix_s* m, bool transpose, const double* x, double* y);
+void matrix_apply_perm(ck_matrix_s* m, const double* x_perm, double* y_perm, cudaStream_t st);
+void gather_perm(const int32_t* perm, int64_t n_out, const double* in, double* out,
+                 cudaStream_t st);
+void scatter_perm(const int32_t* perm, int64_t n_in, const double* in, double* out,
+                  cudaStream_t st);
+double device_norm(const double* v, int64_t n, double* scratch, cudaStream_t st);
+void residual_norms(ck_matrix_s* m, const double* x, const double* b, double* rn, double* xn,
+                    double* bn);
+double loss_explicit_dev(ck_matrix_s* m, const double* x, bool* degenerate);
+void grad_explicit_dev(ck_matrix_s* m, const double* x, double* g, bool* degenerate);
+
+// Host mirror of random_unit_vector (rng.hpp:68-77) on a caller-owned engine
+// state; bit-identical to the reference, Box-Muller transform multithreaded.
+struct Mt64;
+void random_unit_vector_host(void* engine /* std::mt19937_64* */, int64_t n, double* out);
+
+}  // namespace ck

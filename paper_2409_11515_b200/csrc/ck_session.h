@@ -1,0 +1,84 @@
+// Session state of the device-resident Projected-Adam loop (shared between
+// ck_adam.cu, which owns the kernels, and ck_api.cu, which owns the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <random>
+#include <vector>
+
+#include "ck_common.h"
+
+namespace ck {
+
+enum Phase : int32_t { PH_PRO = 0, PH_GRAD = 1, PH_APPLY = 2, PH_WAIT = 3, PH_DONE = 4 };
+
+struct ColState {
+  int32_t phase, cur, nxt, best;
+  int32_t pend, mat, converged, budget;
+  uint64_t t, since, t_loss, n_loss;
+  double b1p, b2p, mc, vc;
+  double rad, ndiv, inv_x2, inv_y2;
+  double loss_min, loss, xnorm, ynorm;
+  double obs_xd, obs_dn;
+};
+
+struct Header {
+  int32_t needA, needT, nwait, ndone;
+  uint32_t cntA, cntT;
+  int32_t observe, ncols;
+};
+
+struct Params {
+  double alpha, beta1, beta2, eps, rel_tol;
+  uint64_t max_iter, patience;
+};
+
+struct LoopArgs {
+  SellView A, AT;
+  int64_t nr, nc, nr_pad, nc_pad;
+  int tiles_A, tpu_A, units_A;
+  int tiles_T, tpu_T, units_T;
+  double* X;   // [3][R][nc_pad] iterate buffers
+  double* m;   // [nc_pad][R]
+  double* v;   // [nc_pad][R]
+  double* dl;  // [nc_pad][R]  delta (pre-projection)
+  double* y;   // [nr_pad][R]  A x~
+  double* partA;
+  double* partT;
+  ColState* st;
+  Header* hdr;
+  Params prm;
+};
+
+}  // namespace ck
+
+struct ck_session_s {
+  using ColState = ck::ColState;
+  using Header = ck::Header;
+  using Params = ck::Params;
+  using LoopArgs = ck::LoopArgs;
+  template <class T>
+  using DBuf = ck::DBuf<T>;
+  ck_matrix_s* A = nullptr;
+  int R = 1;
+  Params prm{};
+  LoopArgs args{};
+  DBuf<double> X, m, v, dl, y, partA, partT, tmp;
+  DBuf<ColState> st;
+  DBuf<Header> hdr;
+  std::vector<std::mt19937_64> gens;
+  ColState* h_st = nullptr;
+  Header* h_hdr = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int gsteps = 0;
+  std::vector<double> hx;
+  bool observe_on = false;
+
+  ~ck_session_s() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (h_st) cudaFreeHost(h_st);
+    if (h_hdr) cudaFreeHost(h_hdr);
+  }
+};
+

@@ -1,0 +1,99 @@
+"""SpMV parity through the C-ABI against the oracle (bit-exact: the device sums
+each row in stored order with unfused multiply/add, exactly matvec /
+transpose_matvec, sparse.hpp:212-242)."""
+import numpy as np
+import pytest
+
+import matrices as M
+import paper_2409_11515_b200 as ck
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(port):
+    yield "random20", M.random_sparse(port, 20, 0.3, 11)
+    yield "random100", M.random_sparse(port, 100, 0.1, 12)
+    yield "laplacian_rowscaled", M.row_scaled(M.laplacian2d(33), port, 1)
+    yield "identity", ck.SparseMatrix.identity(7)
+    rng = np.random.default_rng(5)
+    # ragged rows incl. empty rows and one long row, rectangular
+    r, c = [], []
+    for i in range(700):
+        k = 0 if i % 17 == 0 else (300 if i == 5 else rng.integers(1, 12))
+        cols = np.sort(rng.choice(1000, size=k, replace=False))
+        r += [i] * k
+        c += list(cols)
+    yield "ragged_rect", ck.SparseMatrix.from_coo(700, 1000, r, c, rng.standard_normal(len(r)))
+    yield "empty", ck.SparseMatrix.from_triplets(5, 3, [])
+
+
+def test_matvec_bitwise(port):
+    for name, a in _cases(port):
+        x = port.random_unit_vectors(3, a.ncols)[0] if a.ncols else np.zeros(0)
+        y = ck.matvec(a, x)
+        assert np.array_equal(y, port.matvec(a, x)), name
+        u = port.random_unit_vectors(4, a.nrows)[0] if a.nrows else np.zeros(0)
+        z = ck.transpose_matvec(a, u)
+        assert np.array_equal(z, port.transpose_matvec(a, u)), name
+
+
+def test_matvec_matches_dense_and_adjoint(port):
+    # test_sparse.cpp:57-84
+    for seed in (11, 12, 13):
+        a = M.random_sparse(port, 20, 0.3, seed)
+        d = a.to_dense()
+        x = port.random_unit_vectors(seed + 100, 20)[0]
+        assert np.allclose(ck.matvec(a, x), d @ x, atol=1e-13, rtol=0)
+        assert np.allclose(ck.transpose_matvec(a, x), d.T @ x, atol=1e-13, rtol=0)
+    a = M.random_sparse(port, 20, 0.25, 7)
+    xs = port.random_unit_vectors(99, 20, 20)
+    for k in range(10):
+        x, y = xs[2 * k], xs[2 * k + 1]
+        assert abs(y @ ck.matvec(a, x) - x @ ck.transpose_matvec(a, y)) <= 1e-13
+
+
+def test_basis_vectors_reproduce_columns(port):
+    # test_sparse.cpp:86-94
+    a = M.random_sparse(port, 10, 0.4, 3)
+    for j in range(10):
+        e = np.zeros(10)
+        e[j] = 1.0
+        col = ck.matvec(a, e)
+        for i in range(10):
+            assert col[i] == a.coeff(i, j)
+
+
+def test_dimension_mismatch():
+    a = ck.SparseMatrix.identity(3)
+    with pytest.raises(ck.DimensionMismatch):
+        ck.matvec(a, [1.0, 2.0])
+    with pytest.raises(ck.DimensionMismatch):
+        ck.transpose_matvec(a, [1.0, 2.0])
+
+
+def test_device_validation_rejects_bad_csr():
+    # bypass host validation: the device check must still catch it
+    bad = ck.SparseMatrix(2, 2, [0, 2, 3], [1, 0, 1], [1.0, 2.0, 3.0], validate=False)
+    with pytest.raises(ck.DimensionMismatch):
+        bad.device()
+
+
+def test_residual_norms(port):
+    a = M.random_sparse(port, 50, 0.2, 9)
+    x = port.uniform_in(70, 50, -1.0, 1.0)
+    b = port.matvec(a, x) + 1e-3
+    rn, xn, bn = a.device().residual_norms(x, b)
+    r = port.matvec(a, x) - b
+    assert rn == pytest.approx(port.two_norm(r), rel=1e-14)
+    assert xn == pytest.approx(port.two_norm(x), rel=1e-15)
+    assert bn == pytest.approx(port.two_norm(b), rel=1e-15)
+
+
+def test_norm_overflow_safety():
+    # two_norm overflow safety (test_sparse.cpp:49-54) on the device reduction
+    a = ck.SparseMatrix.identity(25)
+    x = np.full(25, 1e300)
+    rn, xn, bn = a.device().residual_norms(x, np.full(25, 3e300))
+    assert xn == pytest.approx(5e300, rel=1e-15)
+    assert bn == pytest.approx(15e300, rel=1e-15)
+    assert rn == pytest.approx(10e300, rel=1e-15)
