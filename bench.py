@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark: Projected-Adam iterations/s on BASELINE config 4 (6-field
+hydro-mechanical operator, 2048^2 cells, n = 25.2M, ~20 nnz/row), sigma_max
+path (ExplicitOracle), fp64, on 1..N B200s.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints one
+JSON line on rank 0. A step is one Projected-Adam loop trip (condest.hpp:210-276)
+over the whole matrix: k_apply + k_transpose, all state HBM-resident.
+``value`` = total iterations/s over all ranks (each rank runs an independent
+restart stream of the same workload: weak scaling, no data-path collective).
+
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref: the unmodified condkit headers) on this box's host cores on the
+same workload, metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Projected-Adam iters/s and effective SpMV HBM GB/s vs roofline, 1/2/4/8 B200"
+UNIT = "iters/s"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for nm, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_workload(cfg_id: int, grid: int | None):
+    from paper_2409_11515_b200 import configs
+    c = configs.CONFIGS[cfg_id]
+    a = configs.generate(c["kind"], grid or c["grid"], 1, c["param"])
+    name = c["name"] if grid is None else f"{c['name']}@grid{grid}"
+    return a, name
+
+
+def bytes_per_iteration(nnz: int, n: int):
+    # algorithmic bytes of the two fused sweeps (fp64 values,
+    # int32 indices): k_apply reads A (12 B/nnz), x and delta (16 B/row) and writes
+    # y (8); k_transpose reads A^T (12 B/nnz), y (8), x m v delta (32) and writes
+    # x m v delta (32). Total 24 nnz + 96 n (SURVEY.md 8d B_iter).
+    return 12 * nnz + 24 * n, 12 * nnz + 72 * n
+
+
+def cpu_reference(a, steps_hint: int, threads: int, iters: int):
+    import pyoracle  # noqa: PLC0415  (bench CPU arm only)
+    from paper_2409_11515_b200 import configs  # noqa: PLC0415
+    which = "ref" if pyoracle.available("ref") else "port"
+    o = pyoracle.Oracle(which)
+    cfg = configs.baseline_adam(1, max_iter=iters)
+    if which == "ref":
+        rate, timed, span = o.time_iterations(a, cfg, threads, iters)
+        return dict(value=rate, cores=threads, kind="reference", timed_iterations=timed,
+                    span_s=span)
+    t0 = time.perf_counter()
+    e = o.projected_adam_explicit(a, cfg)
+    dt = time.perf_counter() - t0
+    return dict(value=e.iterations / dt, cores=1, kind="port", timed_iterations=e.iterations,
+                span_s=dt)
+
+
+def host_threads_budget(a) -> int:
+    ncpu = os.cpu_count() or 1
+    try:
+        with open("/proc/meminfo") as f:
+            avail_kb = next(int(l.split()[1]) for l in f if l.startswith("MemAvailable"))
+    except (OSError, StopIteration):
+        avail_kb = 64 << 20
+    # reference copy of the matrix (16 B/nnz + 8 B/row) once + ~10 n-vectors per run
+    shared = 16 * a.nnz + 8 * a.nrows
+    per_run = 10 * 8 * a.ncols
+    fit = int(max(1, (avail_kb * 1024 * 0.6 - shared) // per_run))
+    return max(1, min(ncpu, fit, 64))
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    a, name = make_workload(args.config, args.grid)
+    threads = args.cpu_threads or host_threads_budget(a)
+    iters = args.cpu_iters
+    res = cpu_reference(a, args.steps, threads, iters)
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * res["cores"] / res["value"] if res["value"] else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, DESIGN.md section 3)", "impl": "reference",
+        "config": {"workload": name, "n": a.nrows, "nnz": a.nnz, "path": "sigma_max",
+                   "adam": "alpha=1e-2,beta1=.9,beta2=.999,eps=1e-8"},
+        "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["cores"],
+                         "kind": res["kind"],
+                         "sample": f"{res['cores']} concurrent reference runs x {iters} "
+                                   f"iterations each; steady-state rate between first and last "
+                                   f"iteration ({res['timed_iterations']} iterations timed)"},
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    os.environ.setdefault("CK_DEVICE", str(local))
+    import paper_2409_11515_b200 as ck  # noqa: PLC0415
+    from paper_2409_11515_b200 import _lib, configs  # noqa: PLC0415
+    _lib.ensure_device()
+    dist = None
+    if world > 1:
+        import torch  # noqa: PLC0415
+        import torch.distributed as td  # noqa: PLC0415
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = (torch, td)
+
+    def barrier():
+        if dist:
+            dist[1].barrier()
+
+    def allmax(v: float) -> float:
+        if not dist:
+            return v
+        t = dist[0].tensor([v], dtype=dist[0].float64, device="cuda")
+        dist[1].all_reduce(t, op=dist[1].ReduceOp.MAX)
+        return float(t.item())
+
+    t_gen = time.perf_counter()
+    a, name = make_workload(args.config, args.grid)
+    t_gen = time.perf_counter() - t_gen
+    seed = 1 if rank == 0 else ck.mix_seed(1, rank)
+    total_iters = args.warmup + args.steps + 8
+    cfg = configs.baseline_adam(seed, max_iter=total_iters)
+
+    t_up = time.perf_counter()
+    dev = a.device()
+    t_up = time.perf_counter() - t_up
+    info = dev.info()
+    sess = ck.Session(ck.ExplicitOracle(a), cfg, [seed])
+    sess.run(args.warmup)
+    barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    ms_total, ms_apply, ms_tr = sess.time(args.steps, mode=0)
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    ms_max = allmax(ms_total)
+    value = world * args.steps / (ms_max / 1000.0)
+    sess.close()
+
+    n, nnz = a.nrows, a.nnz
+    b_apply, b_tr = bytes_per_iteration(nnz, n)
+    peak, peak_kind = measured_peaks()
+    k_apply = {"name": "k_apply<1>", "ms_avg": ms_apply / args.steps, "bytes": b_apply}
+    k_tr = {"name": "k_transpose<1>", "ms_avg": ms_tr / args.steps, "bytes": b_tr}
+    for k in (k_apply, k_tr):
+        k["gbs"] = k["bytes"] / (k["ms_avg"] / 1000.0) / 1e9
+        k["frac"] = k["gbs"] / peak
+    dom = k_tr if ms_tr >= ms_apply else k_apply
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                tr = json.load(f)
+            if tr.get("workload") == name:
+                traffic = tr.get(dom["name"].split("<")[0])
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": dom["frac"], "traffic": traffic, "kernel": dom["name"],
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_per_launch": dom["bytes"]}
+    iter_bytes = b_apply + b_tr
+    step_eff_gbs = iter_bytes / (ms_total / args.steps / 1000.0) / 1e9
+
+    # ---- e2e: the public API call a user makes, from host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        a2 = ck.SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices, a.values,
+                             validate=False)
+        regs = []
+        for arr in (a2.row_offsets, a2.col_indices, a2.values):
+            if _lib.load().ck_host_register(arr.ctypes.data, arr.nbytes) == 0:
+                regs.append(arr)
+        e2e_iters = args.e2e_iters
+        cfg2 = configs.baseline_adam(seed, max_iter=e2e_iters)
+        barrier()
+        t0 = time.perf_counter()
+        est = ck.norm2(a2, cfg2)  # upload (A, A^T build) + x0 + loop + witness check + D2H
+        t1 = time.perf_counter()
+        barrier()
+        for arr in regs:
+            _lib.load().ck_host_unregister(arr.ctypes.data)
+        a2.release_device()
+        dt = allmax(t1 - t0)
+        h2d = 8 * (n + 1) + 12 * nnz + 8 * n
+        d2h = 8 * n + 64
+        e2e = {"value": world * est.iterations / dt, "unit": UNIT,
+               "h2d_bytes_per_step": h2d / max(est.iterations, 1),
+               "d2h_bytes_per_step": d2h / max(est.iterations, 1),
+               "call": f"norm2(A, alpha=1e-2, {e2e_iters} iterations) from pinned host CSR: "
+                       "upload + device A^T/SELL build + x0 + loop + witness check + D2H",
+               "seconds": dt, "iterations": est.iterations, "sigma_max": est.value}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = args.cpu_threads or host_threads_budget(a)
+        r = cpu_reference(a, args.steps, threads, args.cpu_iters)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+               "sample": f"{r['cores']} concurrent reference projected_adam runs x "
+                         f"{args.cpu_iters} iterations on {name}; steady-state rate "
+                         f"({r['timed_iterations']} iterations timed)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, DESIGN.md section 3)",
+            "config": {"workload": name, "n": n, "nnz": nnz, "path": "sigma_max",
+                       "adam": "alpha=1e-2,beta1=.9,beta2=.999,eps=1e-8",
+                       "parallelism": f"replicas{world} (independent restart streams)",
+                       "l2": f"inputs larger than L2 (matrix {(24 * nnz) / 1e9:.1f} GB "
+                             f"per iteration vs 126 MB L2); no flush needed",
+                       "sell_padding": (info["sell_entries_a"] - nnz) / max(nnz, 1)},
+            "roofline": roofline,
+            "kernels": {"apply": k_apply, "transpose": k_tr},
+            "effective_gbs_per_gpu": step_eff_gbs,
+            "bytes_per_iteration": iter_bytes,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": 2 * args.steps,
+            "setup_s": {"generate": t_gen, "upload_and_build": t_up},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist[1].destroy_process_group()
+    return 0
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=300)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=4)
+    p.add_argument("--grid", type=int, default=None, help="override the grid (smoke runs)")
+    p.add_argument("--e2e-iters", type=int, default=2000)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0)
+    p.add_argument("--cpu-iters", type=int, default=3)
+    args = p.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.exit(main())

@@ -99,6 +99,10 @@ uint64_t ck_mix_seed(uint64_t base, uint64_t stream);
  * rng.hpp:68-77; bit-identical to the reference. */
 ck_status ck_random_unit_vectors(uint64_t seed, int64_t n, int64_t count, double* out);
 
+/* `count` uniform_in(gen, lo, hi) draws of one mt19937_64(seed), rng.hpp:36-38
+ * (make_known_solution's x*, bench.hpp:141-150). */
+ck_status ck_uniform_in(uint64_t seed, int64_t count, double lo, double hi, double* out);
+
 /* ------------------------------------------ error_bounds.hpp scalar formulas */
 ck_status ck_loose_bounds(double residual_norm, double b_norm, double kappa, double* lower,
                           double* upper);                               /* :59-68 */
@@ -155,6 +159,15 @@ ck_status ck_session_time(ck_session s, uint64_t steps, int32_t mode, double* ms
                           double* ms_apply, double* ms_transpose);
 ck_status ck_session_result(ck_session s, int32_t column, ck_norm_result* res, double* witness);
 ck_status ck_session_free(ck_session s);
+
+/* ----------------------------------------------------- synthetic inputs (host) */
+/* Operators of the BASELINE.json configurations (no reference counterpart for
+ * kinds 2-5; kind 1 follows acceptance.cpp:240-254 plus BASELINE row scaling).
+ * kind 1 Laplacian grid^2, 2 Stokes 3*grid^2, 3 hydro-mechanical 6*grid^2,
+ * 5 banded (grid = n, param = bandwidth). Call with row_offsets == NULL to get
+ * *nrows / *nnz, then with buffers of those sizes. */
+ck_status ck_generate(int32_t kind, int64_t grid, int64_t param, uint64_t seed, int64_t* nrows,
+                      int64_t* nnz, int64_t* row_offsets, int32_t* col_indices, double* values);
 
 #ifdef __cplusplus
 }

@@ -373,6 +373,15 @@ class Oracle:
         return {k: getattr(rep, k) for k, _ in BoundsRep._fields_}
 
     # bench.py reference arm (ref backend only)
+    def time_iterations(self, a, cfg, nthreads: int, iters: int):
+        """Steady-state summed iterations/s of `nthreads` concurrent reference runs."""
+        keep, args = self._csr_args(a)
+        c = _cfg(cfg)
+        rate, n, span = C.c_double(), C.c_uint64(), C.c_double()
+        self._f("time_iterations")(*args, C.byref(c), C.c_int32(nthreads), C.c_uint64(iters),
+                                   C.byref(rate), C.byref(n), C.byref(span))
+        return rate.value, n.value, span.value
+
     def throughput_explicit(self, a, cfg, nthreads: int):
         keep, args = self._csr_args(a)
         c = _cfg(cfg)

@@ -363,4 +363,58 @@ int ckref_throughput_explicit(int64_t nr, int64_t nc, const int64_t* rp, const i
   return 0;
 }
 
+// Steady-state iteration rate of the reference projected_adam (condest.hpp:210-276)
+// for bench.py's CPU arm: `nthreads` independent runs (seeds cfg.seed,
+// mix_seed(seed, k)) on std::threads, each limited to `iters` iterations; the
+// rate of each run is measured between its first and last observer callback
+// (so setup -- x0 draw, matrix conversion -- is excluded). Returns the summed
+// iterations/s, the iterations timed and the wall seconds of the timed spans.
+int ckref_time_iterations(int64_t nr, int64_t nc, const int64_t* rp, const int32_t* ci,
+                          const double* va, const ckref_adam_cfg* cfg, int32_t nthreads,
+                          uint64_t iters, double* rate, uint64_t* timed_iters, double* span) {
+  SparseMatrix a = to_sparse(nr, nc, rp, ci, va);
+  ExplicitOracle ox(a);
+  std::vector<double> rates(static_cast<std::size_t>(nthreads), 0.0), spans(rates.size(), 0.0);
+  std::vector<uint64_t> counts(rates.size(), 0);
+  std::vector<std::thread> pool;
+  for (int32_t k = 0; k < nthreads; ++k) {
+    pool.emplace_back([&, k] {
+      AdamConfig c = to_cfg(cfg);
+      c.seed = k == 0 ? cfg->seed : mix_seed(cfg->seed, static_cast<uint64_t>(k));
+      c.max_iter = iters;
+      c.patience = iters + 1;
+      using clk = std::chrono::steady_clock;
+      clk::time_point first{}, last{};
+      uint64_t seen = 0;
+      AdamObserver obs = [&](const AdamState&, const AdamStepInfo&) {
+        last = clk::now();
+        if (seen == 0) first = last;
+        ++seen;
+      };
+      try {
+        projected_adam(ox, c, obs);
+      } catch (...) {
+      }
+      if (seen >= 2) {
+        double sec = std::chrono::duration<double>(last - first).count();
+        rates[static_cast<std::size_t>(k)] = static_cast<double>(seen - 1) / sec;
+        spans[static_cast<std::size_t>(k)] = sec;
+        counts[static_cast<std::size_t>(k)] = seen - 1;
+      }
+    });
+  }
+  for (auto& t : pool) t.join();
+  double r = 0.0, sp = 0.0;
+  uint64_t n = 0;
+  for (std::size_t k = 0; k < rates.size(); ++k) {
+    r += rates[k];
+    sp = std::max(sp, spans[k]);
+    n += counts[k];
+  }
+  *rate = r;
+  *timed_iters = n;
+  *span = sp;
+  return 0;
+}
+
 }  // extern "C"

@@ -58,6 +58,7 @@ _SIGS = {
     "ck_adam_default": (None, [C.POINTER(AdamCfg)]),
     "ck_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ck_random_unit_vectors": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, dp]),
+    "ck_uniform_in": (C.c_int, [C.c_uint64, C.c_int64, C.c_double, C.c_double, dp]),
     "ck_loose_bounds": (C.c_int, [C.c_double, C.c_double, C.c_double, dp, dp]),
     "ck_tight_bounds": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, dp, dp]),
     "ck_propagate_bound": (C.c_int, [C.c_double, dp]),
@@ -80,6 +81,8 @@ _SIGS = {
     "ck_session_time": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, dp, dp, dp]),
     "ck_session_result": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(NormResult), dp]),
     "ck_session_free": (C.c_int, [C.c_void_p]),
+    "ck_generate": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_uint64, i64p, i64p, i64p, i32p,
+                              dp]),
 }
 
 _lib = None

@@ -4,23 +4,26 @@
 // One loop trip ("step") is two kernels over HBM-resident state:
 //
 //   k_apply<R>      x~ = x - (delta - r x)          (tangent step, :231-240)
-//                   y' = A x~                        (sliced-ELL SpMV; loss at
+//                   y' = A x~                        (sliced-ELL SpMV; the loss at
 //                                                     x_{t+1} = x~/||x~||, :249-251)
-//                   reduce ||x~|| (double-double, the compensated norm :241)
+//                   reduce ||x~|| (double-double; the compensated norm, :241)
 //                   and ||y'|| (one-pass scaled sum of squares, two_norm)
-//                   -> last CTA: loss, patience, best-tracking, next iteration
+//                   -> last CTA: loss, patience, best-tracking, next-iteration
 //                      scalars (:221-224, :257-275)
 //   k_transpose<R>  x_{t+1} = x~/||x~|| materialised into a free buffer,
 //                   z = A^T y' / ||x~||              (grad, :96-107)
-//                   g, m, v, delta (Adam, :225-229), reduce r = x.delta (:231)
+//                   g, m, v, delta (Adam, :225-229); reduce r = x.delta (:231)
 //                   -> last CTA: radial scalar for the next k_apply.
 //
-// A x_{t+1} is therefore computed once per iteration and serves both the loss
-// of iteration t and the gradient of iteration t+1 (the reference evaluates it
+// A x_{t+1} is computed once per iteration and serves both the loss of
+// iteration t and the gradient of iteration t+1 (the reference evaluates it
 // twice on bitwise-identical input). The best iterate is tracked by rotating
 // three iterate buffers instead of copying x_min (:264-267). R independent runs
 // (restarts, :301-312) share one sweep over the matrix as columns of a
 // multi-vector; each column's arithmetic is independent of R.
+//
+// Layout: (x, delta) and (m, v) are stored as double2 pairs, so the SpMV gather
+// of x~ is one 16-byte load and the Adam update moves 16-byte vectors.
 //
 // Per-column control state lives on the device; the host only services
 // degenerate-direction restarts (which need the reference's mt19937_64 stream,
@@ -39,6 +42,15 @@ namespace ck {
 
 constexpr int kPA = 9;  // per-column partials of k_apply
 constexpr int kPT = 1;  // per-column partials of k_transpose
+
+// Resident CTAs per SM the fused kernels are compiled for (register budget),
+// hence their one-wave grid sizes. Fixed constants: the reduction tree -- and
+// every result bit -- is the same on every device.
+template <int R>
+struct Occ {
+  static constexpr int apply = R == 1 ? 4 : 2;
+  static constexpr int transpose = R <= 2 ? 4 : 2;
+};
 
 __device__ __forceinline__ int pick_free(int cur, int best) {
   for (int b = 0; b < 3; ++b)
@@ -66,7 +78,9 @@ __device__ __forceinline__ void begin_iteration(ColState& s, const Params& p) {
 }
 
 // Control step after k_apply's reductions (thread 0 of the last CTA).
-__device__ void control_apply(ColState& s, const Params& p, double N, double yn) {
+__device__ __noinline__ void control_apply(ColState* sp, const Params* pp, double N, double yn) {
+  ColState& s = *sp;
+  const Params& p = *pp;
   s.xnorm = N;
   s.ynorm = yn;
   if (s.phase == PH_PRO) {
@@ -124,24 +138,29 @@ __device__ void control_apply(ColState& s, const Params& p, double N, double yn)
   s.phase = PH_GRAD;
 }
 
-template <int R>
-__global__ void __launch_bounds__(kTile) k_apply(LoopArgs a) {
+// x~ from a stored (x, delta) pair: x - (delta - r x)  (:232, :240)
+__device__ __forceinline__ double xtilde(double2 p, double rad) {
+  return __dsub_rn(p.x, __dsub_rn(p.y, __dmul_rn(rad, p.x)));
+}
+
+template <int R, bool OBS, int U = (R == 1 ? 8 : 4)>
+__global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_constant__ LoopArgs a) {
   if (!a.hdr->needA) return;
-  const bool observe = a.hdr->observe != 0;
   __shared__ double s_h[8], s_l[8];
   __shared__ int s_e[8], s_f[8];
-  __shared__ double s_res[R][5];
+  __shared__ double s_res[R][4];
 
   bool act[R], pro[R];
   double rad[R];
-  const double* xc[R];
+  const double2* xc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    int ph = a.st[r].phase;
+    const int ph = a.st[r].phase;
     act[r] = ph == PH_PRO || ph == PH_APPLY;
     pro[r] = ph == PH_PRO;
-    rad[r] = a.st[r].rad;
-    xc[r] = a.X + ((int64_t)a.st[r].cur * R + r) * a.nc_pad;
+    // prologue: delta is zero, so x~ = x exactly (x - (0 - 0 x) = x)
+    rad[r] = pro[r] ? 0.0 : a.st[r].rad;
+    xc[r] = a.PX + ((int64_t)a.st[r].cur * R + r) * a.nc_pad;
   }
   DD dd[R];
   ES es[R], dn[R];
@@ -155,44 +174,55 @@ __global__ void __launch_bounds__(kTile) k_apply(LoopArgs a) {
   }
   const int t0 = blockIdx.x * a.tpu_A;
   const int t1 = min(t0 + a.tpu_A, a.tiles_A);
-  for (int tile = t0; tile < t1; ++tile) {
-    const int64_t i = (int64_t)tile * kTile + threadIdx.x;
-    if (i < a.nc) {
+  // slice metadata of the first row, then prefetched one tile ahead
+  int64_t i = (int64_t)t0 * kTile + threadIdx.x;
+  int64_t sp0 = 0, sp1 = 0;
+  int L = 0;
+  if (t0 < t1 && i < a.nr_pad) {
+    sp0 = a.A.sp[i >> 5];
+    sp1 = a.A.sp[(i >> 5) + 1];
+    L = a.A.len[i];
+  }
+  for (int tile = t0; tile < t1; ++tile, i += kTile) {
+    const int64_t base = sp0 + (i & 31);
+    const int w = (int)((sp1 - sp0) >> 5);  // slice width: uniform across the warp
+    const int Lc = L;
+    const int64_t inext = i + kTile;
+    if (tile + 1 < t1 && inext < a.nr_pad) {
+      sp0 = a.A.sp[inext >> 5];
+      sp1 = a.A.sp[(inext >> 5) + 1];
+      L = a.A.len[inext];
+    }
+    if (i < a.nc) {  // own column-space element: ||x~||^2 (and observer stats)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (!act[r]) continue;
-        double x = xc[r][i];
-        double xt = x;
-        if (!pro[r]) {
-          double dp = __dsub_rn(a.dl[i * R + r], __dmul_rn(rad[r], x));  // :232
-          xt = __dsub_rn(x, dp);                                          // :240
-          if (observe) {
-            xd[r] = __fma_rn(x, dp, xd[r]);
-            es_add(dn[r], dp);
-          }
+        const double2 p = xc[r][i];
+        if (OBS && !pro[r]) {
+          const double dp = __dsub_rn(p.y, __dmul_rn(rad[r], p.x));
+          xd[r] = __fma_rn(p.x, dp, xd[r]);
+          es_add(dn[r], dp);
         }
-        dd_add_sq(dd[r], xt);
+        dd_add_sq(dd[r], xtilde(p, rad[r]));
       }
     }
     if (i < a.nr_pad) {
-      const int64_t base = a.A.sp[i >> 5] + (i & 31);
-      const int L = a.A.len[i];
       double acc[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = 0.0;
-#pragma unroll 4
-      for (int j = 0; j < L; ++j) {
-        const int64_t k = base + (int64_t)j * kSlice;
-        const int c = ld_stream(a.A.col + k);
-        const double v = ld_stream(a.A.val + k);
+      for (int j0 = 0; j0 < w; j0 += U) {
+        int c[U];
+        double v[U];
+        load_chunk<U>(a.A, base, j0, w, c, v);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!act[r]) continue;
-          double x = __ldg(xc[r] + c);
-          double xt = pro[r] ? x
-                             : __dsub_rn(x, __dsub_rn(__ldg(a.dl + (int64_t)c * R + r),
-                                                      __dmul_rn(rad[r], x)));
-          acc[r] = __dadd_rn(acc[r], __dmul_rn(v, xt));
+          double2 g[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) g[u] = __ldg(xc[r] + c[u]);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xtilde(g[u], rad[r])));
         }
       }
 #pragma unroll
@@ -210,7 +240,7 @@ __global__ void __launch_bounds__(kTile) k_apply(LoopArgs a) {
     ES e = block_es(es[r], s_h, s_e, s_f);
     double x2 = 0.0;
     ES e2 = es_zero();
-    if (observe) {
+    if (OBS) {
       x2 = block_sum(xd[r], s_h);
       e2 = block_es(dn[r], s_h, s_e, s_f);
     }
@@ -239,13 +269,17 @@ __global__ void __launch_bounds__(kTile) k_apply(LoopArgs a) {
       const double* p = a.partA + ((int64_t)u * R + r) * kPA;
       dd_merge(d, DD{__ldcg(p), __ldcg(p + 1)});
       es_merge(e, ES{__ldcg(p + 2), (int)__ldcg(p + 3), (int)__ldcg(p + 4)});
-      x2 = __dadd_rn(x2, __ldcg(p + 5));
-      es_merge(e2, ES{__ldcg(p + 6), (int)__ldcg(p + 7), (int)__ldcg(p + 8)});
+      if (OBS) {
+        x2 = __dadd_rn(x2, __ldcg(p + 5));
+        es_merge(e2, ES{__ldcg(p + 6), (int)__ldcg(p + 7), (int)__ldcg(p + 8)});
+      }
     }
     d = block_dd(d, s_h, s_l);
     e = block_es(e, s_h, s_e, s_f);
-    x2 = block_sum(x2, s_h);
-    e2 = block_es(e2, s_h, s_e, s_f);
+    if (OBS) {
+      x2 = block_sum(x2, s_h);
+      e2 = block_es(e2, s_h, s_e, s_f);
+    }
     if (threadIdx.x == 0) {
       s_res[r][0] = sqrt(__dadd_rn(d.hi, d.lo));
       s_res[r][1] = es_norm(e);
@@ -256,18 +290,18 @@ __global__ void __launch_bounds__(kTile) k_apply(LoopArgs a) {
   if (threadIdx.x == 0) {
     int needT = 0, nwait = 0, ndone = 0;
     for (int r = 0; r < R; ++r) {
-      ColState s = a.st[r];
-      if (s.phase == PH_PRO || s.phase == PH_APPLY) {
-        if (s.phase == PH_APPLY && observe) {
-          s.obs_xd = s_res[r][2];
-          s.obs_dn = s_res[r][3];
+      ColState* s = a.st + r;
+      const int ph = s->phase;
+      if (ph == PH_PRO || ph == PH_APPLY) {
+        if (OBS && ph == PH_APPLY) {
+          s->obs_xd = s_res[r][2];
+          s->obs_dn = s_res[r][3];
         }
-        control_apply(s, a.prm, s_res[r][0], s_res[r][1]);
-        a.st[r] = s;
+        control_apply(s, &a.prm, s_res[r][0], s_res[r][1]);
       }
-      needT |= s.phase == PH_GRAD;
-      nwait += s.phase == PH_WAIT;
-      ndone += s.phase == PH_DONE;
+      needT |= s->phase == PH_GRAD;
+      nwait += s->phase == PH_WAIT;
+      ndone += s->phase == PH_DONE;
     }
     a.hdr->needT = needT;
     a.hdr->needA = 0;
@@ -276,16 +310,17 @@ __global__ void __launch_bounds__(kTile) k_apply(LoopArgs a) {
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(kTile) k_transpose(LoopArgs a) {
+template <int R, int U = (R <= 2 ? 8 : 4)>
+__global__ void __launch_bounds__(kTile, Occ<R>::transpose)
+    k_transpose(const __grid_constant__ LoopArgs a) {
   if (!a.hdr->needT) return;
   __shared__ double s_h[8];
   __shared__ double s_res[R];
-  const Params p = a.prm;
+  const Params& p = a.prm;
   bool act[R], mat[R];
   double rad[R], ndiv[R], ix2[R], iy2[R], mc[R], vc[R];
-  const double* xc[R];
-  double* xn_out[R];
+  const double2* xc[R];
+  double2* xn_out[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const ColState& s = a.st[r];
@@ -297,8 +332,9 @@ __global__ void __launch_bounds__(kTile) k_transpose(LoopArgs a) {
     iy2[r] = s.inv_y2;
     mc[r] = s.mc;
     vc[r] = s.vc;
-    xc[r] = a.X + ((int64_t)s.cur * R + r) * a.nc_pad;
-    xn_out[r] = a.X + ((int64_t)s.nxt * R + r) * a.nc_pad;
+    xc[r] = a.PX + ((int64_t)s.cur * R + r) * a.nc_pad;
+    // prologue (mat = 0): x stays where it is and only delta is rewritten
+    xn_out[r] = a.PX + ((int64_t)(mat[r] ? s.nxt : s.cur) * R + r) * a.nc_pad;
   }
   const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
   double dot[R];
@@ -306,50 +342,65 @@ __global__ void __launch_bounds__(kTile) k_transpose(LoopArgs a) {
   for (int r = 0; r < R; ++r) dot[r] = 0.0;
   const int t0 = blockIdx.x * a.tpu_T;
   const int t1 = min(t0 + a.tpu_T, a.tiles_T);
-  for (int tile = t0; tile < t1; ++tile) {
-    const int64_t j = (int64_t)tile * kTile + threadIdx.x;
-    const int64_t base = a.AT.sp[j >> 5] + (j & 31);
-    const int L = a.AT.len[j];
+  int64_t j = (int64_t)t0 * kTile + threadIdx.x;
+  int64_t sp0 = 0, sp1 = 0;
+  int L = 0;
+  if (t0 < t1) {
+    sp0 = a.AT.sp[j >> 5];
+    sp1 = a.AT.sp[(j >> 5) + 1];
+    L = a.AT.len[j];
+  }
+  for (int tile = t0; tile < t1; ++tile, j += kTile) {
+    const int64_t base = sp0 + (j & 31);
+    const int w = (int)((sp1 - sp0) >> 5);
+    const int Lc = L;
+    if (tile + 1 < t1) {
+      const int64_t jn = j + kTile;
+      sp0 = a.AT.sp[jn >> 5];
+      sp1 = a.AT.sp[(jn >> 5) + 1];
+      L = a.AT.len[jn];
+    }
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
-#pragma unroll 4
-    for (int q = 0; q < L; ++q) {
-      const int64_t k = base + (int64_t)q * kSlice;
-      const int c = ld_stream(a.AT.col + k);
-      const double v = ld_stream(a.AT.val + k);
+    for (int j0 = 0; j0 < w; j0 += U) {
+      int c[U];
+      double v[U];
+      load_chunk<U>(a.AT, base, j0, w, c, v);
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v, __ldg(a.y + (int64_t)c * R + r)));
+      for (int r = 0; r < R; ++r) {
+        if (!act[r]) continue;
+        double yg[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) yg[u] = __ldg(a.y + (int64_t)c[u] * R + r);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], yg[u]));
+      }
     }
     if (j < a.nc) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (!act[r]) continue;
         const int64_t e = j * R + r;
-        double xo = xc[r][j];
-        double xn = xo;
-        if (mat[r]) {
-          double dp = __dsub_rn(a.dl[e], __dmul_rn(rad[r], xo));
-          xn = __ddiv_rn(__dsub_rn(xo, dp), ndiv[r]);  // :240-247
-          xn_out[r][j] = xn;
-        }
-        double z = __ddiv_rn(acc[r], ndiv[r]);  // A^T A x_{t+1}
-        double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(z, iy2[r]));  // :105
-        double mm = __dadd_rn(__dmul_rn(p.beta1, a.m[e]), __dmul_rn(om1, g));  // :226
-        double vv = __dadd_rn(__dmul_rn(p.beta2, a.v[e]), __dmul_rn(__dmul_rn(om2, g), g));  // :227
-        double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
-                             __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));  // :228
-        a.m[e] = mm;
-        a.v[e] = vv;
-        a.dl[e] = d;
+        const double2 px = xc[r][j];
+        const double xn = mat[r] ? __ddiv_rn(xtilde(px, rad[r]), ndiv[r]) : px.x;  // :240-247
+        const double z = __ddiv_rn(acc[r], ndiv[r]);                               // A^T A x_{t+1}
+        const double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(z, iy2[r]));  // :105
+        const double2 mv = a.MV[e];
+        const double mm = __dadd_rn(__dmul_rn(p.beta1, mv.x), __dmul_rn(om1, g));             // :226
+        const double vv = __dadd_rn(__dmul_rn(p.beta2, mv.y), __dmul_rn(__dmul_rn(om2, g), g));  // :227
+        const double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
+                                   __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));  // :228
+        a.MV[e] = make_double2(mm, vv);
+        xn_out[r][j] = make_double2(xn, d);
         dot[r] = __fma_rn(xn, d, dot[r]);
       }
     }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    double s = block_sum(dot[r], s_h);
+    const double s = block_sum(dot[r], s_h);
     if (threadIdx.x == 0) a.partT[(int64_t)blockIdx.x * R + r] = s;
   }
   if (!elect_last_block(&a.hdr->cntT, (unsigned)a.units_T)) return;
@@ -364,63 +415,62 @@ __global__ void __launch_bounds__(kTile) k_transpose(LoopArgs a) {
   if (threadIdx.x == 0) {
     int needA = 0;
     for (int r = 0; r < R; ++r) {
-      ColState s = a.st[r];
-      if (s.phase == PH_GRAD) {
-        s.rad = s_res[r];
-        if (s.mat) {
-          s.cur = s.nxt;
-          s.pend = 0;
+      ColState* s = a.st + r;
+      if (s->phase == PH_GRAD) {
+        s->rad = s_res[r];
+        if (s->mat) {
+          s->cur = s->nxt;
+          s->pend = 0;
         }
-        s.phase = PH_APPLY;
-        a.st[r] = s;
+        s->phase = PH_APPLY;
       }
-      needA |= s.phase == PH_APPLY;
+      needA |= s->phase == PH_APPLY;
     }
     a.hdr->needA = needA;
     a.hdr->needT = 0;
   }
 }
 
-// x_{t+1} = (x - (delta - r x)) / N into `out` (epilogue materialisation).
-__global__ void k_materialise(int64_t nc, int R, int col, const double* __restrict__ x,
-                              const double* __restrict__ dl, double rad, double ndiv,
+// x_{t+1} = x~ / N from (x, delta) pairs, into a plain vector (epilogue / observer).
+__global__ void k_materialise(int64_t nc, const double2* __restrict__ px, double rad, double ndiv,
                               double* out) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= nc) return;
-  double xo = x[j];
-  double dp = __dsub_rn(dl[j * R + col], __dmul_rn(rad, xo));
-  out[j] = __ddiv_rn(__dsub_rn(xo, dp), ndiv);
+  if (j < nc) out[j] = __ddiv_rn(xtilde(px[j], rad), ndiv);
 }
 
-__global__ void k_zero_column(int64_t n, int R, int col, double* a, double* b, double* c) {
+__global__ void k_extract_x(int64_t n, const double2* __restrict__ px, double* out) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  a[j * R + col] = 0.0;
-  b[j * R + col] = 0.0;
-  c[j * R + col] = 0.0;
+  if (j < n) out[j] = px[j].x;
 }
 
-}  // namespace ck
+__global__ void k_store_x(int64_t n, const double* __restrict__ x, double2* px) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) px[j] = make_double2(x[j], 0.0);
+}
 
-namespace ck {
+__global__ void k_zero_moments(int64_t n, int R, int col, double2* mv) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) mv[j * R + col] = make_double2(0.0, 0.0);
+}
 
-static void launch_step(ck_session_s* s, cudaStream_t st) {
-  const LoopArgs& a = s->args;
-  switch (s->R) {
-    case 1: k_apply<1><<<a.units_A, kTile, 0, st>>>(a); k_transpose<1><<<a.units_T, kTile, 0, st>>>(a); break;
-    case 2: k_apply<2><<<a.units_A, kTile, 0, st>>>(a); k_transpose<2><<<a.units_T, kTile, 0, st>>>(a); break;
-    case 3: k_apply<3><<<a.units_A, kTile, 0, st>>>(a); k_transpose<3><<<a.units_T, kTile, 0, st>>>(a); break;
-    default: k_apply<4><<<a.units_A, kTile, 0, st>>>(a); k_transpose<4><<<a.units_T, kTile, 0, st>>>(a); break;
-  }
+// ---------------------------------------------------------------- host side
+
+static unsigned grid256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
+
+template <int R>
+static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
+  if (s->observe_on)
+    k_apply<R, true><<<s->args.units_A, kTile, 0, st>>>(s->args);
+  else
+    k_apply<R, false><<<s->args.units_A, kTile, 0, st>>>(s->args);
 }
 
 static void launch_apply_only(ck_session_s* s, cudaStream_t st) {
-  const LoopArgs& a = s->args;
   switch (s->R) {
-    case 1: k_apply<1><<<a.units_A, kTile, 0, st>>>(a); break;
-    case 2: k_apply<2><<<a.units_A, kTile, 0, st>>>(a); break;
-    case 3: k_apply<3><<<a.units_A, kTile, 0, st>>>(a); break;
-    default: k_apply<4><<<a.units_A, kTile, 0, st>>>(a); break;
+    case 1: launch_apply_r<1>(s, st); break;
+    case 2: launch_apply_r<2>(s, st); break;
+    case 3: launch_apply_r<3>(s, st); break;
+    default: launch_apply_r<4>(s, st); break;
   }
 }
 
@@ -432,6 +482,21 @@ static void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
     case 3: k_transpose<3><<<a.units_T, kTile, 0, st>>>(a); break;
     default: k_transpose<4><<<a.units_T, kTile, 0, st>>>(a); break;
   }
+}
+
+static void launch_step(ck_session_s* s, cudaStream_t st) {
+  launch_apply_only(s, st);
+  launch_transpose_only(s, st);
+}
+
+static int occ_apply(int R) {
+  return R == 1 ? Occ<1>::apply : R == 2 ? Occ<2>::apply : R == 3 ? Occ<3>::apply : Occ<4>::apply;
+}
+static int occ_transpose(int R) {
+  return R == 1   ? Occ<1>::transpose
+         : R == 2 ? Occ<2>::transpose
+         : R == 3 ? Occ<3>::transpose
+                  : Occ<4>::transpose;
 }
 
 static void pull_state(ck_session_s* s) {
@@ -448,14 +513,20 @@ static void push_state(ck_session_s* s) {
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
-// Upload a fresh start vector for column c (original order) into buffer b.
+static double2* col_buf(ck_session_s* s, int b, int c) {
+  return s->PX.p + ((int64_t)b * s->R + c) * s->args.nc_pad;
+}
+
+// Upload a fresh start vector for column c (original order) into buffer b:
+// (x, delta = 0) pairs in the permuted column space, m = v = 0.
 static void load_start(ck_session_s* s, int c, int b, const double* x) {
   cudaStream_t st = s->A->stream;
-  int64_t nc = s->A->ncols;
+  const int64_t nc = s->A->ncols, ncp = s->args.nc_pad;
   CK_CUDA(cudaMemcpyAsync(s->tmp.p, x, sizeof(double) * nc, cudaMemcpyHostToDevice, st));
-  double* dst = s->X.p + ((int64_t)b * s->R + c) * s->args.nc_pad;
-  gather_perm(s->A->at.perm.p, s->args.nc_pad, s->tmp.p, dst, st);
-  k_zero_column<<<(unsigned)ceil_div(s->args.nc_pad, 256), 256, 0, st>>>(s->args.nc_pad, s->R, c, s->m.p, s->v.p, s->dl.p);
+  double* perm = s->tmp.p + ncp;
+  gather_perm(s->A->at.perm.p, ncp, s->tmp.p, perm, st);
+  k_store_x<<<grid256(ncp), 256, 0, st>>>(ncp, perm, col_buf(s, b, c));
+  k_zero_moments<<<grid256(ncp), 256, 0, st>>>(ncp, s->R, c, s->MV.p);
   CK_CUDA(cudaGetLastError());
   CK_CUDA(cudaStreamSynchronize(st));
 }
@@ -468,7 +539,7 @@ static void service_restarts(ck_session_s* s) {
     ColState& cs = s->h_st[c];
     if (cs.phase != PH_WAIT) continue;
     random_unit_vector_host(&s->gens[c], s->A->ncols, s->hx.data());
-    int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
+    const int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
     load_start(s, c, b, s->hx.data());
     cs.cur = b;
     cs.b1p = 1.0;
@@ -513,28 +584,26 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   a.nr_pad = A->a.nrows_pad;
   a.nc_pad = A->at.nrows_pad;
   a.tiles_A = (int)(std::max(a.nr_pad, a.nc_pad) / kTile);
-  a.tpu_A = (int)std::max<int64_t>(1, ceil_div(a.tiles_A, kTargetUnits));
+  const int64_t unitsA = 148 * occ_apply(R), unitsT = 148 * occ_transpose(R);
+  a.tpu_A = (int)std::max<int64_t>(1, ceil_div(a.tiles_A, unitsA));
   a.units_A = (int)ceil_div(a.tiles_A, a.tpu_A);
   a.tiles_T = (int)(a.nc_pad / kTile);
-  a.tpu_T = (int)std::max<int64_t>(1, ceil_div(a.tiles_T, kTargetUnits));
+  a.tpu_T = (int)std::max<int64_t>(1, ceil_div(a.tiles_T, unitsT));
   a.units_T = (int)ceil_div(a.tiles_T, a.tpu_T);
   cudaStream_t st = A->stream;
-  s->X.alloc(3 * R * a.nc_pad);
-  s->m.alloc(a.nc_pad * R);
-  s->v.alloc(a.nc_pad * R);
-  s->dl.alloc(a.nc_pad * R);
+  s->PX.alloc(3 * R * a.nc_pad);
+  s->MV.alloc(a.nc_pad * R);
   s->y.alloc(std::max(a.nr_pad, a.nc_pad) * R);
   s->partA.alloc((int64_t)a.units_A * R * kPA);
   s->partT.alloc((int64_t)a.units_T * R * kPT);
-  s->tmp.alloc(std::max(a.nr_pad, a.nc_pad));
+  s->tmp.alloc(2 * std::max(a.nr_pad, a.nc_pad));
   s->st.alloc(R);
   s->hdr.alloc(1);
-  CK_CUDA(cudaMemsetAsync(s->X.p, 0, s->X.bytes(), st));
+  CK_CUDA(cudaMemsetAsync(s->PX.p, 0, s->PX.bytes(), st));
+  CK_CUDA(cudaMemsetAsync(s->MV.p, 0, s->MV.bytes(), st));
   CK_CUDA(cudaMemsetAsync(s->y.p, 0, s->y.bytes(), st));
-  a.X = s->X.p;
-  a.m = s->m.p;
-  a.v = s->v.p;
-  a.dl = s->dl.p;
+  a.PX = s->PX.p;
+  a.MV = s->MV.p;
   a.y = s->y.p;
   a.partA = s->partA.p;
   a.partT = s->partT.p;
@@ -566,9 +635,10 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   h.ndone = cfg->max_iter == 0 ? R : 0;
   *s->h_hdr = h;
   push_state(s);
-  // chunk length: about 4 ms of work per host round trip, 4..256 steps
-  double bytes_per_step = 24.0 * (double)A->nnz * 1.0 + 100.0 * (double)A->ncols * R;
-  int steps = (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
+  // chunk length: about 4 ms of device work per host round trip, 4..256 steps
+  const double bytes_per_step = 24.0 * (double)A->nnz + 100.0 * (double)A->ncols * R;
+  const int steps =
+      (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
   build_graph(s, steps);
 }
 
@@ -584,10 +654,11 @@ void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished) {
     }
     if (s->h_hdr->nwait > 0) service_restarts(s);
     if (max_steps && done >= max_steps) return;
-    if (max_steps && max_steps - done < (uint64_t)s->gsteps) {
-      for (uint64_t k = done; k < max_steps; ++k) launch_step(s, st);
+    if (s->observe_on || (max_steps && max_steps - done < (uint64_t)s->gsteps)) {
+      const uint64_t n = max_steps ? std::min<uint64_t>(max_steps - done, s->gsteps) : s->gsteps;
+      for (uint64_t k = 0; k < n; ++k) launch_step(s, st);
       CK_CUDA(cudaGetLastError());
-      done = max_steps;
+      done += n;
     } else {
       CK_CUDA(cudaGraphLaunch(s->gexec, st));
       done += (uint64_t)s->gsteps;
@@ -607,7 +678,8 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
     CK_CUDA(cudaStreamSynchronize(st));
     CK_CUDA(cudaEventRecord(e0, st));
     uint64_t k = 0;
-    for (; k + (uint64_t)s->gsteps <= steps; k += (uint64_t)s->gsteps) CK_CUDA(cudaGraphLaunch(s->gexec, st));
+    for (; k + (uint64_t)s->gsteps <= steps; k += (uint64_t)s->gsteps)
+      CK_CUDA(cudaGraphLaunch(s->gexec, st));
     for (; k < steps; ++k) launch_step(s, st);
     CK_CUDA(cudaEventRecord(e1, st));
     CK_CUDA(cudaEventSynchronize(e1));
@@ -648,6 +720,12 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
   *ms_transpose = tt;
 }
 
+// x of buffer b / column c as a plain permuted vector in `out` (nc_pad doubles).
+static void extract_x(ck_session_s* s, int b, int c, double* out, cudaStream_t st) {
+  k_extract_x<<<grid256(s->args.nc_pad), 256, 0, st>>>(s->args.nc_pad, col_buf(s, b, c), out);
+  CK_CUDA(cudaGetLastError());
+}
+
 // Final NormEstimate for column c (condest.hpp:278-296).
 void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness) {
   if (c < 0 || c >= s->R) fail(CK_ERR_INVALID_ARGUMENT, "column out of range");
@@ -655,14 +733,14 @@ void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness
   pull_state(s);
   ColState& cs = s->h_st[c];
   const int64_t ncp = s->args.nc_pad;
-  double* best = s->X.p + ((int64_t)cs.best * s->R + c) * ncp;
+  double* xbest = s->tmp.p + ncp;  // plain copy of x_min (permuted space)
   if (cs.pend) {  // x_{t+1} became the best but was never materialised
-    const double* cur = s->X.p + ((int64_t)cs.cur * s->R + c) * ncp;
-    k_materialise<<<(unsigned)ceil_div(ncp, 256), 256, 0, st>>>(s->A->ncols > 0 ? ncp : 0, s->R, c, cur, s->dl.p, cs.rad, cs.ndiv, best);
+    CK_CUDA(cudaMemsetAsync(xbest, 0, sizeof(double) * ncp, st));
+    k_materialise<<<grid256(ncp), 256, 0, st>>>(s->A->ncols, col_buf(s, cs.cur, c), cs.rad,
+                                                cs.ndiv, xbest);
     CK_CUDA(cudaGetLastError());
-    cs.pend = 0;
-    cs.cur = cs.best;
-    push_state(s);
+  } else {
+    extract_x(s, cs.best, c, xbest, st);
   }
   res->iterations = cs.t;
   res->converged = cs.converged;
@@ -670,8 +748,8 @@ void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness
   if (std::isfinite(cs.loss_min)) {
     res->value = std::exp(-cs.loss_min);
     // witness re-check, condest.hpp:284-289
-    matrix_apply_perm(s->A, best, s->tmp.p, st);
-    double chk = device_norm(s->tmp.p, s->A->a.nrows_pad, s->A->s_red.p, st);
+    matrix_apply_perm(s->A, xbest, s->tmp.p, st);
+    const double chk = device_norm(s->tmp.p, s->A->a.nrows_pad, s->A->s_red.p, st);
     if (!(std::fabs(chk - res->value) <= 1e-12 * std::max(res->value, chk)))
       fail(CK_ERR_LOGIC, "norm estimate does not match ||Op witness||");
   } else {
@@ -679,10 +757,18 @@ void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness
     res->converged = 0;
   }
   if (witness) {
-    scatter_perm(s->A->at.perm.p, ncp, best, s->tmp.p, st);
-    CK_CUDA(cudaMemcpyAsync(witness, s->tmp.p, sizeof(double) * s->A->ncols, cudaMemcpyDeviceToHost, st));
+    scatter_perm(s->A->at.perm.p, ncp, xbest, s->tmp.p, st);
+    CK_CUDA(cudaMemcpyAsync(witness, s->tmp.p, sizeof(double) * s->A->ncols,
+                            cudaMemcpyDeviceToHost, st));
     CK_CUDA(cudaStreamSynchronize(st));
   }
+}
+
+static void download_perm(ck_session_s* s, const double* xperm, double* host, cudaStream_t st) {
+  scatter_perm(s->A->at.perm.p, s->args.nc_pad, xperm, s->A->s_out.p, st);
+  CK_CUDA(cudaMemcpyAsync(host, s->A->s_out.p, sizeof(double) * s->A->ncols,
+                          cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
 }
 
 // Observer mode (AdamObserver, condest.hpp:234-238, 268-271) for column 0:
@@ -690,14 +776,13 @@ void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness
 // iteration's scalars and, optionally, x_{t+1} and x_min.
 void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, double* x_min) {
   cudaStream_t st = s->A->stream;
+  s->observe_on = true;  // k_apply<R, true> from here on (no graphs in this mode)
   pull_state(s);
-  if (!s->observe_on) {
-    s->h_hdr->observe = 1;
-    push_state(s);
-    s->observe_on = true;
-  }
-  uint64_t n0 = s->h_st[0].n_loss;
+  const uint64_t n0 = s->h_st[0].n_loss;
   std::memset(info, 0, sizeof(*info));
+  const int64_t ncp = s->args.nc_pad;
+  double* xnext = s->tmp.p;
+  double* xm = s->tmp.p + ncp;
   for (;;) {
     if (s->h_st[0].phase == PH_DONE) {
       info->phase = 2;
@@ -709,41 +794,27 @@ void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, doubl
     launch_apply_only(s, st);
     CK_CUDA(cudaGetLastError());
     pull_state(s);
-    bool reported = s->h_st[0].n_loss != n0;
+    const bool reported = s->h_st[0].n_loss != n0;
     ColState cs = s->h_st[0];
-    // k_transpose materialises x_{t+1}; when the column just finished it
-    // does not run, so materialise into scratch instead.
-    const int64_t ncp = s->args.nc_pad;
-    const double* xnext = nullptr;
-    if (reported && cs.phase == PH_DONE) {
-      const double* cur = s->X.p + ((int64_t)cs.cur * s->R) * ncp;
-      k_materialise<<<(unsigned)ceil_div(ncp, 256), 256, 0, st>>>(s->A->ncols, s->R, 0, cur, s->dl.p, cs.rad, cs.ndiv, s->tmp.p);
-      xnext = s->tmp.p;
+    if (reported) {
+      // x_{t+1} from the pre-step pair buffer, before k_transpose moves on
+      CK_CUDA(cudaMemsetAsync(xnext, 0, sizeof(double) * ncp, st));
+      k_materialise<<<grid256(ncp), 256, 0, st>>>(s->A->ncols, col_buf(s, cs.cur, 0), cs.rad,
+                                                  cs.ndiv, xnext);
+      if (!cs.pend) extract_x(s, cs.best, 0, xm, st);
     }
     launch_transpose_only(s, st);
     CK_CUDA(cudaGetLastError());
     pull_state(s);
     if (!reported) continue;
-    cs = s->h_st[0];
     info->t = cs.t_loss;
     info->loss = cs.loss;
     info->loss_min = cs.loss_min;
     info->x_dot_delta = cs.obs_xd;
     info->delta_norm = cs.obs_dn;
     info->phase = 0;
-    if (!xnext) xnext = s->X.p + ((int64_t)cs.cur * s->R) * ncp;
-    const double* xm = cs.pend ? xnext : s->X.p + ((int64_t)cs.best * s->R) * ncp;
-    std::vector<double> tmp2;
-    if (x) {
-      scatter_perm(s->A->at.perm.p, ncp, xnext, s->A->s_out.p, st);
-      CK_CUDA(cudaMemcpyAsync(x, s->A->s_out.p, sizeof(double) * s->A->ncols, cudaMemcpyDeviceToHost, st));
-      CK_CUDA(cudaStreamSynchronize(st));
-    }
-    if (x_min) {
-      scatter_perm(s->A->at.perm.p, ncp, xm, s->A->s_out.p, st);
-      CK_CUDA(cudaMemcpyAsync(x_min, s->A->s_out.p, sizeof(double) * s->A->ncols, cudaMemcpyDeviceToHost, st));
-      CK_CUDA(cudaStreamSynchronize(st));
-    }
+    if (x) download_perm(s, xnext, x, st);
+    if (x_min) download_perm(s, cs.pend ? xnext : xm, x_min, st);
     return;
   }
 }

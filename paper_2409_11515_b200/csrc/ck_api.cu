@@ -198,6 +198,15 @@ ck_status ck_random_unit_vectors(uint64_t seed, int64_t n, int64_t count, double
   });
 }
 
+ck_status ck_uniform_in(uint64_t seed, int64_t count, double lo, double hi, double* out) {
+  return guarded([&] {
+    if (count < 0) fail(CK_ERR_INVALID_ARGUMENT, "negative size");
+    std::mt19937_64 g(seed);
+    for (int64_t i = 0; i < count; ++i)
+      out[i] = lo + (hi - lo) * (static_cast<double>(g() >> 11) * 0x1.0p-53);
+  });
+}
+
 // ---------------------------------------------- error_bounds.hpp:59-99
 ck_status ck_loose_bounds(double rn, double bn, double kappa, double* lo, double* hi) {
   return guarded([&] {

@@ -14,10 +14,6 @@ namespace ck {
 constexpr int kTile = 256;
 constexpr int kSlice = 32;
 constexpr int kSlicesPerTile = kTile / kSlice;
-// Target number of work units (CTAs) per kernel: 148 SMs x 8 resident CTAs.
-// Fixed (not queried) so the reduction tree -- and hence every result bit --
-// is identical on every device.
-constexpr int kTargetUnits = 148 * 8;
 constexpr int kMaxCols = 4;  // restarts carried as columns of one multi-vector
 
 // Error carrying a ck_status across the C++ implementation; converted at the ABI.

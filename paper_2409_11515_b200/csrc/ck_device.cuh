@@ -190,4 +190,21 @@ __device__ __forceinline__ bool elect_last_block(unsigned int* counter, unsigned
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
 
+// Loads U consecutive stored entries (stored positions j0..j0+U-1) of a
+// sliced-ELL row. All loads of the chunk are issued before any use; positions at
+// or beyond the warp-uniform slice width w are predicated off and read as
+// (column 0, value 0). Padding inside [len, w) is stored as (0, 0.0), so the
+// gathers that follow never need a bounds check.
+template <int U>
+__device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int j0, int w, int* c,
+                                           double* v) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool ok = j0 + u < w;
+    const int64_t k = base + (int64_t)(j0 + u) * kSlice;
+    c[u] = ok ? ld_stream(A.col + k) : 0;
+    v[u] = ok ? ld_stream(A.val + k) : 0.0;
+  }
+}
+
 }  // namespace ck

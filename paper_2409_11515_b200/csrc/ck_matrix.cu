@@ -148,14 +148,23 @@ __global__ void k_sell_fill(int64_t nrows_pad, const int32_t* __restrict__ perm,
 __global__ void __launch_bounds__(kTile) k_sell_spmv(SellView A, int64_t nrows_pad,
                                                      const double* __restrict__ x,
                                                      double* __restrict__ y) {
+  constexpr int U = 8;
   int64_t row = blockIdx.x * (int64_t)kTile + threadIdx.x;
   if (row >= nrows_pad) return;
-  int64_t base = A.sp[row >> 5] + (row & 31);
-  int L = A.len[row];
+  const int64_t s0 = A.sp[row >> 5], s1 = A.sp[(row >> 5) + 1];
+  const int64_t base = s0 + (row & 31);
+  const int w = (int)((s1 - s0) >> 5);
+  const int L = A.len[row];
   double acc = 0.0;
-  for (int j = 0; j < L; ++j) {
-    int64_t k = base + (int64_t)j * kSlice;
-    acc = __dadd_rn(acc, __dmul_rn(ld_stream(A.val + k), __ldg(x + ld_stream(A.col + k))));
+  for (int j0 = 0; j0 < w; j0 += U) {
+    int c[U];
+    double v[U], xg[U];
+    load_chunk<U>(A, base, j0, w, c, v);
+#pragma unroll
+    for (int u = 0; u < U; ++u) xg[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j0 + u < L) acc = __dadd_rn(acc, __dmul_rn(v[u], xg[u]));
   }
   y[row] = acc;
 }

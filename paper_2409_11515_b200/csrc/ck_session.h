@@ -39,11 +39,9 @@ struct LoopArgs {
   int64_t nr, nc, nr_pad, nc_pad;
   int tiles_A, tpu_A, units_A;
   int tiles_T, tpu_T, units_T;
-  double* X;   // [3][R][nc_pad] iterate buffers
-  double* m;   // [nc_pad][R]
-  double* v;   // [nc_pad][R]
-  double* dl;  // [nc_pad][R]  delta (pre-projection)
-  double* y;   // [nr_pad][R]  A x~
+  double2* PX;  // [3][R][nc_pad] (x, delta) pairs; three rotating iterate buffers
+  double2* MV;  // [nc_pad][R]    (m, v) Adam moments
+  double* y;    // [nr_pad][R]    A x~
   double* partA;
   double* partT;
   ColState* st;
@@ -64,7 +62,8 @@ struct ck_session_s {
   int R = 1;
   Params prm{};
   LoopArgs args{};
-  DBuf<double> X, m, v, dl, y, partA, partT, tmp;
+  DBuf<double2> PX, MV;
+  DBuf<double> y, partA, partT, tmp;
   DBuf<ColState> st;
   DBuf<Header> hdr;
   std::vector<std::mt19937_64> gens;
