@@ -80,6 +80,7 @@ typedef struct {
 
 typedef struct ck_matrix_s* ck_matrix;
 typedef struct ck_session_s* ck_session;
+typedef struct ck_lu_s* ck_lu;
 
 /* ----------------------------------------------------------------- runtime */
 const char* ck_last_error(void);
@@ -159,6 +160,39 @@ ck_status ck_session_time(ck_session s, uint64_t steps, int32_t mode, double* ms
                           double* ms_apply, double* ms_transpose);
 ck_status ck_session_result(ck_session s, int32_t column, ck_norm_result* res, double* witness);
 ck_status ck_session_free(ck_session s);
+
+/* ------------------------------------------- LU factors and the InverseOracle */
+/* lu_factorize(A, pivot_tol), lu.hpp:55-177, on the device: band LU with row
+ * partial pivoting (first largest candidate), the same singularity tests
+ * (NumericallySingular when the best pivot < pivot_tol * column max;
+ * StructurallySingular only for an empty column -- the band form does not track
+ * structure). On failure *fail_col / *fail_pivot (may be NULL) are set. */
+ck_status ck_lu_factorize(ck_matrix a, double pivot_tol, ck_lu* out, int64_t* fail_col,
+                          double* fail_pivot);
+ck_status ck_lu_free(ck_lu f);
+/* n, band widths, LUFactors::pivot_min (lu.hpp:46), device bytes. */
+ck_status ck_lu_get_info(ck_lu f, int64_t* n, int64_t* kl, int64_t* ku, double* pivot_min,
+                         int64_t* device_bytes);
+/* LAPACK band layout (ldab = 2kl+ku+1, column major, n columns) and 0-based ipiv. */
+ck_status ck_lu_export(ck_lu f, double* ab, int32_t* ipiv);
+/* lu_solve (lu.hpp:180-202): x = A^-1 b; lu_transpose_solve (lu.hpp:207-227): x = A^-T b. */
+ck_status ck_lu_solve(ck_lu f, const double* b, double* x);
+ck_status ck_lu_transpose_solve(ck_lu f, const double* b, double* x);
+/* InverseOracle::loss / grad_inverse (condest.hpp:112-123, 142-146) on the device. */
+ck_status ck_loss_inverse(ck_lu f, const double* x, double* loss);
+ck_status ck_grad_inverse(ck_lu f, const double* x, double* g);
+/* projected_adam(InverseOracle(f), cfg) / inv_norm2 (condest.hpp:138-152, 184-297, 320-322). */
+ck_status ck_inv_projected_adam(ck_lu f, const ck_adam_cfg* cfg, ck_norm_result* res,
+                                double* witness);
+/* estimate_norm(InverseOracle(f), cfg, restarts), condest.hpp:301-312. */
+ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restarts,
+                               ck_norm_result* res, double* witness);
+ck_status ck_session_create_inverse(ck_lu f, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                                    int32_t ncols, ck_session* out);
+/* cond2(A, cfg, restarts, pivot_tol), condest.hpp:341-365 (Cond2Result without the
+ * factors: has_factors reports whether they were formed). */
+ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, double pivot_tol,
+                   double* kappa, ck_norm_result* fwd, ck_norm_result* inv, int32_t* has_factors);
 
 /* ----------------------------------------------------- synthetic inputs (host) */
 /* Operators of the BASELINE.json configurations (no reference counterpart for

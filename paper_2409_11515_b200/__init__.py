@@ -11,6 +11,10 @@ from .condest import (AdamConfig, AdamState, AdamStepInfo, ExplicitOracle, Gradi
 from .errors import (CondkitError, DegenerateDirection, DeviceUnavailable, DimensionMismatch,
                      InvalidArgument, LogicError, NativeLibraryMissing, NumericallySingular,
                      StructurallySingular, ZeroRHS, ZeroSolution)
+from .error_bounds import (Bounds, BoundsReport, Verdict, VerifyOptions, kEpsMach, loose_bounds,
+                           propagate_bound, singularity_bound, tight_bounds, verify_solution)
+from .inverse import (Cond2Result, InverseOracle, LUFactors, cond2, grad_inverse, inv_norm2,
+                      lu_factorize, lu_solve, lu_transpose_solve)
 from .rng import mix_seed, random_unit_vector, random_unit_vectors
 from .sparse import DeviceMatrix, SparseMatrix, matvec, transpose_matvec
 
@@ -21,5 +25,8 @@ __all__ = [
     "DimensionMismatch", "InvalidArgument", "LogicError", "NativeLibraryMissing",
     "NumericallySingular", "StructurallySingular", "ZeroRHS", "ZeroSolution", "mix_seed",
     "random_unit_vector", "random_unit_vectors", "DeviceMatrix", "SparseMatrix", "matvec",
-    "transpose_matvec",
+    "transpose_matvec", "Bounds", "BoundsReport", "Verdict", "VerifyOptions", "kEpsMach",
+    "loose_bounds", "propagate_bound", "singularity_bound", "tight_bounds", "verify_solution",
+    "Cond2Result", "InverseOracle", "LUFactors", "cond2", "grad_inverse", "inv_norm2",
+    "lu_factorize", "lu_solve", "lu_transpose_solve",
 ]

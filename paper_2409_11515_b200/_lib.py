@@ -81,6 +81,21 @@ _SIGS = {
     "ck_session_time": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, dp, dp, dp]),
     "ck_session_result": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(NormResult), dp]),
     "ck_session_free": (C.c_int, [C.c_void_p]),
+    "ck_lu_factorize": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(C.c_void_p), i64p, dp]),
+    "ck_lu_free": (C.c_int, [C.c_void_p]),
+    "ck_lu_get_info": (C.c_int, [C.c_void_p, i64p, i64p, i64p, dp, i64p]),
+    "ck_lu_export": (C.c_int, [C.c_void_p, dp, i32p]),
+    "ck_lu_solve": (C.c_int, [C.c_void_p, dp, dp]),
+    "ck_lu_transpose_solve": (C.c_int, [C.c_void_p, dp, dp]),
+    "ck_loss_inverse": (C.c_int, [C.c_void_p, dp, dp]),
+    "ck_grad_inverse": (C.c_int, [C.c_void_p, dp, dp]),
+    "ck_inv_projected_adam": (C.c_int, [C.c_void_p, C.POINTER(AdamCfg), C.POINTER(NormResult), dp]),
+    "ck_inv_estimate_norm": (C.c_int, [C.c_void_p, C.POINTER(AdamCfg), C.c_uint64,
+                                       C.POINTER(NormResult), dp]),
+    "ck_session_create_inverse": (C.c_int, [C.c_void_p, C.POINTER(AdamCfg), u64p, C.c_int32,
+                                            C.POINTER(C.c_void_p)]),
+    "ck_cond2": (C.c_int, [C.c_void_p, C.POINTER(AdamCfg), C.c_uint64, C.c_double, dp,
+                           C.POINTER(NormResult), C.POINTER(NormResult), i32p]),
     "ck_generate": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_uint64, i64p, i64p, i64p, i32p,
                               dp]),
 }

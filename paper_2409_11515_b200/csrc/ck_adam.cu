@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "ck_common.h"
+#include "ck_control.cuh"
 #include "ck_device.cuh"
 #include "ck_internal.h"
 #include "ck_session.h"
@@ -51,92 +52,6 @@ struct Occ {
   static constexpr int apply = R == 1 ? 4 : 2;
   static constexpr int transpose = R <= 2 ? 4 : 2;
 };
-
-__device__ __forceinline__ int pick_free(int cur, int best) {
-  for (int b = 0; b < 3; ++b)
-    if (b != cur && b != best) return b;
-  return 0;
-}
-
-// DegenerateDirection handling, condest.hpp:213-219/242-256: spend one unit of
-// the 16-restart budget or stop; the host supplies the re-randomised start.
-__device__ __forceinline__ void on_degenerate(ColState& s, const Params& p) {
-  if (s.budget == 0) {
-    s.phase = PH_DONE;
-    s.converged = 0;
-    return;
-  }
-  s.budget -= 1;
-  s.phase = (s.t >= p.max_iter) ? PH_DONE : PH_WAIT;
-}
-
-__device__ __forceinline__ void begin_iteration(ColState& s, const Params& p) {
-  s.b1p = __dmul_rn(s.b1p, p.beta1);
-  s.b2p = __dmul_rn(s.b2p, p.beta2);
-  s.mc = 1.0 / (1.0 - s.b1p);
-  s.vc = 1.0 / (1.0 - s.b2p);
-}
-
-// Control step after k_apply's reductions (thread 0 of the last CTA).
-__device__ __noinline__ void control_apply(ColState* sp, const Params* pp, double N, double yn) {
-  ColState& s = *sp;
-  const Params& p = *pp;
-  s.xnorm = N;
-  s.ynorm = yn;
-  if (s.phase == PH_PRO) {
-    // First iteration after a (re)start: the gradient at x needs ||A x|| != 0.
-    s.t += 1;
-    if (yn == 0.0) {
-      on_degenerate(s, p);
-      return;
-    }
-    begin_iteration(s, p);
-    s.inv_x2 = 1.0 / (N * N);
-    s.inv_y2 = 1.0 / (yn * yn);
-    s.ndiv = 1.0;
-    s.mat = 0;
-    s.phase = PH_GRAD;
-    return;
-  }
-  // PH_APPLY: finish iteration t at x_{t+1} = x~/N.
-  if (N == 0.0 || !isfinite(N)) {
-    on_degenerate(s, p);
-    return;
-  }
-  double den = yn / N;  // ||A x_{t+1}||
-  if (den == 0.0) {
-    on_degenerate(s, p);
-    return;
-  }
-  double loss = -log(den);  // log||x_{t+1}|| - log||A x_{t+1}||, ||x_{t+1}|| = 1
-  s.loss = loss;
-  s.t_loss = s.t;
-  s.n_loss += 1;
-  bool improved = !isfinite(s.loss_min) || s.loss_min - loss > p.rel_tol * fabs(s.loss_min);
-  s.since = improved ? 0 : s.since + 1;
-  s.nxt = pick_free(s.cur, s.best);
-  s.ndiv = N;
-  if (loss < s.loss_min) {
-    s.loss_min = loss;
-    s.best = s.nxt;  // x_{t+1} lands there (k_transpose or the epilogue)
-    s.pend = 1;
-  }
-  if (s.since >= p.patience) {
-    s.phase = PH_DONE;
-    s.converged = 1;
-    return;
-  }
-  if (s.t >= p.max_iter) {
-    s.phase = PH_DONE;
-    return;
-  }
-  s.t += 1;
-  begin_iteration(s, p);
-  s.inv_x2 = 1.0;
-  s.inv_y2 = 1.0 / (den * den);
-  s.mat = 1;
-  s.phase = PH_GRAD;
-}
 
 // x~ from a stored (x, delta) pair: x - (delta - r x)  (:232, :240)
 __device__ __forceinline__ double xtilde(double2 p, double rad) {
@@ -465,7 +380,22 @@ static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
     k_apply<R, false><<<s->args.units_A, kTile, 0, st>>>(s->args);
 }
 
+void launch_inv_step(const InvArgs& a, int R, cudaStream_t st);
+void prepare_inv_step(const BandView& b, int R);
+int lu_ring_size(const BandView& b);
+void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st);
+
+static void launch_inv_half(ck_session_s* s, int half, cudaStream_t st) {
+  InvArgs a = s->iargs;
+  a.half = half;
+  launch_inv_step(a, s->R, st);
+}
+
 static void launch_apply_only(ck_session_s* s, cudaStream_t st) {
+  if (s->kind == 1) {
+    launch_inv_half(s, 1, st);
+    return;
+  }
   switch (s->R) {
     case 1: launch_apply_r<1>(s, st); break;
     case 2: launch_apply_r<2>(s, st); break;
@@ -475,6 +405,10 @@ static void launch_apply_only(ck_session_s* s, cudaStream_t st) {
 }
 
 static void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
+  if (s->kind == 1) {
+    launch_inv_half(s, 2, st);
+    return;
+  }
   const LoopArgs& a = s->args;
   switch (s->R) {
     case 1: k_transpose<1><<<a.units_T, kTile, 0, st>>>(a); break;
@@ -485,6 +419,10 @@ static void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
 }
 
 static void launch_step(ck_session_s* s, cudaStream_t st) {
+  if (s->kind == 1) {
+    launch_inv_half(s, 0, st);
+    return;
+  }
   launch_apply_only(s, st);
   launch_transpose_only(s, st);
 }
@@ -500,31 +438,53 @@ static int occ_transpose(int R) {
 }
 
 static void pull_state(ck_session_s* s) {
-  cudaStream_t st = s->A->stream;
+  cudaStream_t st = s->stream;
   CK_CUDA(cudaMemcpyAsync(s->h_st, s->st.p, sizeof(ColState) * s->R, cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaMemcpyAsync(s->h_hdr, s->hdr.p, sizeof(Header), cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
 static void push_state(ck_session_s* s) {
-  cudaStream_t st = s->A->stream;
+  cudaStream_t st = s->stream;
   CK_CUDA(cudaMemcpyAsync(s->st.p, s->h_st, sizeof(ColState) * s->R, cudaMemcpyHostToDevice, st));
   CK_CUDA(cudaMemcpyAsync(s->hdr.p, s->h_hdr, sizeof(Header), cudaMemcpyHostToDevice, st));
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
 static double2* col_buf(ck_session_s* s, int b, int c) {
-  return s->PX.p + ((int64_t)b * s->R + c) * s->args.nc_pad;
+  return s->PX.p + ((int64_t)b * s->R + c) * s->npad;
+}
+
+// host vector (original order) -> internal plain vector `dst` (npad doubles)
+static void to_internal(ck_session_s* s, const double* host, double* dst, cudaStream_t st) {
+  if (s->perm) {
+    CK_CUDA(cudaMemcpyAsync(s->tmp.p, host, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
+    gather_perm(s->perm, s->npad, s->tmp.p, dst, st);
+  } else {
+    CK_CUDA(cudaMemcpyAsync(dst, host, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
+  }
+}
+
+// internal plain vector -> host vector (original order); `src` may be s->tmp + npad
+static void to_host(ck_session_s* s, const double* src, double* host, cudaStream_t st) {
+  const double* out = src;
+  if (s->perm) {
+    double* scratch = s->tmp.p;
+    scatter_perm(s->perm, s->npad, src, scratch, st);
+    out = scratch;
+  }
+  CK_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * s->n, cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
 }
 
 // Upload a fresh start vector for column c (original order) into buffer b:
-// (x, delta = 0) pairs in the permuted column space, m = v = 0.
+// (x, delta = 0) pairs in the internal (permuted) space, m = v = 0.
 static void load_start(ck_session_s* s, int c, int b, const double* x) {
-  cudaStream_t st = s->A->stream;
-  const int64_t nc = s->A->ncols, ncp = s->args.nc_pad;
-  CK_CUDA(cudaMemcpyAsync(s->tmp.p, x, sizeof(double) * nc, cudaMemcpyHostToDevice, st));
+  cudaStream_t st = s->stream;
+  const int64_t ncp = s->npad;
   double* perm = s->tmp.p + ncp;
-  gather_perm(s->A->at.perm.p, ncp, s->tmp.p, perm, st);
+  CK_CUDA(cudaMemsetAsync(perm, 0, sizeof(double) * ncp, st));
+  to_internal(s, x, perm, st);
   k_store_x<<<grid256(ncp), 256, 0, st>>>(ncp, perm, col_buf(s, b, c));
   k_zero_moments<<<grid256(ncp), 256, 0, st>>>(ncp, s->R, c, s->MV.p);
   CK_CUDA(cudaGetLastError());
@@ -538,7 +498,7 @@ static void service_restarts(ck_session_s* s) {
   for (int c = 0; c < s->R; ++c) {
     ColState& cs = s->h_st[c];
     if (cs.phase != PH_WAIT) continue;
-    random_unit_vector_host(&s->gens[c], s->A->ncols, s->hx.data());
+    random_unit_vector_host(&s->gens[c], s->n, s->hx.data());
     const int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
     load_start(s, c, b, s->hx.data());
     cs.cur = b;
@@ -558,7 +518,7 @@ static void service_restarts(ck_session_s* s) {
 }
 
 static void build_graph(ck_session_s* s, int steps) {
-  cudaStream_t st = s->A->stream;
+  cudaStream_t st = s->stream;
   cudaGraph_t g;
   CK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   for (int k = 0; k < steps; ++k) launch_step(s, st);
@@ -568,55 +528,22 @@ static void build_graph(ck_session_s* s, int steps) {
   s->gsteps = steps;
 }
 
-void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
-                    const uint64_t* seeds, int R) {
-  if (R < 1 || R > kMaxCols) fail(CK_ERR_INVALID_ARGUMENT, "session columns must be 1..4");
-  if (A->ncols == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
-  s->A = A;
-  s->R = R;
-  s->prm = Params{cfg->alpha, cfg->beta1, cfg->beta2, cfg->eps_stab, cfg->rel_tol, cfg->max_iter,
-                  cfg->patience};
-  LoopArgs& a = s->args;
-  a.A = view(A->a);
-  a.AT = view(A->at);
-  a.nr = A->nrows;
-  a.nc = A->ncols;
-  a.nr_pad = A->a.nrows_pad;
-  a.nc_pad = A->at.nrows_pad;
-  a.tiles_A = (int)(std::max(a.nr_pad, a.nc_pad) / kTile);
-  const int64_t unitsA = 148 * occ_apply(R), unitsT = 148 * occ_transpose(R);
-  a.tpu_A = (int)std::max<int64_t>(1, ceil_div(a.tiles_A, unitsA));
-  a.units_A = (int)ceil_div(a.tiles_A, a.tpu_A);
-  a.tiles_T = (int)(a.nc_pad / kTile);
-  a.tpu_T = (int)std::max<int64_t>(1, ceil_div(a.tiles_T, unitsT));
-  a.units_T = (int)ceil_div(a.tiles_T, a.tpu_T);
-  cudaStream_t st = A->stream;
-  s->PX.alloc(3 * R * a.nc_pad);
-  s->MV.alloc(a.nc_pad * R);
-  s->y.alloc(std::max(a.nr_pad, a.nc_pad) * R);
-  s->partA.alloc((int64_t)a.units_A * R * kPA);
-  s->partT.alloc((int64_t)a.units_T * R * kPT);
-  s->tmp.alloc(2 * std::max(a.nr_pad, a.nc_pad));
-  s->st.alloc(R);
-  s->hdr.alloc(1);
+// Common part of session creation: state buffers, x0 per column, graphs.
+static void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                                int R, int64_t ywords, double bytes_per_step) {
+  cudaStream_t st = s->stream;
+  s->thalf = std::max(s->npad, ywords / R);
+  s->tmp.alloc(2 * s->thalf);
   CK_CUDA(cudaMemsetAsync(s->PX.p, 0, s->PX.bytes(), st));
   CK_CUDA(cudaMemsetAsync(s->MV.p, 0, s->MV.bytes(), st));
   CK_CUDA(cudaMemsetAsync(s->y.p, 0, s->y.bytes(), st));
-  a.PX = s->PX.p;
-  a.MV = s->MV.p;
-  a.y = s->y.p;
-  a.partA = s->partA.p;
-  a.partT = s->partT.p;
-  a.st = s->st.p;
-  a.hdr = s->hdr.p;
-  a.prm = s->prm;
   CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_st), sizeof(ColState) * R));
   CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_hdr), sizeof(Header)));
-  s->hx.resize((size_t)A->ncols);
+  s->hx.resize((size_t)s->n);
   s->gens.clear();
   for (int c = 0; c < R; ++c) {
     s->gens.emplace_back(seeds[c]);
-    random_unit_vector_host(&s->gens[c], A->ncols, s->hx.data());  // x0, rng.hpp:68-77
+    random_unit_vector_host(&s->gens[c], s->n, s->hx.data());  // x0, rng.hpp:68-77
     load_start(s, c, 0, s->hx.data());
     ColState cs{};
     cs.phase = cfg->max_iter == 0 ? PH_DONE : PH_PRO;
@@ -636,14 +563,99 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   *s->h_hdr = h;
   push_state(s);
   // chunk length: about 4 ms of device work per host round trip, 4..256 steps
-  const double bytes_per_step = 24.0 * (double)A->nnz + 100.0 * (double)A->ncols * R;
   const int steps =
       (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
   build_graph(s, steps);
 }
 
+void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
+                    const uint64_t* seeds, int R) {
+  if (R < 1 || R > kMaxCols) fail(CK_ERR_INVALID_ARGUMENT, "session columns must be 1..4");
+  if (A->ncols == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
+  s->kind = 0;
+  s->A = A;
+  s->R = R;
+  s->stream = A->stream;
+  s->device = A->device;
+  s->n = A->ncols;
+  s->npad = A->at.nrows_pad;
+  s->perm = A->at.perm.p;
+  s->prm = Params{cfg->alpha, cfg->beta1, cfg->beta2, cfg->eps_stab, cfg->rel_tol, cfg->max_iter,
+                  cfg->patience};
+  LoopArgs& a = s->args;
+  a.A = view(A->a);
+  a.AT = view(A->at);
+  a.nr = A->nrows;
+  a.nc = A->ncols;
+  a.nr_pad = A->a.nrows_pad;
+  a.nc_pad = A->at.nrows_pad;
+  a.tiles_A = (int)(std::max(a.nr_pad, a.nc_pad) / kTile);
+  const int64_t unitsA = 148 * occ_apply(R), unitsT = 148 * occ_transpose(R);
+  a.tpu_A = (int)std::max<int64_t>(1, ceil_div(a.tiles_A, unitsA));
+  a.units_A = (int)ceil_div(a.tiles_A, a.tpu_A);
+  a.tiles_T = (int)(a.nc_pad / kTile);
+  a.tpu_T = (int)std::max<int64_t>(1, ceil_div(a.tiles_T, unitsT));
+  a.units_T = (int)ceil_div(a.tiles_T, a.tpu_T);
+  s->partA.alloc((int64_t)a.units_A * R * kPA);
+  s->partT.alloc((int64_t)a.units_T * R * kPT);
+  const int64_t yw = std::max(a.nr_pad, a.nc_pad) * R;
+  a.prm = s->prm;
+  s->PX.alloc(3 * R * s->npad);
+  s->MV.alloc(s->npad * R);
+  s->y.alloc(yw);
+  s->st.alloc(R);
+  s->hdr.alloc(1);
+  a.PX = s->PX.p;
+  a.MV = s->MV.p;
+  a.y = s->y.p;
+  a.partA = s->partA.p;
+  a.partT = s->partT.p;
+  a.st = s->st.p;
+  a.hdr = s->hdr.p;
+  const double bytes_per_step = 24.0 * (double)A->nnz + 100.0 * (double)A->ncols * R;
+  session_init_common(s, cfg, seeds, R, yw, bytes_per_step);
+}
+
+void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg,
+                            const uint64_t* seeds, int R) {
+  if (R < 1 || R > kMaxCols) fail(CK_ERR_INVALID_ARGUMENT, "session columns must be 1..4");
+  if (lu->n == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
+  s->kind = 1;
+  s->lu = lu;
+  s->A = nullptr;
+  s->R = R;
+  s->stream = lu->stream;
+  s->device = lu->device;
+  s->n = lu->n;
+  s->npad = lu->n;
+  s->perm = nullptr;
+  s->prm = Params{cfg->alpha, cfg->beta1, cfg->beta2, cfg->eps_stab, cfg->rel_tol, cfg->max_iter,
+                  cfg->patience};
+  const BandView b = lu->view();
+  prepare_inv_step(b, R);
+  const int64_t yw = s->n * R;
+  s->PX.alloc(3 * R * s->npad);
+  s->MV.alloc(s->npad * R);
+  s->y.alloc(yw);
+  s->st.alloc(R);
+  s->hdr.alloc(1);
+  InvArgs& a = s->iargs;
+  a.b = b;
+  a.n = s->n;
+  a.ring_size = lu_ring_size(b);
+  a.PX = s->PX.p;
+  a.MV = s->MV.p;
+  a.y = s->y.p;
+  a.st = s->st.p;
+  a.hdr = s->hdr.p;
+  a.prm = s->prm;
+  a.half = 0;
+  const double bytes_per_step = 8.0 * 4.0 * (double)(2 * lu->kl + lu->ku + 1) * (double)lu->n;
+  session_init_common(s, cfg, seeds, R, yw, bytes_per_step * 50.0);
+}
+
 void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished) {
-  cudaStream_t st = s->A->stream;
+  cudaStream_t st = s->stream;
   uint64_t done = 0;
   *finished = 0;
   for (;;) {
@@ -668,10 +680,10 @@ void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished) {
 
 void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_total,
                   double* ms_apply, double* ms_transpose) {
-  cudaStream_t st = s->A->stream;
+  cudaStream_t st = s->stream;
   pull_state(s);
   if (s->h_hdr->nwait > 0) service_restarts(s);
-  if (mode == 1) {  // whole graph chunks, no per-kernel events
+  if (mode == 1 || s->kind == 1) {  // whole steps (graph chunks), no per-kernel split
     cudaEvent_t e0, e1;
     CK_CUDA(cudaEventCreate(&e0));
     CK_CUDA(cudaEventCreate(&e1));
@@ -686,8 +698,8 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
     float ms = 0.f;
     CK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     *ms_total = ms;
-    *ms_apply = -1.0;
-    *ms_transpose = -1.0;
+    *ms_apply = s->kind == 1 ? ms : -1.0;
+    *ms_transpose = s->kind == 1 ? 0.0 : -1.0;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return;
@@ -706,11 +718,11 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
   CK_CUDA(cudaGetLastError());
   double ta = 0.0, tt = 0.0;
   for (uint64_t k = 0; k < steps; ++k) {
-    float a = 0.f, b = 0.f;
-    CK_CUDA(cudaEventElapsedTime(&a, ev[2 * k], ev[2 * k + 1]));
-    CK_CUDA(cudaEventElapsedTime(&b, ev[2 * k + 1], ev[2 * k + 2]));
-    ta += a;
-    tt += b;
+    float x = 0.f, y = 0.f;
+    CK_CUDA(cudaEventElapsedTime(&x, ev[2 * k], ev[2 * k + 1]));
+    CK_CUDA(cudaEventElapsedTime(&y, ev[2 * k + 1], ev[2 * k + 2]));
+    ta += x;
+    tt += y;
   }
   float tot = 0.f;
   CK_CUDA(cudaEventElapsedTime(&tot, ev[0], ev[2 * steps]));
@@ -720,24 +732,37 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
   *ms_transpose = tt;
 }
 
-// x of buffer b / column c as a plain permuted vector in `out` (nc_pad doubles).
+// x of buffer b / column c as a plain internal vector in `out` (npad doubles).
 static void extract_x(ck_session_s* s, int b, int c, double* out, cudaStream_t st) {
-  k_extract_x<<<grid256(s->args.nc_pad), 256, 0, st>>>(s->args.nc_pad, col_buf(s, b, c), out);
+  k_extract_x<<<grid256(s->npad), 256, 0, st>>>(s->npad, col_buf(s, b, c), out);
   CK_CUDA(cudaGetLastError());
+}
+
+// ||Op v|| for an internal plain vector v (witness re-check, condest.hpp:284-289).
+static double op_norm(ck_session_s* s, const double* v, cudaStream_t st) {
+  if (s->kind == 0) {
+    matrix_apply_perm(s->A, v, s->tmp.p, st);
+    return device_norm(s->tmp.p, s->A->a.nrows_pad, s->A->s_red.p, st);
+  }
+  double* w = s->lu->work.p;
+  CK_CUDA(cudaMemcpyAsync(w, v, sizeof(double) * s->n, cudaMemcpyDeviceToDevice, st));
+  double* xs[1] = {w};
+  lu_solve_launch(s->lu, xs, 1, false, st);
+  return device_norm(w, s->n, w + s->n, st);
 }
 
 // Final NormEstimate for column c (condest.hpp:278-296).
 void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness) {
   if (c < 0 || c >= s->R) fail(CK_ERR_INVALID_ARGUMENT, "column out of range");
-  cudaStream_t st = s->A->stream;
+  cudaStream_t st = s->stream;
   pull_state(s);
   ColState& cs = s->h_st[c];
-  const int64_t ncp = s->args.nc_pad;
-  double* xbest = s->tmp.p + ncp;  // plain copy of x_min (permuted space)
+  const int64_t ncp = s->npad;
+  double* xbest = s->tmp.p + s->thalf;  // plain copy of x_min (internal order)
   if (cs.pend) {  // x_{t+1} became the best but was never materialised
     CK_CUDA(cudaMemsetAsync(xbest, 0, sizeof(double) * ncp, st));
-    k_materialise<<<grid256(ncp), 256, 0, st>>>(s->A->ncols, col_buf(s, cs.cur, c), cs.rad,
-                                                cs.ndiv, xbest);
+    k_materialise<<<grid256(ncp), 256, 0, st>>>(s->n, col_buf(s, cs.cur, c), cs.rad, cs.ndiv,
+                                                xbest);
     CK_CUDA(cudaGetLastError());
   } else {
     extract_x(s, cs.best, c, xbest, st);
@@ -747,9 +772,7 @@ void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness
   res->_pad = 0;
   if (std::isfinite(cs.loss_min)) {
     res->value = std::exp(-cs.loss_min);
-    // witness re-check, condest.hpp:284-289
-    matrix_apply_perm(s->A, xbest, s->tmp.p, st);
-    const double chk = device_norm(s->tmp.p, s->A->a.nrows_pad, s->A->s_red.p, st);
+    const double chk = op_norm(s, xbest, st);
     if (!(std::fabs(chk - res->value) <= 1e-12 * std::max(res->value, chk)))
       fail(CK_ERR_LOGIC, "norm estimate does not match ||Op witness||");
   } else {
@@ -757,32 +780,31 @@ void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness
     res->converged = 0;
   }
   if (witness) {
-    scatter_perm(s->A->at.perm.p, ncp, xbest, s->tmp.p, st);
-    CK_CUDA(cudaMemcpyAsync(witness, s->tmp.p, sizeof(double) * s->A->ncols,
-                            cudaMemcpyDeviceToHost, st));
-    CK_CUDA(cudaStreamSynchronize(st));
+    if (s->perm) {
+      // to_host uses tmp[0, npad) as scratch; xbest lives at tmp + npad
+      to_host(s, xbest, witness, st);
+    } else {
+      CK_CUDA(cudaMemcpyAsync(witness, xbest, sizeof(double) * s->n, cudaMemcpyDeviceToHost, st));
+      CK_CUDA(cudaStreamSynchronize(st));
+    }
   }
-}
-
-static void download_perm(ck_session_s* s, const double* xperm, double* host, cudaStream_t st) {
-  scatter_perm(s->A->at.perm.p, s->args.nc_pad, xperm, s->A->s_out.p, st);
-  CK_CUDA(cudaMemcpyAsync(host, s->A->s_out.p, sizeof(double) * s->A->ncols,
-                          cudaMemcpyDeviceToHost, st));
-  CK_CUDA(cudaStreamSynchronize(st));
 }
 
 // Observer mode (AdamObserver, condest.hpp:234-238, 268-271) for column 0:
 // advances until column 0 evaluates a loss (or finishes) and reports the
 // iteration's scalars and, optionally, x_{t+1} and x_min.
 void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, double* x_min) {
-  cudaStream_t st = s->A->stream;
+  cudaStream_t st = s->stream;
   s->observe_on = true;  // k_apply<R, true> from here on (no graphs in this mode)
   pull_state(s);
   const uint64_t n0 = s->h_st[0].n_loss;
   std::memset(info, 0, sizeof(*info));
-  const int64_t ncp = s->args.nc_pad;
-  double* xnext = s->tmp.p;
-  double* xm = s->tmp.p + ncp;
+  const int64_t ncp = s->npad;
+  // scratch: y work vector is free between steps only for the explicit kind;
+  // use dedicated buffers
+  if (s->obs.n < 2 * ncp) s->obs.alloc(2 * ncp);
+  double* xnext = s->obs.p;
+  double* xm = s->obs.p + ncp;
   for (;;) {
     if (s->h_st[0].phase == PH_DONE) {
       info->phase = 2;
@@ -797,10 +819,10 @@ void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, doubl
     const bool reported = s->h_st[0].n_loss != n0;
     ColState cs = s->h_st[0];
     if (reported) {
-      // x_{t+1} from the pre-step pair buffer, before k_transpose moves on
+      // x_{t+1} from the pre-step pair buffer, before the transpose half moves on
       CK_CUDA(cudaMemsetAsync(xnext, 0, sizeof(double) * ncp, st));
-      k_materialise<<<grid256(ncp), 256, 0, st>>>(s->A->ncols, col_buf(s, cs.cur, 0), cs.rad,
-                                                  cs.ndiv, xnext);
+      k_materialise<<<grid256(ncp), 256, 0, st>>>(s->n, col_buf(s, cs.cur, 0), cs.rad, cs.ndiv,
+                                                  xnext);
       if (!cs.pend) extract_x(s, cs.best, 0, xm, st);
     }
     launch_transpose_only(s, st);
@@ -813,8 +835,8 @@ void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, doubl
     info->x_dot_delta = cs.obs_xd;
     info->delta_norm = cs.obs_dn;
     info->phase = 0;
-    if (x) download_perm(s, xnext, x, st);
-    if (x_min) download_perm(s, cs.pend ? xnext : xm, x_min, st);
+    if (x) to_host(s, xnext, x, st);
+    if (x_min) to_host(s, cs.pend ? xnext : xm, x_min, st);
     return;
   }
 }

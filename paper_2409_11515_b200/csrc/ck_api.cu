@@ -11,6 +11,7 @@
 
 #include "ck_common.h"
 #include "ck_internal.h"
+#include "ck_lu.h"
 #include "ck_session.h"
 
 namespace ck {
@@ -110,6 +111,12 @@ void random_unit_vector_host(void* engine, int64_t n, double* out) {
 
 static void check_cfg(const ck_adam_cfg* cfg) {
   if (cfg == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "cfg is NULL");
+}
+
+static ck_session_s* S(ck_session s) {
+  if (s == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "session handle is NULL");
+  CK_CUDA(cudaSetDevice(s->device));
+  return s;
 }
 
 static ck_matrix_s* M(ck_matrix a) {
@@ -353,14 +360,14 @@ ck_status ck_session_create(ck_matrix a, const ck_adam_cfg* cfg, const uint64_t*
 
 ck_status ck_session_run(ck_session s, uint64_t max_steps, int32_t* finished) {
   return guarded([&] {
-    M(s->A);
+    S(s);
     session_run(s, max_steps, finished);
   });
 }
 
 ck_status ck_session_step_observed(ck_session s, ck_step_info* info, double* x, double* x_min) {
   return guarded([&] {
-    M(s->A);
+    S(s);
     if (s->R != 1) fail(CK_ERR_INVALID_ARGUMENT, "observer mode needs a single-column session");
     session_step_observed(s, info, x, x_min);
   });
@@ -369,14 +376,14 @@ ck_status ck_session_step_observed(ck_session s, ck_step_info* info, double* x, 
 ck_status ck_session_time(ck_session s, uint64_t steps, int32_t mode, double* ms_total,
                           double* ms_apply, double* ms_transpose) {
   return guarded([&] {
-    M(s->A);
+    S(s);
     session_time(s, steps, mode, ms_total, ms_apply, ms_transpose);
   });
 }
 
 ck_status ck_session_result(ck_session s, int32_t column, ck_norm_result* res, double* witness) {
   return guarded([&] {
-    M(s->A);
+    S(s);
     session_result(s, column, res, witness);
   });
 }
@@ -384,8 +391,8 @@ ck_status ck_session_result(ck_session s, int32_t column, ck_norm_result* res, d
 ck_status ck_session_free(ck_session s) {
   return guarded([&] {
     if (!s) return;
-    cudaSetDevice(s->A->device);
-    cudaStreamSynchronize(s->A->stream);
+    cudaSetDevice(s->device);
+    cudaStreamSynchronize(s->stream);
     delete s;
   });
 }
@@ -435,6 +442,236 @@ ck_status ck_estimate_norm(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restart
         }
       }
     }
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ LU / InverseOracle
+namespace ck {
+void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_col,
+                  double* fail_pivot);
+void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st);
+void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg,
+                            const uint64_t* seeds, int R);
+
+static ck_lu_s* LU(ck_lu f) {
+  if (f == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "LU handle is NULL");
+  CK_CUDA(cudaSetDevice(f->device));
+  return f;
+}
+
+static void lu_solve_host(ck_lu_s* f, const double* b, double* x, bool transpose) {
+  cudaStream_t st = f->stream;
+  double* w = f->work.p;
+  CK_CUDA(cudaMemcpyAsync(w, b, sizeof(double) * f->n, cudaMemcpyHostToDevice, st));
+  double* xs[1] = {w};
+  lu_solve_launch(f, xs, 1, transpose, st);
+  CK_CUDA(cudaMemcpyAsync(x, w, sizeof(double) * f->n, cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+}
+
+// estimate_norm over an already created session kind (restart groups of <= 4).
+template <class MakeSession>
+static void estimate_norm_groups(const ck_adam_cfg* cfg, uint64_t restarts, ck_norm_result* res,
+                                 double* witness, MakeSession&& make) {
+  if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
+  bool have = false;
+  for (uint64_t r0 = 0; r0 < restarts; r0 += kMaxCols) {
+    const int R = (int)std::min<uint64_t>(kMaxCols, restarts - r0);
+    std::vector<uint64_t> seeds(R);
+    for (int c = 0; c < R; ++c) {
+      const uint64_t r = r0 + c;
+      seeds[c] = r == 0 ? cfg->seed : ck_mix_seed(cfg->seed, r);
+    }
+    ck_session_s s;
+    make(&s, seeds.data(), R);
+    int32_t fin = 0;
+    session_run(&s, 0, &fin);
+    for (int c = 0; c < R; ++c) {
+      ck_norm_result e{};
+      session_result(&s, c, &e, nullptr);
+      if (!have || e.value > res->value) {
+        *res = e;
+        have = true;
+        if (witness) session_result(&s, c, &e, witness);
+      }
+    }
+  }
+}
+}  // namespace ck
+
+extern "C" {
+
+ck_status ck_lu_factorize(ck_matrix a, double pivot_tol, ck_lu* out, int64_t* fail_col,
+                          double* fail_pivot) {
+  return guarded([&] {
+    if (out == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "out is NULL");
+    auto* f = new ck_lu_s();
+    try {
+      lu_factorize(f, M(a), pivot_tol, fail_col, fail_pivot);
+    } catch (...) {
+      delete f;
+      throw;
+    }
+    *out = f;
+  });
+}
+
+ck_status ck_lu_free(ck_lu f) {
+  return guarded([&] {
+    if (!f) return;
+    cudaSetDevice(f->device);
+    delete f;
+  });
+}
+
+ck_status ck_lu_get_info(ck_lu f, int64_t* n, int64_t* kl, int64_t* ku, double* pivot_min,
+                         int64_t* device_bytes) {
+  return guarded([&] {
+    LU(f);
+    *n = f->n;
+    *kl = f->kl;
+    *ku = f->ku;
+    *pivot_min = f->pivot_min;
+    *device_bytes = f->ab.bytes() + f->lb.bytes() + f->ipiv.bytes();
+  });
+}
+
+ck_status ck_lu_export(ck_lu f, double* ab, int32_t* ipiv) {
+  return guarded([&] {
+    LU(f);
+    cudaStream_t st = f->stream;
+    if (ab) CK_CUDA(cudaMemcpyAsync(ab, f->ab.p, f->ab.bytes(), cudaMemcpyDeviceToHost, st));
+    if (ipiv) CK_CUDA(cudaMemcpyAsync(ipiv, f->ipiv.p, sizeof(int32_t) * f->n, cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+ck_status ck_lu_solve(ck_lu f, const double* b, double* x) {
+  return guarded([&] { lu_solve_host(LU(f), b, x, false); });
+}
+
+ck_status ck_lu_transpose_solve(ck_lu f, const double* b, double* x) {
+  return guarded([&] { lu_solve_host(LU(f), b, x, true); });
+}
+
+ck_status ck_session_create_inverse(ck_lu f, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                                    int32_t ncols, ck_session* out) {
+  return guarded([&] {
+    check_cfg(cfg);
+    auto* s = new ck_session_s();
+    try {
+      session_create_inverse(s, LU(f), cfg, seeds, ncols);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+ck_status ck_inv_projected_adam(ck_lu f, const ck_adam_cfg* cfg, ck_norm_result* res,
+                                double* witness) {
+  return guarded([&] {
+    check_cfg(cfg);
+    ck_session_s s;
+    uint64_t seed = cfg->seed;
+    session_create_inverse(&s, LU(f), cfg, &seed, 1);
+    int32_t fin = 0;
+    session_run(&s, 0, &fin);
+    session_result(&s, 0, res, witness);
+  });
+}
+
+ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restarts,
+                               ck_norm_result* res, double* witness) {
+  return guarded([&] {
+    check_cfg(cfg);
+    LU(f);
+    estimate_norm_groups(cfg, restarts, res, witness, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+      session_create_inverse(s, f, cfg, seeds, R);
+    });
+  });
+}
+
+// cond2, condest.hpp:341-365: ||A|| by estimate_norm on A, then the LU with
+// pivot_tol and ||A^-1|| with seed mix_seed(seed, 0x1234); a singular
+// factorisation yields kappa = +inf (no error).
+ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, double pivot_tol,
+                   double* kappa, ck_norm_result* fwd, ck_norm_result* inv, int32_t* has_factors) {
+  return guarded([&] {
+    check_cfg(cfg);
+    ck_matrix_s* m = M(a);
+    if (m->nrows != m->ncols) fail(CK_ERR_DIMENSION, "cond2: matrix must be square");
+    estimate_norm_groups(cfg, restarts, fwd, nullptr, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+      session_create(s, m, cfg, seeds, R);
+    });
+    *inv = ck_norm_result{};
+    *has_factors = 0;
+    ck_lu_s f;
+    try {
+      lu_factorize(&f, m, pivot_tol, nullptr, nullptr);
+    } catch (const Error& e) {
+      if (e.code == CK_ERR_STRUCT_SINGULAR || e.code == CK_ERR_NUM_SINGULAR) {
+        inv->value = std::numeric_limits<double>::infinity();
+        *kappa = std::numeric_limits<double>::infinity();
+        return;
+      }
+      throw;
+    }
+    ck_adam_cfg ci = *cfg;
+    ci.seed = ck_mix_seed(cfg->seed, 0x1234);
+    estimate_norm_groups(&ci, restarts, inv, nullptr, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+      session_create_inverse(s, &f, &ci, seeds, R);
+    });
+    *kappa = fwd->value * inv->value;
+    *has_factors = 1;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// loss / grad of the InverseOracle (condest.hpp:112-123, 142-146) on the device.
+ck_status ck_loss_inverse(ck_lu f, const double* x, double* loss) {
+  return guarded([&] {
+    ck_lu_s* F = LU(f);
+    cudaStream_t st = F->stream;
+    const int64_t n = F->n;
+    double* w = F->work.p;
+    double* red = F->work.p + 2 * n;
+    CK_CUDA(cudaMemcpyAsync(w, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    const double xn = device_norm(w, n, red, st);
+    double* xs[1] = {w};
+    lu_solve_launch(F, xs, 1, false, st);
+    const double rn = device_norm(w, n, red, st);
+    if (rn == 0.0) fail(CK_ERR_INVALID_ARGUMENT, "operator maps direction to zero (DegenerateDirection)");
+    *loss = std::log(xn) - std::log(rn);
+  });
+}
+
+ck_status ck_grad_inverse(ck_lu f, const double* x, double* g) {
+  return guarded([&] {
+    ck_lu_s* F = LU(f);
+    cudaStream_t st = F->stream;
+    const int64_t n = F->n;
+    double* w = F->work.p;
+    double* red = F->work.p + 2 * n;
+    CK_CUDA(cudaMemcpyAsync(w, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    double* xs[1] = {w};
+    lu_solve_launch(F, xs, 1, false, st);
+    const double rn = device_norm(w, n, red, st);
+    if (rn == 0.0) fail(CK_ERR_INVALID_ARGUMENT, "operator maps direction to zero (DegenerateDirection)");
+    lu_solve_launch(F, xs, 1, true, st);
+    std::vector<double> s((size_t)n), hx(x, x + n);
+    CK_CUDA(cudaMemcpyAsync(s.data(), w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    // ||x|| of the host input (two_norm, exact mirror) and the combine (:117-121)
+    const double xn = two_norm_seq(hx.data(), n);
+    const double inv_x2 = 1.0 / (xn * xn), inv_r2 = 1.0 / (rn * rn);
+    for (int64_t i = 0; i < n; ++i) g[i] = x[i] * inv_x2 - s[(size_t)i] * inv_r2;
   });
 }
 

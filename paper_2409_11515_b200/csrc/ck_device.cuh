@@ -9,6 +9,9 @@
 
 namespace ck {
 
+__host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
+
 // ---------------------------------------------------------------------------
 // Overflow-safe sum of squares in one pass (the two-pass amax/scale scheme of
 // two_norm, sparse.hpp:175-186, folded into a running power-of-two scale):

@@ -1,0 +1,226 @@
+// Projected Adam on Op = A^{-1} (InverseOracle, condest.hpp:109-152) through the
+// device band LU (ck_lu.cu). One CTA owns the whole iteration -- the solves are
+// a single dependency chain each -- and one launch is one loop trip:
+//
+//   x~ = x - (delta - r x)          ||x~|| (double-double)
+//   y' = U^{-1} L^{-1} P x~         ||y'|| (scaled sum of squares)   -> control
+//   z  = P^T L^{-T} U^{-T} y'       (grad_inverse, :112-123)
+//   Adam / projection on (x, delta), (m, v); r = x.delta             -> control
+//
+// State layout and control are those of the explicit path (ck_adam.cu), so the
+// host session, restarts, best tracking and observer mode are shared.
+#include <cmath>
+
+#include "ck_common.h"
+#include "ck_device.cuh"
+#include "ck_internal.h"
+#include "ck_control.cuh"
+#include "ck_lu.h"
+#include "ck_lu_sweeps.cuh"
+#include "ck_session.h"
+
+namespace ck {
+
+__device__ __forceinline__ double xtilde_inv(double2 p, double rad) {
+  return __dsub_rn(p.x, __dsub_rn(p.y, __dmul_rn(rad, p.x)));
+}
+
+template <int R>
+__global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvArgs a) {
+  extern __shared__ double smem[];
+  __shared__ double s_h[32], s_l[32];
+  __shared__ int s_e[32], s_f[32];
+  __shared__ double s_res[R][4];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t n = a.n;
+  double* ys[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) ys[r] = a.y + (int64_t)(r < R ? r : 0) * n;
+
+  // ---------------- apply half: y' = A^{-1} x~ and the control step
+  bool act[R], pro[R];
+  double rad[R];
+  const double2* xc[R];
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int ph = a.st[r].phase;
+    act[r] = ph == PH_PRO || ph == PH_APPLY;
+    pro[r] = ph == PH_PRO;
+    rad[r] = pro[r] ? 0.0 : a.st[r].rad;
+    xc[r] = a.PX + ((int64_t)a.st[r].cur * R + r) * n;
+    any |= act[r];
+  }
+  if (any && a.half != 2) {
+    DD dd[R];
+    ES dn[R];
+    double xd[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      dd[r] = dd_zero();
+      dn[r] = es_zero();
+      xd[r] = 0.0;
+    }
+    for (int64_t i = tid; i < n; i += nt) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double2 p = xc[r][i];
+        const double xt = xtilde_inv(p, rad[r]);
+        ys[r][i] = xt;
+        if (act[r]) {
+          dd_add_sq(dd[r], xt);
+          if (!pro[r]) {
+            const double dp = __dsub_rn(p.y, __dmul_rn(rad[r], p.x));
+            xd[r] = __fma_rn(p.x, dp, xd[r]);
+            es_add(dn[r], dp);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      DD d = block_dd(dd[r], s_h, s_l);
+      double x2 = block_sum(xd[r], s_h);
+      ES e2 = block_es(dn[r], s_h, s_e, s_f);
+      if (tid == 0) {
+        s_res[r][0] = sqrt(__dadd_rn(d.hi, d.lo));
+        s_res[r][2] = x2;
+        s_res[r][3] = es_norm(e2);
+      }
+    }
+    __syncthreads();
+    inv_solve<R>(a.b, ys, smem, a.ring_size, false);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      ES e = es_zero();
+      for (int64_t i = tid; i < n; i += nt) es_add(e, ys[r][i]);
+      e = block_es(e, s_h, s_e, s_f);
+      if (tid == 0) s_res[r][1] = es_norm(e);
+    }
+    if (tid == 0) {
+      for (int r = 0; r < R; ++r) {
+        ColState* s = a.st + r;
+        const int ph = s->phase;
+        if (ph == PH_PRO || ph == PH_APPLY) {
+          if (ph == PH_APPLY) {
+            s->obs_xd = s_res[r][2];
+            s->obs_dn = s_res[r][3];
+          }
+          control_apply(s, &a.prm, s_res[r][0], s_res[r][1]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---------------- transpose half: z = A^{-T} y', Adam, r = x.delta
+  bool grad[R], mat[R];
+  double ndiv[R], ix2[R], iy2[R], mc[R], vc[R];
+  double2* xn_out[R];
+  bool anyg = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const ColState& s = a.st[r];
+    grad[r] = s.phase == PH_GRAD;
+    mat[r] = s.mat != 0;
+    rad[r] = s.rad;
+    ndiv[r] = s.ndiv;
+    ix2[r] = s.inv_x2;
+    iy2[r] = s.inv_y2;
+    mc[r] = s.mc;
+    vc[r] = s.vc;
+    xc[r] = a.PX + ((int64_t)s.cur * R + r) * n;
+    xn_out[r] = a.PX + ((int64_t)(mat[r] ? s.nxt : s.cur) * R + r) * n;
+    anyg |= grad[r];
+  }
+  if (anyg && a.half != 1) {
+    inv_solve<R>(a.b, ys, smem, a.ring_size, true);
+    __syncthreads();
+    const Params& p = a.prm;
+    const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
+    double dot[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) dot[r] = 0.0;
+    for (int64_t j = tid; j < n; j += nt) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!grad[r]) continue;
+        const int64_t e = j * R + r;
+        const double2 px = xc[r][j];
+        const double xn = mat[r] ? __ddiv_rn(xtilde_inv(px, rad[r]), ndiv[r]) : px.x;
+        const double zz = __ddiv_rn(ys[r][j], ndiv[r]);
+        const double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(zz, iy2[r]));
+        const double2 mv = a.MV[e];
+        const double mm = __dadd_rn(__dmul_rn(p.beta1, mv.x), __dmul_rn(om1, g));
+        const double vv = __dadd_rn(__dmul_rn(p.beta2, mv.y), __dmul_rn(__dmul_rn(om2, g), g));
+        const double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
+                                   __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));
+        a.MV[e] = make_double2(mm, vv);
+        xn_out[r][j] = make_double2(xn, d);
+        dot[r] = __fma_rn(xn, d, dot[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double s = block_sum(dot[r], s_h);
+      if (tid == 0) s_res[r][0] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int r = 0; r < R; ++r) {
+        ColState* s = a.st + r;
+        if (s->phase == PH_GRAD) {
+          s->rad = s_res[r][0];
+          if (s->mat) {
+            s->cur = s->nxt;
+            s->pend = 0;
+          }
+          s->phase = PH_APPLY;
+        }
+      }
+    }
+  }
+  if (tid == 0) {
+    int nwait = 0, ndone = 0;
+    for (int r = 0; r < R; ++r) {
+      nwait += a.st[r].phase == PH_WAIT;
+      ndone += a.st[r].phase == PH_DONE;
+    }
+    a.hdr->nwait = nwait;
+    a.hdr->ndone = ndone;
+    a.hdr->needA = 1;
+  }
+}
+
+size_t inv_step_smem(const BandView& b, int R);
+int lu_ring_size(const BandView& b);
+
+void prepare_inv_step(const BandView& b, int R) {
+  const size_t smem = inv_step_smem(b, R);
+  if (smem > 227 * 1024) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+  switch (R) {
+    case 1: CK_CUDA(cudaFuncSetAttribute(k_inv_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
+    case 2: CK_CUDA(cudaFuncSetAttribute(k_inv_step<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
+    case 3: CK_CUDA(cudaFuncSetAttribute(k_inv_step<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
+    default: CK_CUDA(cudaFuncSetAttribute(k_inv_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
+  }
+}
+
+void launch_inv_step(const InvArgs& a, int R, cudaStream_t st) {
+  const size_t smem = inv_step_smem(a.b, R);
+  switch (R) {
+#define CK_INV_CASE(RR)                                                                        \
+  case RR:                                                                                     \
+    k_inv_step<RR><<<1, 1024, smem, st>>>(a);                                                  \
+    break;
+    CK_INV_CASE(1)
+    CK_INV_CASE(2)
+    CK_INV_CASE(3)
+    CK_INV_CASE(4)
+#undef CK_INV_CASE
+    default: fail(CK_ERR_INVALID_ARGUMENT, "1..4 columns");
+  }
+}
+
+}  // namespace ck

@@ -1,0 +1,354 @@
+// Band LU with row partial pivoting on the device and the four triangular
+// sweeps of the InverseOracle (lu.hpp:55-227, condest.hpp:109-152).
+//
+// Factorisation: right-looking, 32-column panels (LAPACK gbtrf layout). A panel
+// CTA factors its 32 columns (pivot = first largest |candidate|, the
+// singularity tests of lu.hpp:112-129 with pivot_tol * column max); then every
+// trailing column touched by the panel's interchanges receives, in pivot
+// order, the interchange and the update -l(r,j) * u(j,k) of each panel step
+// (one warp per column, the panel's multipliers staged in shared memory). Each
+// entry therefore sees the same updates in the same order as the reference's
+// left-looking elimination, with unfused multiply/subtract -- the factors agree
+// with lu_factorize value for value when the pivot sequence agrees.
+//
+// Solves: one CTA sweeps 32-row blocks with the active rows of the right-hand
+// side(s) in a shared-memory ring. Inside a block the 32x32 triangle is solved
+// by one warp (shuffles); everything outside it is a GEMV over contiguous band
+// columns spread over all warps. The L part interleaves row interchanges with
+// eliminations; each block uses multipliers re-expressed in the block's local
+// pivot order (convert_l_blocks), which turns the interleaved sequence into
+// "permute window, unit-lower solve, update tail" without changing any value.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ck_common.h"
+#include "ck_device.cuh"
+#include "ck_internal.h"
+#include "ck_lu.h"
+#include "ck_lu_sweeps.cuh"
+
+namespace ck {
+
+
+// ----------------------------------------------------------- band fill
+__global__ void k_band_bounds(SellView A, int64_t nrows_pad, const int32_t* __restrict__ rperm,
+                              const int32_t* __restrict__ cperm, int* klku) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nrows_pad) return;
+  const int32_t row = rperm[p];
+  if (row < 0) return;
+  const int64_t base = A.sp[p >> 5] + (p & 31);
+  const int L = A.len[p];
+  int lo = 0, up = 0;
+  for (int j = 0; j < L; ++j) {
+    const int32_t col = cperm[A.col[base + (int64_t)j * kSlice]];
+    lo = max(lo, row - col);
+    up = max(up, col - row);
+  }
+  atomicMax(klku, lo);
+  atomicMax(klku + 1, up);
+}
+
+__global__ void k_band_fill(SellView A, int64_t nrows_pad, const int32_t* __restrict__ rperm,
+                            const int32_t* __restrict__ cperm, BandView b) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nrows_pad) return;
+  const int32_t row = rperm[p];
+  if (row < 0) return;
+  const int64_t base = A.sp[p >> 5] + (p & 31);
+  const int L = A.len[p];
+  for (int j = 0; j < L; ++j) {
+    const int64_t k = base + (int64_t)j * kSlice;
+    AB(b, row, cperm[A.col[k]]) = A.val[k];
+  }
+}
+
+// ----------------------------------------------------------- factorisation
+// Panel: columns j0 .. j0+jb-1 by one CTA.
+__global__ void __launch_bounds__(256) k_gbtrf_panel(BandView b, int64_t j0, int jb,
+                                                     double pivot_tol, LUStatus* st) {
+  __shared__ double s_mag[256], s_cmax[256];
+  __shared__ int64_t s_idx[256];
+  __shared__ int64_t s_p;
+  __shared__ double s_piv;
+  if (st->code != 0) return;
+  const int tid = threadIdx.x;
+  int64_t ju = 0;
+  for (int c = 0; c < jb; ++c) {
+    const int64_t j = j0 + c;
+    const int64_t km = lmin(b.kl, b.n - 1 - j);
+    // pivot search over rows j..j+km; column maximum over every stored row of
+    // column j (U part above the diagonal included), lu.hpp:112-125
+    double best = -1.0, cmax = 0.0;
+    int64_t bi = -1;
+    const int64_t top = lmax(0, j - b.kv);
+    for (int64_t i = top + tid; i <= j + km; i += blockDim.x) {
+      const double m = fabs(AB(b, i, j));
+      cmax = fmax(cmax, m);
+      if (i >= j && m > best) {
+        best = m;
+        bi = i;
+      }
+    }
+    s_mag[tid] = best;
+    s_idx[tid] = bi;
+    s_cmax[tid] = cmax;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (tid < s) {
+        const double om = s_mag[tid + s];
+        const int64_t oi = s_idx[tid + s];
+        if (om > s_mag[tid] || (om == s_mag[tid] && oi >= 0 && (s_idx[tid] < 0 || oi < s_idx[tid]))) {
+          s_mag[tid] = om;
+          s_idx[tid] = oi;
+        }
+        s_cmax[tid] = fmax(s_cmax[tid], s_cmax[tid + s]);
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const double bm = s_mag[0];
+      const int64_t p = s_idx[0];
+      if (bm == 0.0 || p < 0 || bm < pivot_tol * s_cmax[0]) {
+        st->code = 5;
+        st->column = j;
+        st->pivot = bm < 0.0 ? 0.0 : bm;
+        s_p = -1;
+      } else {
+        st->pivot_min = fmin(st->pivot_min, bm);
+        b.ipiv[j] = (int32_t)p;
+        s_p = p;
+        s_piv = AB(b, p, j);
+      }
+    }
+    __syncthreads();
+    const int64_t p = s_p;
+    if (p < 0) return;
+    ju = lmax(ju, lmin(j + b.ku + (p - j), b.n - 1));
+    // interchange rows j and p inside the panel (columns j .. j0+jb-1)
+    // columns beyond j + kv hold no entry in rows j..j+km (LAPACK's ju bound)
+    const int64_t kend = lmin(j0 + jb, j + b.kv + 1);
+    if (p != j)
+      for (int64_t k = j + tid; k < kend; k += blockDim.x) {
+        double t = AB(b, j, k);
+        AB(b, j, k) = AB(b, p, k);
+        AB(b, p, k) = t;
+      }
+    __syncthreads();
+    // multipliers l = a / pivot (lu.hpp:136)
+    const double piv = s_piv;
+    for (int64_t i = j + 1 + tid; i <= j + km; i += blockDim.x) AB(b, i, j) = __ddiv_rn(AB(b, i, j), piv);
+    __syncthreads();
+    // rank-1 update of the remaining panel columns (lu.hpp:102-109 order)
+    const int64_t ncol = kend - (j + 1);
+    for (int64_t q = tid; q < ncol * km; q += blockDim.x) {
+      const int64_t k = j + 1 + q / km, i = j + 1 + q % km;
+      const double u = AB(b, j, k);
+      AB(b, i, k) = __dsub_rn(AB(b, i, k), __dmul_rn(AB(b, i, j), u));
+    }
+    __syncthreads();
+  }
+  if (tid == 0) st->ju = ju;
+}
+
+// Trailing columns j0+jb .. ju: per column, the panel's interchanges and
+// updates in pivot order. One warp per column; multipliers of the panel in
+// shared memory: s_l[c * (kl+1) + r] = l(j0+c+1+r, j0+c).
+__global__ void __launch_bounds__(512) k_gbtrf_update(BandView b, int64_t j0, int jb,
+                                                      const LUStatus* st) {
+  extern __shared__ double s_l[];
+  if (st->code != 0) return;
+  const int64_t ju = st->ju;
+  const int64_t kfirst = j0 + jb;
+  if (kfirst > ju) return;
+  const int64_t ld = b.kl + 1;
+  for (int64_t q = threadIdx.x; q < (int64_t)jb * ld; q += blockDim.x) {
+    const int c = (int)(q / ld);
+    const int64_t r = q % ld;
+    const int64_t j = j0 + c, km = lmin(b.kl, b.n - 1 - j);
+    s_l[q] = (r < km) ? AB(b, j + 1 + r, j) : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int64_t k = kfirst + (int64_t)blockIdx.x * nw + warp; k <= ju; k += (int64_t)gridDim.x * nw) {
+    for (int c = 0; c < jb; ++c) {
+      const int64_t j = j0 + c;
+      if (k - j > b.kv) continue;  // row j (and p) hold no entry in column k
+      const int64_t p = b.ipiv[j];
+      const int64_t km = lmin(b.kl, b.n - 1 - j);
+      if (p != j && lane == 0) {
+        double t = AB(b, j, k);
+        AB(b, j, k) = AB(b, p, k);
+        AB(b, p, k) = t;
+      }
+      __syncwarp();
+      const double u = AB(b, j, k);
+      if (u != 0.0)
+        for (int64_t r = lane; r < km; r += 32)
+          AB(b, j + 1 + r, k) = __dsub_rn(AB(b, j + 1 + r, k), __dmul_rn(s_l[c * ld + r], u));
+      __syncwarp();
+    }
+  }
+}
+
+// L blocks in local pivot order: for block blk (columns J..J+jb-1), column c
+// holds the step-(J+c) multipliers with the later interchanges of the same
+// block applied, at window rows (relative to J) 0 .. 32+kl-1.
+__global__ void __launch_bounds__(256) k_convert_l_blocks(BandView b) {
+  const int64_t blk = blockIdx.x;
+  const int64_t J = blk * kLUBlock;
+  const int jb = (int)lmin(kLUBlock, b.n - J);
+  double* dst = b.lb + blk * kLUBlock * b.lb_ld;
+  for (int64_t q = threadIdx.x; q < (int64_t)kLUBlock * b.lb_ld; q += blockDim.x) {
+    const int c = (int)(q / b.lb_ld);
+    const int64_t r = q % b.lb_ld;
+    double v = 0.0;
+    if (c < jb) {
+      const int64_t j = J + c, row = J + r, km = lmin(b.kl, b.n - 1 - j);
+      if (row > j && row <= j + km) v = AB(b, row, j);
+    }
+    dst[q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < jb) {
+    const int c = threadIdx.x;
+    double* col = dst + (int64_t)c * b.lb_ld;
+    for (int c2 = c + 1; c2 < jb; ++c2) {
+      const int64_t p = b.ipiv[J + c2];
+      if (p != J + c2) {
+        const int64_t ra = c2, rb = p - J;
+        double t = col[ra];
+        col[ra] = col[rb];
+        col[rb] = t;
+      }
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(1024) k_lu_solve(BandView b, double* x0, double* x1, double* x2,
+                                                   double* x3, int transpose, int ring_size) {
+  extern __shared__ double smem[];
+  double* xs[4] = {x0, x1, x2, x3};
+  inv_solve<R>(b, xs, smem, ring_size, transpose != 0);
+}
+
+// ---------------------------------------------------------------- host side
+int lu_ring_size(const BandView& b) {
+  int64_t need = std::max<int64_t>(b.kv, b.kl) + 2 * kLUBlock + 1;
+  int s = 64;
+  while (s < need) s <<= 1;
+  return s;
+}
+
+size_t lu_solve_smem(const BandView& b, int R) {
+  return sizeof(double) * ((size_t)R * lu_ring_size(b) + (size_t)R * kLUBlock);
+}
+
+size_t inv_step_smem(const BandView& b, int R) { return lu_solve_smem(b, R); }
+
+void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st) {
+  BandView b = f->view();
+  const int ring = lu_ring_size(b);
+  const size_t smem = lu_solve_smem(b, R);
+  if (smem > 227 * 1024) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+  double* xs[4] = {x[0], R > 1 ? x[1] : nullptr, R > 2 ? x[2] : nullptr, R > 3 ? x[3] : nullptr};
+  switch (R) {
+#define CK_SOLVE_CASE(RR)                                                                       \
+  case RR:                                                                                      \
+    CK_CUDA(cudaFuncSetAttribute(k_lu_solve<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                 (int)smem));                                                   \
+    k_lu_solve<RR><<<1, 1024, smem, st>>>(b, xs[0], xs[1], xs[2], xs[3], transpose ? 1 : 0, ring); \
+    break;
+    CK_SOLVE_CASE(1)
+    CK_SOLVE_CASE(2)
+    CK_SOLVE_CASE(3)
+    CK_SOLVE_CASE(4)
+#undef CK_SOLVE_CASE
+    default: fail(CK_ERR_INVALID_ARGUMENT, "1..4 right-hand sides");
+  }
+  CK_CUDA(cudaGetLastError());
+}
+
+void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_col,
+                  double* fail_pivot) {
+  if (m->nrows != m->ncols) fail(CK_ERR_DIMENSION, "lu_factorize: matrix must be square");
+  f->device = m->device;
+  // the factors outlive the matrix handle (LUFactors is a value in lu.hpp:42-47):
+  // they get their own stream
+  CK_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+  f->own_stream = true;
+  CK_CUDA(cudaStreamSynchronize(m->stream));
+  cudaStream_t st = f->stream;
+  const int64_t n = m->nrows;
+  f->n = n;
+  DBuf<int> klku(2);
+  CK_CUDA(cudaMemsetAsync(klku.p, 0, 2 * sizeof(int), st));
+  const unsigned g = (unsigned)std::max<int64_t>(1, ceil_div(m->a.nrows_pad, 256));
+  if (n > 0) k_band_bounds<<<g, 256, 0, st>>>(view(m->a), m->a.nrows_pad, m->a.perm.p, m->at.perm.p, klku.p);
+  int h[2] = {0, 0};
+  CK_CUDA(cudaMemcpyAsync(h, klku.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+  f->kl = h[0];
+  f->ku = h[1];
+  const int64_t ldab = 2 * f->kl + f->ku + 1;
+  const double bytes = (double)ldab * (double)n * 8.0;
+  size_t freeb = 0, totalb = 0;
+  CK_CUDA(cudaMemGetInfo(&freeb, &totalb));
+  if (bytes * 1.2 > (double)freeb)
+    fail(CK_ERR_OUT_OF_MEMORY, "band LU storage (" + std::to_string(bytes / 1e9) + " GB) exceeds free device memory");
+  f->ab.alloc(std::max<int64_t>(1, ldab * n));
+  f->ipiv.alloc(std::max<int64_t>(1, n));
+  f->status.alloc(1);
+  CK_CUDA(cudaMemsetAsync(f->ab.p, 0, f->ab.bytes(), st));
+  LUStatus s0{0, 0, -1, 0.0, INFINITY, 0};
+  CK_CUDA(cudaMemcpyAsync(f->status.p, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
+  BandView b = f->view();
+  if (n > 0) k_band_fill<<<g, 256, 0, st>>>(view(m->a), m->a.nrows_pad, m->a.perm.p, m->at.perm.p, b);
+  CK_CUDA(cudaGetLastError());
+  const size_t usmem = sizeof(double) * kLUBlock * (size_t)(f->kl + 1);
+  if (usmem > 227 * 1024) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip panel update");
+  CK_CUDA(cudaFuncSetAttribute(k_gbtrf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem));
+  const int64_t maxcols = f->kl + f->ku + 1;
+  const unsigned ublocks = (unsigned)std::min<int64_t>(148, std::max<int64_t>(1, ceil_div(maxcols, 16)));
+  for (int64_t j0 = 0; j0 < n; j0 += kLUBlock) {
+    const int jb = (int)std::min<int64_t>(kLUBlock, n - j0);
+    k_gbtrf_panel<<<1, 256, 0, st>>>(b, j0, jb, pivot_tol, f->status.p);
+    if (j0 + jb < n) k_gbtrf_update<<<ublocks, 512, usmem, st>>>(b, j0, jb, f->status.p);
+  }
+  CK_CUDA(cudaGetLastError());
+  LUStatus s{};
+  CK_CUDA(cudaMemcpyAsync(&s, f->status.p, sizeof(s), cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+  if (s.code != 0) {
+    if (fail_col) *fail_col = s.column;
+    if (fail_pivot) *fail_pivot = s.pivot;
+    f->ab.reset();
+    if (s.code == 5 && s.pivot == 0.0 && s.column >= 0 && s.column < n) {
+      // No nonzero candidate. The reference calls this structural when no
+      // unpivoted row is touched at all (lu.hpp:126); the band form does not
+      // track structure, so an empty column of A is the case classified here.
+      int32_t pos = 0;
+      uint16_t len = 1;
+      CK_CUDA(cudaMemcpy(&pos, m->at.inv.p + s.column, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      CK_CUDA(cudaMemcpy(&len, m->at.len.p + pos, sizeof(uint16_t), cudaMemcpyDeviceToHost));
+      if (len == 0) s.code = 4;
+    }
+    fail(s.code == 4 ? CK_ERR_STRUCT_SINGULAR : CK_ERR_NUM_SINGULAR,
+         (s.code == 4 ? std::string("structurally singular: no pivot candidate in column ")
+                      : std::string("numerically singular: best pivot below threshold in column ")) +
+             std::to_string(s.column));
+  }
+  f->pivot_min = n > 0 ? s.pivot_min : INFINITY;
+  const int64_t nblk = ceil_div(n, kLUBlock);
+  f->lb.alloc(std::max<int64_t>(1, nblk * kLUBlock * (kLUBlock + f->kl)));
+  f->work.alloc(2 * n + 3 * kNormParts + 16);
+  b = f->view();
+  if (n > 0) k_convert_l_blocks<<<(unsigned)nblk, 256, 0, st>>>(b);
+  CK_CUDA(cudaGetLastError());
+  CK_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace ck

@@ -1,0 +1,65 @@
+// Device band LU with row partial pivoting (the factorisation behind the
+// InverseOracle, lu.hpp:55-227) -- shared by ck_lu.cu (factorisation, solves)
+// and ck_inverse.cu (the Projected-Adam loop on A^-1).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ck_common.h"
+
+namespace ck {
+
+// LAPACK band layout (column major): entry (i, j) of the factored matrix at
+// ab[(kv + i - j) + j * ldab] with kv = kl + ku and ldab = 2*kl + ku + 1, for
+// max(0, j - kv) <= i <= min(n-1, j + kl). Rows kv+1.. of column j hold the
+// multipliers of elimination step j (not permuted by later interchanges);
+// ipiv[j] is the row interchanged with row j at step j.
+struct BandView {
+  int64_t n, kl, ku, kv, ldab;
+  double* ab;
+  int32_t* ipiv;
+  // Per 32-column block of L, the multipliers re-expressed in the block's local
+  // pivot order: lb[blk][c][r] for r in [0, nb + kl) rows of the window that
+  // starts at row 32*blk (see ck_lu.cu, convert_l_blocks).
+  double* lb;
+  int64_t lb_ld;  // rows per column of lb (= 32 + kl)
+};
+
+struct LUStatus {
+  int32_t code;  // 0 ok, 4 structurally singular, 5 numerically singular
+  int32_t _pad;
+  int64_t column;
+  double pivot;
+  double pivot_min;
+  int64_t ju;  // last column touched by the current panel's interchanges
+};
+
+constexpr int kLUBlock = 32;  // panel width / solve block
+
+}  // namespace ck
+
+struct ck_lu_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t n = 0, kl = 0, ku = 0;
+  double pivot_min = 0.0;
+  ck::DBuf<double> ab, lb;
+  ck::DBuf<int32_t> ipiv;
+  ck::DBuf<ck::LUStatus> status;
+  ck::DBuf<double> work;  // solve scratch
+  ck_lu_s() = default;
+  ck_lu_s(const ck_lu_s&) = delete;
+  ck_lu_s& operator=(const ck_lu_s&) = delete;
+  ~ck_lu_s() {
+    if (own_stream && stream) {
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+  ck::BandView view() {
+    return ck::BandView{n, kl, ku, kl + ku, 2 * kl + ku + 1, ab.p, ipiv.p, lb.p,
+                        ck::kLUBlock + kl};
+  }
+};

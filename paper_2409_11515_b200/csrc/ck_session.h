@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ck_common.h"
+#include "ck_lu.h"
 
 namespace ck {
 
@@ -49,6 +50,20 @@ struct LoopArgs {
   Params prm;
 };
 
+// Arguments of the inverse-operator step (ck_inverse.cu).
+struct InvArgs {
+  BandView b;
+  int64_t n;
+  int ring_size;
+  double2* PX;  // [3][R][n]
+  double2* MV;  // [n][R]
+  double* y;    // [R][n] work vector (solve in place)
+  ColState* st;
+  Header* hdr;
+  Params prm;
+  int half;  // 0 whole step, 1 apply half only, 2 transpose half only (observer)
+};
+
 }  // namespace ck
 
 struct ck_session_s {
@@ -62,8 +77,17 @@ struct ck_session_s {
   int R = 1;
   Params prm{};
   LoopArgs args{};
+  int kind = 0;              // 0: ExplicitOracle (ck_matrix), 1: InverseOracle (ck_lu)
+  ck_lu_s* lu = nullptr;
+  ck::InvArgs iargs{};
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int64_t n = 0;            // operator dimension (columns of A)
+  int64_t npad = 0;         // length of the internal vectors
+  int64_t thalf = 0;        // tmp holds two halves of thalf doubles
+  const int32_t* perm = nullptr;  // internal position -> original index (nullptr: identity)
   DBuf<double2> PX, MV;
-  DBuf<double> y, partA, partT, tmp;
+  DBuf<double> y, partA, partT, tmp, obs;
   DBuf<ColState> st;
   DBuf<Header> hdr;
   std::vector<std::mt19937_64> gens;

@@ -1,23 +1,235 @@
-"""InverseOracle: ||A^-1||_2 through LU factors (condest.hpp:109-152, lu.hpp).
+"""||A^-1||_2 and kappa_2 on the device: LU factors, InverseOracle, cond2.
 
-Placeholder until the device factorisation lands; every entry point raises.
+Mirror of the reference's lu.hpp / condest.hpp inverse half:
+  LUFactors (lu.hpp:42-47), lu_factorize (:55-177), lu_solve (:180-202),
+  lu_transpose_solve (:207-227), InverseOracle (condest.hpp:138-152),
+  inv_norm2 (:320-322), Cond2Result / cond2 (:324-365).
+
+The factors live on the B200 as a LAPACK-layout band LU with row partial
+pivoting (csrc/ck_lu.cu); every solve and every Projected-Adam iteration on
+A^-1 runs there (csrc/ck_inverse.cu).
 """
 from __future__ import annotations
 
-from .errors import Unsupported
+import ctypes as C
+import math
+import weakref
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .condest import (AdamConfig, ExplicitOracle, GradientOracle, NormEstimate, Session,
+                      estimate_norm)
+from .errors import (DimensionMismatch, InvalidArgument, NumericallySingular,
+                     StructurallySingular)
+from .sparse import SparseMatrix
 
 
-class InverseOracle:
-    def __init__(self, factors):
+class LUFactors:
+    """Device LU of a square SparseMatrix (P A = L U, band storage)."""
+
+    def __init__(self, handle, n: int):
+        self.handle = handle
+        self._fin = weakref.finalize(self, _lib.load().ck_lu_free, handle)
+        n_, kl, ku, pm, nb = C.c_int64(), C.c_int64(), C.c_int64(), C.c_double(), C.c_int64()
+        _lib.check(_lib.load().ck_lu_get_info(handle, C.byref(n_), C.byref(kl), C.byref(ku),
+                                              C.byref(pm), C.byref(nb)), "ck_lu_get_info")
+        self.n, self.kl, self.ku = n_.value, kl.value, ku.value
+        self.pivot_min = pm.value
+        self.device_bytes = nb.value
+
+    def solve(self, b) -> np.ndarray:
+        b = _lib.as_f64(b, self.n, "lu_solve: rhs")
+        x = np.empty(self.n)
+        _lib.check(_lib.load().ck_lu_solve(self.handle, _lib.dptr(b), _lib.dptr(x)), "lu_solve")
+        return x
+
+    def transpose_solve(self, b) -> np.ndarray:
+        b = _lib.as_f64(b, self.n, "lu_transpose_solve: rhs")
+        x = np.empty(self.n)
+        _lib.check(_lib.load().ck_lu_transpose_solve(self.handle, _lib.dptr(b), _lib.dptr(x)),
+                   "lu_transpose_solve")
+        return x
+
+    def export_band(self):
+        """(ab, ipiv) in LAPACK band layout: ab[kv + i - j, j] = factor(i, j)."""
+        ldab = 2 * self.kl + self.ku + 1
+        ab = np.empty(ldab * self.n)
+        ipiv = np.empty(self.n, np.int32)
+        _lib.check(_lib.load().ck_lu_export(self.handle, _lib.dptr(ab), _lib.i32ptr(ipiv)),
+                   "ck_lu_export")
+        return ab.reshape(self.n, ldab).T.copy(), ipiv
+
+    def dense_factors(self):
+        """(perm, L, U) with A[perm] = L @ U (dense; small n only, for inspection)."""
+        ab, ipiv = self.export_band()
+        n, kl, ku = self.n, self.kl, self.ku
+        kv = kl + ku
+        L = np.eye(n)
+        U = np.zeros((n, n))
+        for j in range(n):
+            for i in range(max(0, j - kv), j + 1):
+                U[i, j] = ab[kv + i - j, j]
+        perm = np.arange(n)
+        # multipliers of step j are in rows j+1.. of the row order at step j; apply
+        # every later interchange to them to reach final pivot coordinates
+        cols = []
+        for j in range(n):
+            km = min(kl, n - 1 - j)
+            cols.append({j + 1 + r: ab[kv + 1 + r, j] for r in range(km)})
+        for j in range(n):
+            p = int(ipiv[j])
+            if p != j:
+                perm[[j, p]] = perm[[p, j]]
+                for k in range(j):
+                    c = cols[k]
+                    a, b = c.pop(j, 0.0), c.pop(p, 0.0)
+                    if b != 0.0:
+                        c[j] = b
+                    if a != 0.0:
+                        c[p] = a
+        for j in range(n):
+            for i, v in cols[j].items():
+                L[i, j] = v
+        return perm, L, U
+
+
+def lu_factorize(a: SparseMatrix, pivot_tol: float = 1e-12) -> LUFactors:
+    """lu.hpp:55-177 on the device; raises Structurally/NumericallySingular."""
+    if a.nrows != a.ncols:
+        raise DimensionMismatch("lu_factorize: matrix must be square")
+    h = C.c_void_p()
+    col, piv = C.c_int64(-1), C.c_double(0.0)
+    st = _lib.load().ck_lu_factorize(a.device().handle, pivot_tol, C.byref(h), C.byref(col),
+                                     C.byref(piv))
+    if st == StructurallySingular.status:
+        raise StructurallySingular(_lib.load().ck_last_error().decode(), column=col.value)
+    if st == NumericallySingular.status:
+        raise NumericallySingular(_lib.load().ck_last_error().decode(), column=col.value,
+                                  pivot=piv.value)
+    _lib.check(st, "lu_factorize")
+    return LUFactors(h, a.nrows)
+
+
+def lu_solve(f: LUFactors, b) -> np.ndarray:
+    return f.solve(b)
+
+
+def lu_transpose_solve(f: LUFactors, b) -> np.ndarray:
+    return f.transpose_solve(b)
+
+
+class InverseOracle(GradientOracle):
+    """Op = A^-1 through the factors (condest.hpp:138-152); holds them by reference."""
+
+    def __init__(self, factors: LUFactors):
         self.factors = factors
 
     def dimension(self) -> int:
         return self.factors.n
 
+    def loss(self, x) -> float:
+        x = _lib.as_f64(x, self.factors.n)
+        out = C.c_double()
+        _lib.check(_lib.load().ck_loss_inverse(self.factors.handle, _lib.dptr(x), C.byref(out)),
+                   "loss_inverse")
+        return out.value
 
-def _inverse_projected_adam(oracle, cfg, observer):
-    raise Unsupported("InverseOracle is not available in this build yet")
+    def grad(self, x) -> np.ndarray:
+        x = _lib.as_f64(x, self.factors.n)
+        g = np.empty(self.factors.n)
+        _lib.check(_lib.load().ck_grad_inverse(self.factors.handle, _lib.dptr(x), _lib.dptr(g)),
+                   "grad_inverse")
+        return g
+
+    def apply(self, x) -> np.ndarray:
+        return self.factors.solve(x)
 
 
-def _inverse_estimate_norm(oracle, cfg, restarts):
-    raise Unsupported("InverseOracle is not available in this build yet")
+def grad_inverse(f: LUFactors, x) -> np.ndarray:
+    """condest.hpp:112-123."""
+    return InverseOracle(f).grad(x)
+
+
+class InverseSession(Session):
+    def __init__(self, oracle: InverseOracle, cfg: AdamConfig, seeds):
+        if oracle.dimension() == 0:
+            raise InvalidArgument("projected_adam: zero-dimensional operator")
+        self.oracle = oracle
+        self.n = oracle.dimension()
+        lib = _lib.load()
+        self._cfg = _lib.cfg_struct(cfg)
+        seeds = np.ascontiguousarray([int(s) & 0xFFFFFFFFFFFFFFFF for s in seeds], np.uint64)
+        self.ncols = seeds.size
+        h = C.c_void_p()
+        _lib.check(lib.ck_session_create_inverse(oracle.factors.handle, C.byref(self._cfg),
+                                                 seeds.ctypes.data_as(_lib.u64p), self.ncols,
+                                                 C.byref(h)), "ck_session_create_inverse")
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.ck_session_free, h)
+
+
+def _inverse_projected_adam(oracle: InverseOracle, cfg: AdamConfig, observer):
+    from .condest import AdamState, AdamStepInfo  # noqa: PLC0415
+    s = InverseSession(oracle, cfg, [cfg.seed])
+    try:
+        if observer is None:
+            s.run()
+        else:
+            while True:
+                info, x, xm = s.step_observed(True)
+                if info.phase == 2:
+                    break
+                observer(AdamState(x=x, t=int(info.t), loss_min=info.loss_min, x_min=xm),
+                         AdamStepInfo(info.x_dot_delta, info.delta_norm, info.loss))
+        return s.result(0)
+    finally:
+        s.close()
+
+
+def _inverse_estimate_norm(oracle: InverseOracle, cfg: AdamConfig, restarts: int):
+    r = _lib.NormResult()
+    w = np.empty(oracle.dimension())
+    c = _lib.cfg_struct(cfg)
+    _lib.check(_lib.load().ck_inv_estimate_norm(oracle.factors.handle, C.byref(c), restarts,
+                                                C.byref(r), _lib.dptr(w)), "estimate_norm")
+    return NormEstimate(r.value, w, int(r.iterations), bool(r.converged))
+
+
+def inv_norm2(f: LUFactors, cfg: Optional[AdamConfig] = None) -> NormEstimate:
+    """||A^-1||_2 estimate, single run (condest.hpp:320-322)."""
+    from .condest import projected_adam  # noqa: PLC0415
+    return projected_adam(InverseOracle(f), cfg)
+
+
+@dataclass
+class Cond2Result:
+    kappa: float = 0.0
+    operator_norm: NormEstimate = field(default_factory=NormEstimate)
+    inverse_norm: NormEstimate = field(default_factory=NormEstimate)
+    factors: Optional[LUFactors] = None
+
+
+def cond2(a: SparseMatrix, cfg: Optional[AdamConfig] = None, restarts: int = 3,
+          pivot_tol: float = 1e-14) -> Cond2Result:
+    """kappa_2(A) = ||A|| ||A^-1|| (condest.hpp:341-365); singular -> +inf."""
+    cfg = cfg or AdamConfig()
+    if a.nrows != a.ncols:
+        raise DimensionMismatch("cond2: matrix must be square")
+    res = Cond2Result()
+    res.operator_norm = estimate_norm(ExplicitOracle(a), cfg, restarts)
+    try:
+        f = lu_factorize(a, pivot_tol)
+    except (StructurallySingular, NumericallySingular):
+        res.inverse_norm = NormEstimate(value=math.inf)
+        res.kappa = math.inf
+        return res
+    ci = AdamConfig(**{**cfg.__dict__})
+    from .rng import mix_seed  # noqa: PLC0415
+    ci.seed = mix_seed(cfg.seed, 0x1234)
+    res.inverse_norm = estimate_norm(InverseOracle(f), ci, restarts)
+    res.kappa = res.operator_norm.value * res.inverse_norm.value
+    res.factors = f
+    return res

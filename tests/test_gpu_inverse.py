@@ -1,0 +1,216 @@
+"""sigma_min path on the device vs the oracle: band LU (lu.hpp), triangular
+solves, Projected Adam on A^-1 (InverseOracle), cond2 and verify_solution."""
+import math
+
+import numpy as np
+import pytest
+
+import matrices as M
+import paper_2409_11515_b200 as ck
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_dense_lu(port, a, tol):
+    f = port.lu_factorize(a, tol)
+    e = f.export()
+    n = a.nrows
+    L = np.eye(n)
+    U = np.zeros((n, n))
+    lrp, lci, lva = e["l"]
+    urp, uci, uva = e["u"]
+    for i in range(n):
+        for k in range(lrp[i], lrp[i + 1]):
+            L[i, lci[k]] = lva[k]
+        for k in range(urp[i], urp[i + 1]):
+            U[i, uci[k]] = uva[k]
+    return e["row_perm"], L, U, f
+
+
+@pytest.mark.parametrize("n,seed", [(5, 8), (20, 15), (50, 29), (50, 36), (100, 3)])
+def test_factors_match_reference_bitwise(port, n, seed):
+    # test_lu.cpp:54-70 fixtures; same pivots and unfused arithmetic -> same factors
+    a = M.random_sparse(port, n, 0.3, seed)
+    f = ck.lu_factorize(a, 1e-12)
+    perm, L, U = f.dense_factors()
+    rperm, rL, rU, rf = oracle_dense_lu(port, a, 1e-12)
+    assert np.array_equal(perm, rperm)
+    assert np.array_equal(U, rU)
+    assert np.array_equal(L, rL)
+    assert f.pivot_min == rf.pivot_min
+    d = a.to_dense()
+    assert np.linalg.norm(d[perm] - L @ U) <= 1e-13 * np.linalg.norm(d)
+    assert np.abs(L).max() <= 1.0
+
+
+def test_identity_and_permutation():
+    # test_lu.cpp:28-52
+    f = ck.lu_factorize(ck.SparseMatrix.identity(4))
+    assert f.pivot_min == 1.0
+    assert np.array_equal(f.solve([1.0, 2.0, 3.0, 4.0]), [1.0, 2.0, 3.0, 4.0])
+    a = ck.SparseMatrix.from_triplets(2, 2, [(0, 1, 1.0), (1, 0, 1.0)])
+    f = ck.lu_factorize(a)
+    assert f.pivot_min == 1.0
+    assert np.array_equal(f.solve([1.0, 2.0]), [2.0, 1.0])
+    assert np.array_equal(f.transpose_solve([3.0, 4.0]), [4.0, 3.0])
+    f = ck.lu_factorize(M.diag_matrix([5.0, 3.0, 8.0]))
+    assert f.pivot_min == 3.0
+
+
+def _banded(n, bw, seed):
+    rng = np.random.default_rng(seed)
+    r, c, v = [], [], []
+    for i in range(n):
+        for j in range(max(0, i - bw), min(n, i + bw + 1)):
+            if i == j or rng.random() < 0.3:
+                r.append(i)
+                c.append(j)
+                v.append(rng.standard_normal() * (3.0 if i == j else 1.0))
+    return ck.SparseMatrix.from_coo(n, n, r, c, v)
+
+
+@pytest.mark.parametrize("kind", ["random40", "laplacian24", "banded700", "rowscaled33"])
+def test_solves_match_reference(port, kind):
+    a = {"random40": lambda: M.random_sparse(port, 40, 0.2, 4),
+         "laplacian24": lambda: M.laplacian2d(24),
+         "banded700": lambda: _banded(700, 45, 2),
+         "rowscaled33": lambda: M.row_scaled(M.laplacian2d(33), port, 1)}[kind]()
+    f = ck.lu_factorize(a, 1e-14)
+    rf = port.lu_factorize(a, 1e-14)
+    d = a.to_dense()
+    for seed in (1, 2):
+        b = port.random_unit_vectors(seed, a.nrows)[0]
+        x, xr = f.solve(b), port.lu_solve(rf, b)
+        assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
+        t, tr = f.transpose_solve(b), port.lu_transpose_solve(rf, b)
+        assert np.linalg.norm(t - tr) <= 1e-12 * np.linalg.norm(tr)
+        assert np.linalg.norm(d @ x - b) <= 1e-12 * np.linalg.norm(d) * np.linalg.norm(x)
+
+
+def test_singular_factorisations():
+    dup = ck.SparseMatrix.from_triplets(3, 3, [(0, 0, 1.0), (0, 1, 2.0), (1, 0, 1.0), (1, 1, 2.0),
+                                               (2, 2, 5.0)])
+    with pytest.raises(ck.NumericallySingular) as e:
+        ck.lu_factorize(dup, 1e-14)
+    assert e.value.column == 1
+    empty = ck.SparseMatrix.from_triplets(3, 3, [(0, 0, 1.0), (1, 1, 1.0), (2, 0, 1.0)])
+    with pytest.raises(ck.StructurallySingular) as e:
+        ck.lu_factorize(empty, 1e-14)
+    assert e.value.column == 2
+    r = ck.cond2(dup)
+    assert math.isinf(r.kappa) and math.isinf(r.inverse_norm.value)
+    assert r.operator_norm.value > 0 and r.factors is None
+    r = ck.cond2(ck.SparseMatrix.from_triplets(3, 3, []))
+    assert math.isinf(r.kappa) and r.operator_norm.value == 0.0
+
+
+def test_inverse_loss_grad(port):
+    a = M.random_sparse(port, 20, 0.3, 7)
+    f, rf = ck.lu_factorize(a), port.lu_factorize(a)
+    ox = ck.InverseOracle(f)
+    for x in port.random_unit_vectors(13, 20, 4):
+        assert ox.loss(x) == pytest.approx(port.loss_inverse(rf, x), rel=1e-12, abs=1e-14)
+        assert np.allclose(ox.grad(x), port.grad_inverse(rf, x), rtol=1e-11, atol=1e-14)
+
+
+def test_inverse_known_norm():
+    # test_condest.cpp:150-160
+    f = ck.lu_factorize(M.diag_matrix([3.0, 1.0, 1e-3]))
+    e = ck.inv_norm2(f)
+    assert e.converged and e.value == pytest.approx(1e3, rel=1e-9)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_inverse_projected_adam_vs_oracle(port, seed):
+    a = M.row_scaled(M.laplacian2d(16), port, seed)
+    c = M.cfg(alpha=1e-2, max_iter=2000, patience=2000, seed=seed)
+    f, rf = ck.lu_factorize(a, 1e-14), port.lu_factorize(a, 1e-14)
+    g = ck.projected_adam(ck.InverseOracle(f), c)
+    o = port.projected_adam_inverse(rf, c)
+    assert g.iterations == o.iterations and g.converged == o.converged
+    assert g.value == pytest.approx(o.value, rel=1e-3)
+    assert np.linalg.norm(port.lu_solve(rf, g.witness)) == pytest.approx(g.value, rel=1e-11)
+
+
+def test_inverse_default_config_vs_oracle(port):
+    a = M.random_sparse(port, 30, 0.2, 9)
+    f, rf = ck.lu_factorize(a), port.lu_factorize(a)
+    c = M.cfg(seed=4)
+    g = ck.projected_adam(ck.InverseOracle(f), c)
+    o = port.projected_adam_inverse(rf, c)
+    assert g.iterations == o.iterations and g.converged == o.converged
+    assert g.value == pytest.approx(o.value, rel=1e-9)
+    e = ck.estimate_norm(ck.InverseOracle(f), c, 3)
+    eo = port.estimate_norm_inverse(rf, c, 3)
+    assert e.value == pytest.approx(eo.value, rel=1e-9)
+
+
+def test_inverse_trajectory_invariants():
+    # acceptance.cpp:319-352 for the inverse oracle
+    a, _ = M.svd_constructed(30, M.geometric_sigmas(30, 2.0, 1e6), 44)
+    f = ck.lu_factorize(a, 1e-14)
+    prev_t, prev_min, calls = 0, math.inf, 0
+
+    def obs(st, info):
+        nonlocal prev_t, prev_min, calls
+        calls += 1
+        assert abs(np.linalg.norm(st.x) - 1.0) <= 1e-14
+        assert abs(info.x_dot_delta) <= 1e-13 * info.delta_norm + 1e-300
+        assert st.loss_min <= prev_min and st.t == prev_t + 1
+        prev_t, prev_min = st.t, st.loss_min
+
+    c = M.cfg(seed=13)
+    e = ck.projected_adam(ck.InverseOracle(f), c, obs)
+    again = ck.projected_adam(ck.InverseOracle(f), c)
+    assert calls > 0 and e.value == again.value and np.array_equal(e.witness, again.witness)
+
+
+@pytest.mark.parametrize("case", ["random30", "diag", "constructed1e8", "config1_shape"])
+def test_cond2_vs_oracle(port, case):
+    # test_condest.cpp:274-301 and the BASELINE config-1 recipe (on a 24x24 grid)
+    if case == "random30":
+        a, c, tol = M.random_sparse(port, 30, 0.3, 53), M.cfg(), 1e-9
+    elif case == "diag":
+        a, c, tol = M.diag_matrix([10.0, 2.0, 1.0]), M.cfg(), 1e-12
+    elif case == "constructed1e8":
+        a, c, tol = M.svd_constructed(40, M.geometric_sigmas(40, 1.0, 1e8), 77)[0], M.cfg(), 1e-3
+    else:
+        a = M.row_scaled(M.laplacian2d(24), port, 1)
+        c, tol = M.cfg(alpha=1e-2, max_iter=2000, patience=2000), 1e-3
+    r = ck.cond2(a, c)
+    o = port.cond2(a, c)
+    assert r.kappa == pytest.approx(o["kappa"], rel=tol)
+    assert r.operator_norm.value == pytest.approx(o["operator_norm"].value, rel=tol)
+    assert r.inverse_norm.value == pytest.approx(o["inverse_norm"].value, rel=tol)
+    assert r.factors is not None
+
+
+def test_cond2_against_dense_svd():
+    a, d = M.svd_constructed(40, M.geometric_sigmas(40, 1.0, 1e8), 77)
+    s = np.linalg.svd(d, compute_uv=False)
+    r = ck.cond2(a)
+    assert r.kappa == pytest.approx(s[0] / s[-1], rel=1e-3)
+    assert r.operator_norm.converged and r.inverse_norm.converged
+
+
+def test_verify_solution_vs_oracle(port):
+    a = M.random_sparse(port, 40, 0.2, 3)
+    x = port.uniform_in(70, 40, -1.0, 1.0)
+    b = port.matvec(a, x)
+    xh = x + 1e-6 * port.random_unit_vectors(4, 40)[0]
+    rep = ck.verify_solution(a, xh, b)
+    ro = port.verify_solution(a, xh, b)
+    assert rep.residual_norm == pytest.approx(ro["residual_norm"], rel=1e-13)
+    assert rep.kappa == pytest.approx(ro["kappa"], rel=1e-9)
+    assert rep.loose_upper == pytest.approx(ro["loose_upper"], rel=1e-9)
+    assert rep.verdict.value == ro["verdict"]
+    rep = ck.verify_solution(a, xh, b, ck.VerifyOptions(kappa=50.0, a_norm=3.0))
+    ro = port.verify_solution(a, xh, b, kappa=50.0, a_norm=3.0)
+    for k in ("residual_norm", "b_norm", "xhat_norm", "loose_lower", "loose_upper", "tight_lower",
+              "tight_upper", "true_error_cap", "singularity_cap"):
+        assert getattr(rep, k) == pytest.approx(ro[k], rel=1e-13), k
+    assert rep.kappa_supplied and len(rep.to_kv()) == 15
+    with pytest.raises(ck.ZeroSolution):
+        ck.verify_solution(a, np.zeros(40), b)
+    with pytest.raises(ck.ZeroRHS):
+        ck.verify_solution(a, xh, np.zeros(40))
