@@ -107,3 +107,26 @@ def test_no_silent_cpu_path_without_gpu():
         ck.norm2(ck.SparseMatrix.identity(4))
     with pytest.raises(ck.DeviceUnavailable):
         ck.matvec(ck.SparseMatrix.identity(4), np.ones(4))
+
+
+def _build_dropin(tmp_path, with_reference):
+    exe = tmp_path / ("dropin_ref" if with_reference else "dropin")
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "dropin_demo.cpp"),
+           "-L", os.path.dirname(_lib.LIB_PATH), "-lcondkit_b200",
+           "-Wl,-rpath," + os.path.dirname(_lib.LIB_PATH), "-o", str(exe)]
+    if with_reference:
+        cmd[3:3] = ["-I", "/root/reference/proj/include", "-DWITH_REFERENCE_TYPES"]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return exe
+
+
+def test_cpp_dropin_header_compiles_against_reference_types(tmp_path):
+    # the reference's own condkit::SparseMatrix flows into condkit_b200::cond2 unchanged
+    if not os.path.isdir("/root/reference/proj/include/condkit"):
+        pytest.skip("reference headers not present on this machine")
+    assert _build_dropin(tmp_path, True).exists()
+
+
+def test_cpp_dropin_header_compiles_standalone(tmp_path):
+    assert _build_dropin(tmp_path, False).exists()

@@ -1,0 +1,153 @@
+"""Full-size parity against golden outputs of the reference itself
+(tests/golden/*.json, written by tests/golden/make_golden.py from oracle/_ref).
+
+Tolerances: SpMV bit-exact (stored-order sums); sigma / kappa / the error bound
+within 1e-3 relative after the same iteration count (north_star)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2409_11515_b200 as ck
+from paper_2409_11515_b200 import configs
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-3
+
+
+def gold(name):
+    p = os.path.join(GOLD, name + ".json")
+    if not os.path.exists(p):
+        pytest.skip(f"golden fixture {name}.json not generated yet")
+    with open(p) as f:
+        return json.load(f)
+
+
+def _cmp_est(got, want, tol=TOL):
+    assert got.iterations == want["iterations"]
+    assert got.converged == want["converged"]
+    assert got.value == pytest.approx(want["value"], rel=tol)
+
+
+def _spmv(a, g):
+    x = ck.random_unit_vector(a.ncols, g["x_seed"])
+    y = ck.matvec(a, x)
+    u = ck.random_unit_vector(a.nrows, g["x_seed"] + 1)
+    z = ck.transpose_matvec(a, u)
+    assert np.array_equal(y[np.array(g["y_idx"])], np.array(g["y_val"]))
+    assert np.array_equal(z[np.array(g["z_idx"])], np.array(g["z_val"]))
+    # norms are summed in different orders on both sides: 1e-12, not bitwise
+    assert np.linalg.norm(y) == pytest.approx(g["y_two_norm"], rel=1e-12)
+    assert np.linalg.norm(z) == pytest.approx(g["z_two_norm"], rel=1e-12)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_spmv_full_size_bitwise(k):
+    _spmv(configs.config(k), gold("quick")[f"c{k}_spmv"])
+
+
+def test_config1_sigma_max_and_restarts():
+    g = gold("quick")
+    a = configs.config(1)
+    cfg = configs.baseline_adam(1)
+    _cmp_est(ck.norm2(a, cfg), g["c1_projected_adam"], tol=1e-9)
+    _cmp_est(ck.estimate_norm(ck.ExplicitOracle(a), cfg, 3), g["c1_estimate_norm3"], tol=1e-9)
+
+
+def test_config1_cond2():
+    g = gold("quick")["c1_cond2"]
+    r = ck.cond2(configs.config(1), configs.baseline_adam(1), 3, 1e-14)
+    assert r.kappa == pytest.approx(g["kappa"], rel=TOL)
+    _cmp_est(r.operator_norm, g["operator_norm"])
+    _cmp_est(r.inverse_norm, g["inverse_norm"])
+
+
+def test_config1_sigma_min_single_run():
+    g = gold("quick")["c1_inv_projected_adam"]
+    f = ck.lu_factorize(configs.config(1), 1e-14)
+    e = ck.projected_adam(ck.InverseOracle(f), configs.baseline_adam(ck.mix_seed(1, 0x1234)))
+    _cmp_est(e, g)
+
+
+def test_config2_operator_cond2_and_error_bound():
+    g = gold("quick")
+    s = configs.generate(configs.STOKES, 32, 1)
+    cfg = configs.baseline_adam(1)
+    r = ck.cond2(s, cfg, 1, 1e-14)
+    assert r.kappa == pytest.approx(g["c2_grid32_cond2_r1"]["kappa"], rel=TOL)
+    inp = g["c2_grid32_verify_inputs"]
+    xs = configs.uniform_in(inp["x_seed"], s.ncols, -1.0, 1.0)
+    b = ck.matvec(s, xs)
+    u = ck.random_unit_vector(s.ncols, inp["u_seed"])
+    xh = xs + inp["rel_delta"] * np.linalg.norm(xs) * u
+    rep = ck.verify_solution(s, xh, b, ck.VerifyOptions(adam=cfg, restarts=1))
+    want = g["c2_grid32_verify"]
+    assert rep.residual_norm == pytest.approx(want["residual_norm"], rel=1e-12)
+    assert rep.loose_upper == pytest.approx(want["loose_upper"], rel=TOL)  # kappa ||r|| / ||b||
+    assert rep.tight_upper == pytest.approx(want["tight_upper"], rel=TOL)
+    assert rep.verdict.value == want["verdict"]
+
+
+def test_config2_sigma_max_full_size():
+    g = gold("quick")["c2_projected_adam"]
+    _cmp_est(ck.norm2(configs.config(2), configs.baseline_adam(1)), g)
+
+
+def test_config3_operator_small_grid():
+    g = gold("quick")["c3_grid16_projected_adam"]
+    h = configs.generate(configs.HYDROMECH, 16, 1)
+    _cmp_est(ck.norm2(h, configs.baseline_adam(1)), g)
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_config5_member_cond2(idx):
+    # Config-5 members are numerically singular (kappa >= 1/eps_mach, per-column scales
+    # 10^U(-8,8)): sigma_max is reproduced (here bit for bit), ||A^-1|| is set by the
+    # rounding of the solves and is not a reproducible quantity, so the check is the
+    # verdict class both sides reach (error_bounds.hpp:440 test kappa >= 1/eps).
+    g = gold("quick")[f"c5_member{idx}_n4000_cond2_r4"]
+    m = configs.ensemble_member(idx, 1, n=4000)
+    r = ck.cond2(m, configs.baseline_adam(1), 4, 1e-14)
+    _cmp_est(r.operator_norm, g["operator_norm"], tol=1e-12)
+    assert r.kappa >= 2.0 ** 53 and g["kappa"] >= 2.0 ** 53
+    assert r.inverse_norm.iterations == g["inverse_norm"]["iterations"]
+
+
+def _column_scaled(a):
+    cn = np.zeros(a.ncols)
+    np.add.at(cn, a.col_indices, a.values ** 2)
+    cn = np.sqrt(cn)
+    return ck.SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices,
+                           a.values / cn[a.col_indices])
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_config5_member_column_scaled_cond2(idx):
+    g = gold("c5_scaled")[f"c5_member{idx}_n4000_colscaled_cond2_r4"]
+    m = _column_scaled(configs.ensemble_member(idx, 1, n=4000))
+    r = ck.cond2(m, configs.baseline_adam(1), 4, 1e-14)
+    assert r.kappa == pytest.approx(g["kappa"], rel=TOL)
+    _cmp_est(r.operator_norm, g["operator_norm"])
+    _cmp_est(r.inverse_norm, g["inverse_norm"])
+
+
+def test_config3_sigma_max_full_size():
+    g = gold("c3_sigma_max")["c3_projected_adam"]
+    _cmp_est(ck.norm2(configs.config(3), configs.baseline_adam(1)), g)
+
+
+def test_config4_full_size():
+    g = gold("c4_sigma_max")
+    a = configs.config(4)
+    _spmv(a, g["c4_spmv"])
+    _cmp_est(ck.norm2(a, configs.baseline_adam(1)), g["c4_projected_adam"])
+
+
+def test_config2_cond2_full_size():
+    g = gold("c2_cond2")["c2_cond2_r1"]
+    r = ck.cond2(configs.config(2), configs.baseline_adam(1), 1, 1e-14)
+    assert r.kappa == pytest.approx(g["kappa"], rel=TOL)
+    _cmp_est(r.operator_norm, g["operator_norm"])
+    _cmp_est(r.inverse_norm, g["inverse_norm"])
