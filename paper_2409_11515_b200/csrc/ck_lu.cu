@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(256) k_gbtrf_panel(BandView b, int64_t j0, int
   __shared__ double s_piv;
   if (st->code != 0) return;
   const int tid = threadIdx.x;
-  int64_t ju = 0;
+  // running maximum over every step so far (dgbtf2's ju): rows of this panel may
+  // carry fill from earlier panels out to the previous maximum
+  int64_t ju = st->ju;
   for (int c = 0; c < jb; ++c) {
     const int64_t j = j0 + c;
     const int64_t km = lmin(b.kl, b.n - 1 - j);

@@ -103,16 +103,15 @@ def test_config3_operator_small_grid():
 
 @pytest.mark.parametrize("idx", [0, 1])
 def test_config5_member_cond2(idx):
-    # Config-5 members are numerically singular (kappa >= 1/eps_mach, per-column scales
-    # 10^U(-8,8)): sigma_max is reproduced (here bit for bit), ||A^-1|| is set by the
-    # rounding of the solves and is not a reproducible quantity, so the check is the
-    # verdict class both sides reach (error_bounds.hpp:440 test kappa >= 1/eps).
+    # config-5 members are numerically singular (kappa ~ 1e19 >= 1/eps_mach); the
+    # device LU reproduces the reference's factors, so even ||A^-1|| agrees
     g = gold("quick")[f"c5_member{idx}_n4000_cond2_r4"]
     m = configs.ensemble_member(idx, 1, n=4000)
     r = ck.cond2(m, configs.baseline_adam(1), 4, 1e-14)
+    assert r.kappa == pytest.approx(g["kappa"], rel=TOL)
     _cmp_est(r.operator_norm, g["operator_norm"], tol=1e-12)
+    _cmp_est(r.inverse_norm, g["inverse_norm"])
     assert r.kappa >= 2.0 ** 53 and g["kappa"] >= 2.0 ** 53
-    assert r.inverse_norm.iterations == g["inverse_norm"]["iterations"]
 
 
 def _column_scaled(a):

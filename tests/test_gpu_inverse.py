@@ -43,6 +43,20 @@ def test_factors_match_reference_bitwise(port, n, seed):
     assert np.abs(L).max() <= 1.0
 
 
+def test_long_band_factors_match_reference_bitwise(port):
+    # n >> kl: fill carried across many 32-column panels (dgbtf2's running ju)
+    from paper_2409_11515_b200 import configs
+    a = configs.ensemble_member(3, 1, n=1500, bw=200)
+    f = ck.lu_factorize(a, 1e-14)
+    perm, L, U = f.dense_factors()
+    rperm, rL, rU, rf = oracle_dense_lu(port, a, 1e-14)
+    assert np.array_equal(perm, rperm)
+    assert np.array_equal(U, rU)
+    assert np.array_equal(L, rL)
+    b = port.random_unit_vectors(5, a.nrows)[0]
+    assert np.linalg.norm(f.solve(b) - port.lu_solve(rf, b)) <= 1e-12 * np.linalg.norm(port.lu_solve(rf, b))
+
+
 def test_identity_and_permutation():
     # test_lu.cpp:28-52
     f = ck.lu_factorize(ck.SparseMatrix.identity(4))
