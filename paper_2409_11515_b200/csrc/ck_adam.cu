@@ -87,23 +87,25 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
     dn[r] = es_zero();
     xd[r] = 0.0;
   }
-  const int t0 = blockIdx.x * a.tpu_A;
-  const int t1 = min(t0 + a.tpu_A, a.tiles_A);
-  // slice metadata of the first row, then prefetched one tile ahead
-  int64_t i = (int64_t)t0 * kTile + threadIdx.x;
+  // Tiles are dealt round-robin (tile = blockIdx.x + k * gridDim.x): at any
+  // moment the resident CTAs sweep one contiguous window of the matrix, so the
+  // stencil neighbours of the gathered (x, delta) pairs stay in L2.
+  const int stride = gridDim.x;
+  int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const int64_t istep = (int64_t)stride * kTile;
   int64_t sp0 = 0, sp1 = 0;
   int L = 0;
-  if (t0 < t1 && i < a.nr_pad) {
+  if ((int)blockIdx.x < a.tiles_A && i < a.nr_pad) {
     sp0 = a.A.sp[i >> 5];
     sp1 = a.A.sp[(i >> 5) + 1];
     L = a.A.len[i];
   }
-  for (int tile = t0; tile < t1; ++tile, i += kTile) {
+  for (int tile = blockIdx.x; tile < a.tiles_A; tile += stride, i += istep) {
     const int64_t base = sp0 + (i & 31);
     const int w = (int)((sp1 - sp0) >> 5);  // slice width: uniform across the warp
     const int Lc = L;
-    const int64_t inext = i + kTile;
-    if (tile + 1 < t1 && inext < a.nr_pad) {
+    const int64_t inext = i + istep;
+    if (tile + stride < a.tiles_A && inext < a.nr_pad) {
       sp0 = a.A.sp[inext >> 5];
       sp1 = a.A.sp[(inext >> 5) + 1];
       L = a.A.len[inext];
@@ -255,22 +257,22 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
   double dot[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) dot[r] = 0.0;
-  const int t0 = blockIdx.x * a.tpu_T;
-  const int t1 = min(t0 + a.tpu_T, a.tiles_T);
-  int64_t j = (int64_t)t0 * kTile + threadIdx.x;
+  const int stride = gridDim.x;
+  const int64_t jstep = (int64_t)stride * kTile;
+  int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
   int64_t sp0 = 0, sp1 = 0;
   int L = 0;
-  if (t0 < t1) {
+  if ((int)blockIdx.x < a.tiles_T) {
     sp0 = a.AT.sp[j >> 5];
     sp1 = a.AT.sp[(j >> 5) + 1];
     L = a.AT.len[j];
   }
-  for (int tile = t0; tile < t1; ++tile, j += kTile) {
+  for (int tile = blockIdx.x; tile < a.tiles_T; tile += stride, j += jstep) {
     const int64_t base = sp0 + (j & 31);
     const int w = (int)((sp1 - sp0) >> 5);
     const int Lc = L;
-    if (tile + 1 < t1) {
-      const int64_t jn = j + kTile;
+    if (tile + stride < a.tiles_T) {
+      const int64_t jn = j + jstep;
       sp0 = a.AT.sp[jn >> 5];
       sp1 = a.AT.sp[(jn >> 5) + 1];
       L = a.AT.len[jn];
@@ -591,11 +593,11 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   a.nc_pad = A->at.nrows_pad;
   a.tiles_A = (int)(std::max(a.nr_pad, a.nc_pad) / kTile);
   const int64_t unitsA = 148 * occ_apply(R), unitsT = 148 * occ_transpose(R);
-  a.tpu_A = (int)std::max<int64_t>(1, ceil_div(a.tiles_A, unitsA));
-  a.units_A = (int)ceil_div(a.tiles_A, a.tpu_A);
+  a.tpu_A = 0;  // tiles are dealt round-robin over the grid
+  a.units_A = (int)std::min<int64_t>(a.tiles_A, unitsA);
   a.tiles_T = (int)(a.nc_pad / kTile);
-  a.tpu_T = (int)std::max<int64_t>(1, ceil_div(a.tiles_T, unitsT));
-  a.units_T = (int)ceil_div(a.tiles_T, a.tpu_T);
+  a.tpu_T = 0;
+  a.units_T = (int)std::min<int64_t>(a.tiles_T, unitsT);
   s->partA.alloc((int64_t)a.units_A * R * kPA);
   s->partT.alloc((int64_t)a.units_T * R * kPT);
   const int64_t yw = std::max(a.nr_pad, a.nc_pad) * R;
