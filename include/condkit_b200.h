@@ -143,6 +143,20 @@ ck_status ck_projected_adam(ck_matrix a, const ck_adam_cfg* cfg, ck_norm_result*
 ck_status ck_estimate_norm(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts,
                            ck_norm_result* res, double* witness);
 
+/* Batched ensemble (config 5): S independent square operators packed
+ * block-diagonally into one uploaded matrix, member g at rows/cols
+ * [off_g, off_g + n_g) with off_g = sum over h < g of round_up(n_h, 256).
+ * estimate_norm for every member: restarts with member_seeds[g] (r = 0) or
+ * mix_seed(member_seeds[g], r); results[g] is the best of member g. */
+ck_status ck_estimate_norm_batch(ck_matrix packed, const int64_t* seg_n, int32_t nseg,
+                                 const ck_adam_cfg* cfg, const uint64_t* member_seeds,
+                                 uint64_t restarts, ck_norm_result* results);
+/* Session over a packed batch: nseg members x ncols restart columns; column
+ * k = g * ncols + c in ck_session_result. seeds has nseg * ncols entries. */
+ck_status ck_session_create_batch(ck_matrix packed, const int64_t* seg_n, int32_t nseg,
+                                  const ck_adam_cfg* cfg, const uint64_t* seeds, int32_t ncols,
+                                  ck_session* out);
+
 /* Session: the device-resident loop with explicit control (bench, observer).
  * `ncols` independent runs with seeds[c]; each follows projected_adam exactly. */
 ck_status ck_session_create(ck_matrix a, const ck_adam_cfg* cfg, const uint64_t* seeds,

@@ -1,0 +1,97 @@
+"""Batched ensembles (BASELINE config 5): many independent matrices, several
+restarts each, advanced together by one kernel pair per iteration.
+
+The members are packed block-diagonally into one device operator, each member
+tile-aligned (padded to a multiple of 256 rows/columns with empty rows). Every
+member keeps its own control state, RNG streams, restarts and result; the
+arithmetic of a member is the same as running it alone.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .condest import AdamConfig, NormEstimate, Session
+from .rng import mix_seed
+from .sparse import SparseMatrix
+
+TILE = 256
+
+
+def pack_block_diagonal(members: Sequence[SparseMatrix]):
+    """(packed SparseMatrix, seg_n) with member g at offset sum(round_up(n_h, 256))."""
+    offs, rps, cis, vas = [], [], [], []
+    off = 0
+    nnz = 0
+    for m in members:
+        if m.nrows != m.ncols:
+            raise ValueError("batched members must be square")
+        pad = -(-m.nrows // TILE) * TILE
+        rp = m.row_offsets[1:] + nnz
+        rps.append(rp)
+        rps.append(np.full(pad - m.nrows, rp[-1] if rp.size else nnz, np.int64))
+        cis.append(m.col_indices.astype(np.int64) + off)
+        vas.append(m.values)
+        offs.append(off)
+        off += pad
+        nnz += m.nnz
+    rp = np.concatenate([np.zeros(1, np.int64)] + rps)
+    ci = np.concatenate(cis).astype(np.int32)
+    va = np.concatenate(vas)
+    packed = SparseMatrix(off, off, rp, ci, va, validate=False)
+    return packed, np.array([m.nrows for m in members], np.int64)
+
+
+def member_seeds(count: int, seed: int = 1) -> list[int]:
+    """Per-member estimator seeds, as run_bench seeds cond2 per matrix (bench.hpp:435)."""
+    return [mix_seed(seed, 0x1000 + m) for m in range(count)]
+
+
+def estimate_norm_batch(members: Sequence[SparseMatrix], cfg: Optional[AdamConfig] = None,
+                        restarts: int = 4, seeds: Optional[Sequence[int]] = None,
+                        packed=None) -> list[NormEstimate]:
+    """estimate_norm (condest.hpp:301-312) for every member, all on one device sweep."""
+    cfg = cfg or AdamConfig()
+    if packed is None:
+        packed = pack_block_diagonal(members)
+    a, seg_n = packed
+    seeds = np.ascontiguousarray(seeds if seeds is not None else [cfg.seed] * seg_n.size,
+                                 np.uint64)
+    res = (_lib.NormResult * seg_n.size)()
+    c = _lib.cfg_struct(cfg)
+    _lib.check(_lib.load().ck_estimate_norm_batch(
+        a.device().handle, seg_n.ctypes.data_as(_lib.i64p), int(seg_n.size), C.byref(c),
+        seeds.ctypes.data_as(_lib.u64p), restarts, res), "estimate_norm_batch")
+    return [NormEstimate(r.value, np.zeros(0), int(r.iterations), bool(r.converged)) for r in res]
+
+
+class BatchSession(Session):
+    """Device loop over a packed batch: members x restart columns (bench / inspection)."""
+
+    def __init__(self, packed, cfg: AdamConfig, seeds_per_member_column):
+        a, seg_n = packed
+        self.oracle = a  # keeps the device matrix alive
+        self.seg_n = seg_n
+        self.n = int(seg_n.max())
+        seeds = np.ascontiguousarray(seeds_per_member_column, np.uint64)
+        self.ncols = seeds.size // seg_n.size
+        lib = _lib.load()
+        self._cfg = _lib.cfg_struct(cfg)
+        h = C.c_void_p()
+        _lib.check(lib.ck_session_create_batch(a.device().handle, seg_n.ctypes.data_as(_lib.i64p),
+                                               int(seg_n.size), C.byref(self._cfg),
+                                               seeds.ctypes.data_as(_lib.u64p), self.ncols,
+                                               C.byref(h)), "ck_session_create_batch")
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.ck_session_free, h)
+
+    def member_result(self, g: int, c: int = 0) -> NormEstimate:
+        r = _lib.NormResult()
+        w = np.empty(int(self.seg_n[g]))
+        _lib.check(_lib.load().ck_session_result(self.handle, g * self.ncols + c, C.byref(r),
+                                                 _lib.dptr(w)), "ck_session_result")
+        return NormEstimate(r.value, w, int(r.iterations), bool(r.converged))

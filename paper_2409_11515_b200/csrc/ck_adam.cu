@@ -53,6 +53,30 @@ struct Occ {
   static constexpr int transpose = R <= 2 ? 4 : 2;
 };
 
+// Work assignment of CTA `unit`. One operator (S == 1): the tiles are dealt
+// round-robin over the grid, so at any moment the resident CTAs sweep one
+// contiguous window of the matrix and the stencil neighbours of the gathered
+// vectors stay in L2. A block-diagonal batch (S > 1, config 5): each unit owns
+// a contiguous tile range inside one member.
+__device__ __forceinline__ void unit_range(const LoopArgs& a, int unit, int tiles, int& seg,
+                                           int& t0, int& tend, int& stride, int& u0, int& u1) {
+  if (a.S == 1) {
+    seg = 0;
+    t0 = unit;
+    tend = tiles;
+    stride = gridDim.x;
+    u0 = 0;
+    u1 = gridDim.x;
+  } else {
+    seg = a.unit_seg[unit];
+    t0 = a.unit_t0[unit];
+    tend = a.unit_t1[unit];
+    stride = 1;
+    u0 = a.seg_u0[seg];
+    u1 = a.seg_u0[seg + 1];
+  }
+}
+
 // x~ from a stored (x, delta) pair: x - (delta - r x)  (:232, :240)
 __device__ __forceinline__ double xtilde(double2 p, double rad) {
   return __dsub_rn(p.x, __dsub_rn(p.y, __dmul_rn(rad, p.x)));
@@ -60,7 +84,11 @@ __device__ __forceinline__ double xtilde(double2 p, double rad) {
 
 template <int R, bool OBS, int U = (R == 1 ? 8 : 4)>
 __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_constant__ LoopArgs a) {
-  if (!a.hdr->needA) return;
+  int seg, tile0, tend, stride, u0, u1;
+  unit_range(a, blockIdx.x, a.tiles_A, seg, tile0, tend, stride, u0, u1);
+  Header* hdr = a.hdr + seg;
+  if (!hdr->needA) return;
+  ColState* sts = a.st + (int64_t)seg * R;
   __shared__ double s_h[8], s_l[8];
   __shared__ int s_e[8], s_f[8];
   __shared__ double s_res[R][4];
@@ -70,12 +98,12 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
   const double2* xc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int ph = a.st[r].phase;
+    const int ph = sts[r].phase;
     act[r] = ph == PH_PRO || ph == PH_APPLY;
     pro[r] = ph == PH_PRO;
     // prologue: delta is zero, so x~ = x exactly (x - (0 - 0 x) = x)
-    rad[r] = pro[r] ? 0.0 : a.st[r].rad;
-    xc[r] = a.PX + ((int64_t)a.st[r].cur * R + r) * a.nc_pad;
+    rad[r] = pro[r] ? 0.0 : sts[r].rad;
+    xc[r] = a.PX + ((int64_t)sts[r].cur * R + r) * a.nc_pad;
   }
   DD dd[R];
   ES es[R], dn[R];
@@ -87,25 +115,21 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
     dn[r] = es_zero();
     xd[r] = 0.0;
   }
-  // Tiles are dealt round-robin (tile = blockIdx.x + k * gridDim.x): at any
-  // moment the resident CTAs sweep one contiguous window of the matrix, so the
-  // stencil neighbours of the gathered (x, delta) pairs stay in L2.
-  const int stride = gridDim.x;
-  int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  int64_t i = (int64_t)tile0 * kTile + threadIdx.x;
   const int64_t istep = (int64_t)stride * kTile;
   int64_t sp0 = 0, sp1 = 0;
   int L = 0;
-  if ((int)blockIdx.x < a.tiles_A && i < a.nr_pad) {
+  if (tile0 < tend && i < a.nr_pad) {
     sp0 = a.A.sp[i >> 5];
     sp1 = a.A.sp[(i >> 5) + 1];
     L = a.A.len[i];
   }
-  for (int tile = blockIdx.x; tile < a.tiles_A; tile += stride, i += istep) {
+  for (int tile = tile0; tile < tend; tile += stride, i += istep) {
     const int64_t base = sp0 + (i & 31);
     const int w = (int)((sp1 - sp0) >> 5);  // slice width: uniform across the warp
     const int Lc = L;
     const int64_t inext = i + istep;
-    if (tile + stride < a.tiles_A && inext < a.nr_pad) {
+    if (tile + stride < tend && inext < a.nr_pad) {
       sp0 = a.A.sp[inext >> 5];
       sp1 = a.A.sp[(inext >> 5) + 1];
       L = a.A.len[inext];
@@ -174,15 +198,15 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
       p[8] = (double)e2.flags;
     }
   }
-  if (!elect_last_block(&a.hdr->cntA, (unsigned)a.units_A)) return;
+  if (!elect_last_block(&hdr->cntA, (unsigned)(u1 - u0))) return;
 
-  // Last CTA: fixed-order merge of all partials, then the control step.
+  // Last CTA (of this member): fixed-order merge of its partials, then control.
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     DD d = dd_zero();
     ES e = es_zero(), e2 = es_zero();
     double x2 = 0.0;
-    for (int u = threadIdx.x; u < a.units_A; u += kTile) {
+    for (int u = u0 + threadIdx.x; u < u1; u += kTile) {
       const double* p = a.partA + ((int64_t)u * R + r) * kPA;
       dd_merge(d, DD{__ldcg(p), __ldcg(p + 1)});
       es_merge(e, ES{__ldcg(p + 2), (int)__ldcg(p + 3), (int)__ldcg(p + 4)});
@@ -207,7 +231,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
   if (threadIdx.x == 0) {
     int needT = 0, nwait = 0, ndone = 0;
     for (int r = 0; r < R; ++r) {
-      ColState* s = a.st + r;
+      ColState* s = sts + r;
       const int ph = s->phase;
       if (ph == PH_PRO || ph == PH_APPLY) {
         if (OBS && ph == PH_APPLY) {
@@ -220,17 +244,21 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
       nwait += s->phase == PH_WAIT;
       ndone += s->phase == PH_DONE;
     }
-    a.hdr->needT = needT;
-    a.hdr->needA = 0;
-    a.hdr->nwait = nwait;
-    a.hdr->ndone = ndone;
+    hdr->needT = needT;
+    hdr->needA = 0;
+    hdr->nwait = nwait;
+    hdr->ndone = ndone;
   }
 }
 
 template <int R, int U = (R <= 2 ? 8 : 4)>
 __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     k_transpose(const __grid_constant__ LoopArgs a) {
-  if (!a.hdr->needT) return;
+  int seg, tile0, tend, stride, u0, u1;
+  unit_range(a, blockIdx.x, a.tiles_T, seg, tile0, tend, stride, u0, u1);
+  Header* hdr = a.hdr + seg;
+  if (!hdr->needT) return;
+  ColState* sts = a.st + (int64_t)seg * R;
   __shared__ double s_h[8];
   __shared__ double s_res[R];
   const Params& p = a.prm;
@@ -240,7 +268,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
   double2* xn_out[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const ColState& s = a.st[r];
+    const ColState& s = sts[r];
     act[r] = s.phase == PH_GRAD;
     mat[r] = s.mat != 0;
     rad[r] = s.rad;
@@ -257,21 +285,20 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
   double dot[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) dot[r] = 0.0;
-  const int stride = gridDim.x;
   const int64_t jstep = (int64_t)stride * kTile;
-  int64_t j = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  int64_t j = (int64_t)tile0 * kTile + threadIdx.x;
   int64_t sp0 = 0, sp1 = 0;
   int L = 0;
-  if ((int)blockIdx.x < a.tiles_T) {
+  if (tile0 < tend) {
     sp0 = a.AT.sp[j >> 5];
     sp1 = a.AT.sp[(j >> 5) + 1];
     L = a.AT.len[j];
   }
-  for (int tile = blockIdx.x; tile < a.tiles_T; tile += stride, j += jstep) {
+  for (int tile = tile0; tile < tend; tile += stride, j += jstep) {
     const int64_t base = sp0 + (j & 31);
     const int w = (int)((sp1 - sp0) >> 5);
     const int Lc = L;
-    if (tile + stride < a.tiles_T) {
+    if (tile + stride < tend) {
       const int64_t jn = j + jstep;
       sp0 = a.AT.sp[jn >> 5];
       sp1 = a.AT.sp[(jn >> 5) + 1];
@@ -320,11 +347,11 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     const double s = block_sum(dot[r], s_h);
     if (threadIdx.x == 0) a.partT[(int64_t)blockIdx.x * R + r] = s;
   }
-  if (!elect_last_block(&a.hdr->cntT, (unsigned)a.units_T)) return;
+  if (!elect_last_block(&hdr->cntT, (unsigned)(u1 - u0))) return;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     double s = 0.0;
-    for (int u = threadIdx.x; u < a.units_T; u += kTile)
+    for (int u = u0 + threadIdx.x; u < u1; u += kTile)
       s = __dadd_rn(s, __ldcg(a.partT + (int64_t)u * R + r));
     s = block_sum(s, s_h);
     if (threadIdx.x == 0) s_res[r] = s;
@@ -332,7 +359,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
   if (threadIdx.x == 0) {
     int needA = 0;
     for (int r = 0; r < R; ++r) {
-      ColState* s = a.st + r;
+      ColState* s = sts + r;
       if (s->phase == PH_GRAD) {
         s->rad = s_res[r];
         if (s->mat) {
@@ -343,8 +370,8 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
       }
       needA |= s->phase == PH_APPLY;
     }
-    a.hdr->needA = needA;
-    a.hdr->needT = 0;
+    hdr->needA = needA;
+    hdr->needT = 0;
   }
 }
 
@@ -441,80 +468,104 @@ static int occ_transpose(int R) {
 
 static void pull_state(ck_session_s* s) {
   cudaStream_t st = s->stream;
-  CK_CUDA(cudaMemcpyAsync(s->h_st, s->st.p, sizeof(ColState) * s->R, cudaMemcpyDeviceToHost, st));
-  CK_CUDA(cudaMemcpyAsync(s->h_hdr, s->hdr.p, sizeof(Header), cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaMemcpyAsync(s->h_st, s->st.p, sizeof(ColState) * s->S * s->R,
+                          cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaMemcpyAsync(s->h_hdr, s->hdr.p, sizeof(Header) * s->S, cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
 static void push_state(ck_session_s* s) {
   cudaStream_t st = s->stream;
-  CK_CUDA(cudaMemcpyAsync(s->st.p, s->h_st, sizeof(ColState) * s->R, cudaMemcpyHostToDevice, st));
-  CK_CUDA(cudaMemcpyAsync(s->hdr.p, s->h_hdr, sizeof(Header), cudaMemcpyHostToDevice, st));
+  CK_CUDA(cudaMemcpyAsync(s->st.p, s->h_st, sizeof(ColState) * s->S * s->R,
+                          cudaMemcpyHostToDevice, st));
+  CK_CUDA(cudaMemcpyAsync(s->hdr.p, s->h_hdr, sizeof(Header) * s->S, cudaMemcpyHostToDevice, st));
   CK_CUDA(cudaStreamSynchronize(st));
+}
+
+static int64_t total_done(const ck_session_s* s) {
+  int64_t d = 0;
+  for (int g = 0; g < s->S; ++g) d += s->h_hdr[g].ndone;
+  return d;
+}
+
+static bool any_wait(const ck_session_s* s) {
+  for (int g = 0; g < s->S; ++g)
+    if (s->h_hdr[g].nwait > 0) return true;
+  return false;
 }
 
 static double2* col_buf(ck_session_s* s, int b, int c) {
   return s->PX.p + ((int64_t)b * s->R + c) * s->npad;
 }
 
-// host vector (original order) -> internal plain vector `dst` (npad doubles)
-static void to_internal(ck_session_s* s, const double* host, double* dst, cudaStream_t st) {
+// host vector of member g (original order, seg_n[g] doubles) -> internal plain
+// vector `dst` over the member's internal range [seg_off[g], seg_off[g]+seg_pad[g])
+static void to_internal(ck_session_s* s, int g, const double* host, double* dst,
+                        cudaStream_t st) {
+  const int64_t off = s->seg_off[g], pad = s->seg_pad[g];
+  CK_CUDA(cudaMemsetAsync(s->tmp.p + off, 0, sizeof(double) * pad, st));
   if (s->perm) {
-    CK_CUDA(cudaMemcpyAsync(s->tmp.p, host, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
-    gather_perm(s->perm, s->npad, s->tmp.p, dst, st);
+    CK_CUDA(cudaMemcpyAsync(s->tmp.p + off, host, sizeof(double) * s->seg_n[g],
+                            cudaMemcpyHostToDevice, st));
+    gather_perm(s->perm + off, pad, s->tmp.p, dst + off, st);
   } else {
-    CK_CUDA(cudaMemcpyAsync(dst, host, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
+    CK_CUDA(cudaMemcpyAsync(dst + off, host, sizeof(double) * s->seg_n[g], cudaMemcpyHostToDevice,
+                            st));
   }
 }
 
-// internal plain vector -> host vector (original order); `src` may be s->tmp + npad
-static void to_host(ck_session_s* s, const double* src, double* host, cudaStream_t st) {
-  const double* out = src;
+// internal plain vector -> host vector of member g (original order)
+static void to_host(ck_session_s* s, int g, const double* src, double* host, cudaStream_t st) {
+  const int64_t off = s->seg_off[g], pad = s->seg_pad[g];
+  const double* out = src + off;
   if (s->perm) {
     double* scratch = s->tmp.p;
-    scatter_perm(s->perm, s->npad, src, scratch, st);
-    out = scratch;
+    scatter_perm(s->perm + off, pad, src + off, scratch, st);
+    out = scratch + off;
   }
-  CK_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * s->n, cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * s->seg_n[g], cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
-// Upload a fresh start vector for column c (original order) into buffer b:
-// (x, delta = 0) pairs in the internal (permuted) space, m = v = 0.
-static void load_start(ck_session_s* s, int c, int b, const double* x) {
+// Upload a fresh start vector for member g, column c into buffer b: (x,
+// delta = 0) pairs in the internal (permuted) space, m = v = 0.
+static void load_start(ck_session_s* s, int g, int c, int b, const double* x) {
   cudaStream_t st = s->stream;
-  const int64_t ncp = s->npad;
-  double* perm = s->tmp.p + ncp;
-  CK_CUDA(cudaMemsetAsync(perm, 0, sizeof(double) * ncp, st));
-  to_internal(s, x, perm, st);
-  k_store_x<<<grid256(ncp), 256, 0, st>>>(ncp, perm, col_buf(s, b, c));
-  k_zero_moments<<<grid256(ncp), 256, 0, st>>>(ncp, s->R, c, s->MV.p);
+  const int64_t off = s->seg_off[g], pad = s->seg_pad[g];
+  double* plain = s->tmp.p + s->thalf;
+  CK_CUDA(cudaMemsetAsync(plain + off, 0, sizeof(double) * pad, st));
+  to_internal(s, g, x, plain, st);
+  k_store_x<<<grid256(pad), 256, 0, st>>>(pad, plain + off, col_buf(s, b, c) + off);
+  k_zero_moments<<<grid256(pad), 256, 0, st>>>(pad, s->R, c, s->MV.p + off * s->R);
   CK_CUDA(cudaGetLastError());
-  CK_CUDA(cudaStreamSynchronize(st));
 }
 
 // restart(), condest.hpp:201-207: the next vector of the column's own stream,
 // m = v = 0, bias powers reset; x_min and the patience counters are kept.
 static void service_restarts(ck_session_s* s) {
   bool any = false;
-  for (int c = 0; c < s->R; ++c) {
-    ColState& cs = s->h_st[c];
-    if (cs.phase != PH_WAIT) continue;
-    random_unit_vector_host(&s->gens[c], s->n, s->hx.data());
-    const int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
-    load_start(s, c, b, s->hx.data());
-    cs.cur = b;
-    cs.b1p = 1.0;
-    cs.b2p = 1.0;
-    cs.mat = 0;
-    cs.pend = 0;
-    cs.rad = 0.0;
-    cs.phase = PH_PRO;
-    any = true;
+  for (int g = 0; g < s->S; ++g) {
+    for (int c = 0; c < s->R; ++c) {
+      const int k = g * s->R + c;
+      ColState& cs = s->h_st[k];
+      if (cs.phase != PH_WAIT) continue;
+      random_unit_vector_host(&s->gens[k], s->seg_n[g], s->hx.data());
+      const int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
+      load_start(s, g, c, b, s->hx.data());
+      cs.cur = b;
+      cs.b1p = 1.0;
+      cs.b2p = 1.0;
+      cs.mat = 0;
+      cs.pend = 0;
+      cs.rad = 0.0;
+      cs.phase = PH_PRO;
+      s->h_hdr[g].needA = 1;
+      s->h_hdr[g].nwait = 0;
+      any = true;
+    }
   }
   if (any) {
-    s->h_hdr->needA = 1;
-    s->h_hdr->nwait = 0;
+    CK_CUDA(cudaStreamSynchronize(s->stream));
     push_state(s);
   }
 }
@@ -530,39 +581,46 @@ static void build_graph(ck_session_s* s, int steps) {
   s->gsteps = steps;
 }
 
-// Common part of session creation: state buffers, x0 per column, graphs.
+// Common part of session creation: state buffers, x0 per (member, column), graphs.
 static void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t* seeds,
-                                int R, int64_t ywords, double bytes_per_step) {
+                                int64_t ywords, double bytes_per_step) {
   cudaStream_t st = s->stream;
+  const int R = s->R, S = s->S;
   s->thalf = std::max(s->npad, ywords / R);
   s->tmp.alloc(2 * s->thalf);
   CK_CUDA(cudaMemsetAsync(s->PX.p, 0, s->PX.bytes(), st));
   CK_CUDA(cudaMemsetAsync(s->MV.p, 0, s->MV.bytes(), st));
   CK_CUDA(cudaMemsetAsync(s->y.p, 0, s->y.bytes(), st));
-  CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_st), sizeof(ColState) * R));
-  CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_hdr), sizeof(Header)));
-  s->hx.resize((size_t)s->n);
+  CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_st), sizeof(ColState) * S * R));
+  CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_hdr), sizeof(Header) * S));
+  int64_t nmax = 0;
+  for (int g = 0; g < S; ++g) nmax = std::max(nmax, s->seg_n[g]);
+  s->hx.resize((size_t)nmax);
   s->gens.clear();
-  for (int c = 0; c < R; ++c) {
-    s->gens.emplace_back(seeds[c]);
-    random_unit_vector_host(&s->gens[c], s->n, s->hx.data());  // x0, rng.hpp:68-77
-    load_start(s, c, 0, s->hx.data());
-    ColState cs{};
-    cs.phase = cfg->max_iter == 0 ? PH_DONE : PH_PRO;
-    cs.cur = 0;
-    cs.best = 0;  // x_min = x (condest.hpp:194)
-    cs.nxt = 1;
-    cs.budget = 16;
-    cs.b1p = cs.b2p = 1.0;
-    cs.loss_min = INFINITY;
-    cs.loss = NAN;
-    s->h_st[c] = cs;
+  s->gens.reserve((size_t)S * R);
+  for (int g = 0; g < S; ++g) {
+    for (int c = 0; c < R; ++c) {
+      s->gens.emplace_back(seeds[g * R + c]);
+      random_unit_vector_host(&s->gens.back(), s->seg_n[g], s->hx.data());  // x0, rng.hpp:68-77
+      load_start(s, g, c, 0, s->hx.data());
+      CK_CUDA(cudaStreamSynchronize(st));  // hx is reused for the next upload
+      ColState cs{};
+      cs.phase = cfg->max_iter == 0 ? PH_DONE : PH_PRO;
+      cs.cur = 0;
+      cs.best = 0;  // x_min = x (condest.hpp:194)
+      cs.nxt = 1;
+      cs.budget = 16;
+      cs.b1p = cs.b2p = 1.0;
+      cs.loss_min = INFINITY;
+      cs.loss = NAN;
+      s->h_st[g * R + c] = cs;
+    }
+    Header h{};
+    h.needA = cfg->max_iter == 0 ? 0 : 1;
+    h.ncols = R;
+    h.ndone = cfg->max_iter == 0 ? R : 0;
+    s->h_hdr[g] = h;
   }
-  Header h{};
-  h.needA = cfg->max_iter == 0 ? 0 : 1;
-  h.ncols = R;
-  h.ndone = cfg->max_iter == 0 ? R : 0;
-  *s->h_hdr = h;
   push_state(s);
   // chunk length: about 4 ms of device work per host round trip, 4..256 steps
   const int steps =
@@ -570,13 +628,18 @@ static void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const u
   build_graph(s, steps);
 }
 
-void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
-                    const uint64_t* seeds, int R) {
+// Explicit-operator session over S >= 1 square-or-rectangular members packed
+// block-diagonally in A (member g occupies rows/cols [off_g, off_g + n_g) with
+// off_g = sum of round_up(n_h, 256), h < g). S == 1 is a single operator.
+static void session_create_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
+                                    const uint64_t* seeds, int R, const int64_t* seg_n, int S) {
   if (R < 1 || R > kMaxCols) fail(CK_ERR_INVALID_ARGUMENT, "session columns must be 1..4");
   if (A->ncols == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
+  if (S < 1) fail(CK_ERR_INVALID_ARGUMENT, "at least one member");
   s->kind = 0;
   s->A = A;
   s->R = R;
+  s->S = S;
   s->stream = A->stream;
   s->device = A->device;
   s->n = A->ncols;
@@ -584,6 +647,24 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   s->perm = A->at.perm.p;
   s->prm = Params{cfg->alpha, cfg->beta1, cfg->beta2, cfg->eps_stab, cfg->rel_tol, cfg->max_iter,
                   cfg->patience};
+  s->seg_n.assign(S, 0);
+  s->seg_off.assign(S, 0);
+  s->seg_pad.assign(S, 0);
+  if (S == 1) {
+    s->seg_n[0] = A->ncols;
+    s->seg_pad[0] = s->npad;
+  } else {
+    if (A->nrows != A->ncols) fail(CK_ERR_DIMENSION, "batched members must be square");
+    int64_t off = 0;
+    for (int g = 0; g < S; ++g) {
+      if (seg_n[g] <= 0) fail(CK_ERR_INVALID_ARGUMENT, "empty batch member");
+      s->seg_n[g] = seg_n[g];
+      s->seg_off[g] = off;
+      s->seg_pad[g] = round_up(seg_n[g], kTile);
+      off += s->seg_pad[g];
+    }
+    if (off != A->nrows) fail(CK_ERR_DIMENSION, "member sizes do not tile the packed matrix");
+  }
   LoopArgs& a = s->args;
   a.A = view(A->a);
   a.AT = view(A->at);
@@ -592,12 +673,38 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   a.nr_pad = A->a.nrows_pad;
   a.nc_pad = A->at.nrows_pad;
   a.tiles_A = (int)(std::max(a.nr_pad, a.nc_pad) / kTile);
-  const int64_t unitsA = 148 * occ_apply(R), unitsT = 148 * occ_transpose(R);
-  a.tpu_A = 0;  // tiles are dealt round-robin over the grid
-  a.units_A = (int)std::min<int64_t>(a.tiles_A, unitsA);
   a.tiles_T = (int)(a.nc_pad / kTile);
-  a.tpu_T = 0;
-  a.units_T = (int)std::min<int64_t>(a.tiles_T, unitsT);
+  a.S = S;
+  a.tpu_A = a.tpu_T = 0;
+  if (S == 1) {
+    a.units_A = (int)std::min<int64_t>(a.tiles_A, 148 * occ_apply(R));
+    a.units_T = (int)std::min<int64_t>(a.tiles_T, 148 * occ_transpose(R));
+    a.unit_seg = a.unit_t0 = a.unit_t1 = a.seg_u0 = nullptr;
+  } else {
+    // members are tile-aligned; each unit takes up to 8 consecutive tiles of one member
+    std::vector<int32_t> useg, ut0, ut1, su0(S + 1, 0);
+    for (int g = 0; g < S; ++g) {
+      const int t0 = (int)(s->seg_off[g] / kTile), nt = (int)(s->seg_pad[g] / kTile);
+      su0[g] = (int)useg.size();
+      for (int t = 0; t < nt; t += 8) {
+        useg.push_back(g);
+        ut0.push_back(t0 + t);
+        ut1.push_back(t0 + std::min(nt, t + 8));
+      }
+    }
+    su0[S] = (int)useg.size();
+    a.units_A = a.units_T = (int)useg.size();
+    s->units.alloc(3 * (int64_t)useg.size() + S + 1);
+    int32_t* d = s->units.p;
+    CK_CUDA(cudaMemcpy(d, useg.data(), sizeof(int32_t) * useg.size(), cudaMemcpyHostToDevice));
+    CK_CUDA(cudaMemcpy(d + useg.size(), ut0.data(), sizeof(int32_t) * useg.size(), cudaMemcpyHostToDevice));
+    CK_CUDA(cudaMemcpy(d + 2 * useg.size(), ut1.data(), sizeof(int32_t) * useg.size(), cudaMemcpyHostToDevice));
+    CK_CUDA(cudaMemcpy(d + 3 * useg.size(), su0.data(), sizeof(int32_t) * (S + 1), cudaMemcpyHostToDevice));
+    a.unit_seg = d;
+    a.unit_t0 = d + useg.size();
+    a.unit_t1 = d + 2 * useg.size();
+    a.seg_u0 = d + 3 * useg.size();
+  }
   s->partA.alloc((int64_t)a.units_A * R * kPA);
   s->partT.alloc((int64_t)a.units_T * R * kPT);
   const int64_t yw = std::max(a.nr_pad, a.nc_pad) * R;
@@ -605,8 +712,8 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   s->PX.alloc(3 * R * s->npad);
   s->MV.alloc(s->npad * R);
   s->y.alloc(yw);
-  s->st.alloc(R);
-  s->hdr.alloc(1);
+  s->st.alloc((int64_t)S * R);
+  s->hdr.alloc(S);
   a.PX = s->PX.p;
   a.MV = s->MV.p;
   a.y = s->y.p;
@@ -615,7 +722,17 @@ void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
   a.st = s->st.p;
   a.hdr = s->hdr.p;
   const double bytes_per_step = 24.0 * (double)A->nnz + 100.0 * (double)A->ncols * R;
-  session_init_common(s, cfg, seeds, R, yw, bytes_per_step);
+  session_init_common(s, cfg, seeds, yw, bytes_per_step);
+}
+
+void session_create(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
+                    const uint64_t* seeds, int R) {
+  session_create_explicit(s, A, cfg, seeds, R, nullptr, 1);
+}
+
+void session_create_batch(ck_session_s* s, ck_matrix_s* A, const int64_t* seg_n, int S,
+                          const ck_adam_cfg* cfg, const uint64_t* seeds, int R) {
+  session_create_explicit(s, A, cfg, seeds, R, seg_n, S);
 }
 
 void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg,
@@ -626,11 +743,15 @@ void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg
   s->lu = lu;
   s->A = nullptr;
   s->R = R;
+  s->S = 1;
   s->stream = lu->stream;
   s->device = lu->device;
   s->n = lu->n;
   s->npad = lu->n;
   s->perm = nullptr;
+  s->seg_n.assign(1, lu->n);
+  s->seg_off.assign(1, 0);
+  s->seg_pad.assign(1, lu->n);
   s->prm = Params{cfg->alpha, cfg->beta1, cfg->beta2, cfg->eps_stab, cfg->rel_tol, cfg->max_iter,
                   cfg->patience};
   const BandView b = lu->view();
@@ -653,7 +774,7 @@ void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg
   a.prm = s->prm;
   a.half = 0;
   const double bytes_per_step = 8.0 * 4.0 * (double)(2 * lu->kl + lu->ku + 1) * (double)lu->n;
-  session_init_common(s, cfg, seeds, R, yw, bytes_per_step * 50.0);
+  session_init_common(s, cfg, seeds, yw, bytes_per_step * 50.0);
 }
 
 void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished) {
@@ -662,11 +783,11 @@ void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished) {
   *finished = 0;
   for (;;) {
     pull_state(s);
-    if (s->h_hdr->ndone == s->R) {
+    if (total_done(s) == (int64_t)s->S * s->R) {
       *finished = 1;
       return;
     }
-    if (s->h_hdr->nwait > 0) service_restarts(s);
+    if (any_wait(s)) service_restarts(s);
     if (max_steps && done >= max_steps) return;
     if (s->observe_on || (max_steps && max_steps - done < (uint64_t)s->gsteps)) {
       const uint64_t n = max_steps ? std::min<uint64_t>(max_steps - done, s->gsteps) : s->gsteps;
@@ -684,7 +805,7 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
                   double* ms_apply, double* ms_transpose) {
   cudaStream_t st = s->stream;
   pull_state(s);
-  if (s->h_hdr->nwait > 0) service_restarts(s);
+  if (any_wait(s)) service_restarts(s);
   if (mode == 1 || s->kind == 1) {  // whole steps (graph chunks), no per-kernel split
     cudaEvent_t e0, e1;
     CK_CUDA(cudaEventCreate(&e0));
@@ -734,13 +855,9 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
   *ms_transpose = tt;
 }
 
-// x of buffer b / column c as a plain internal vector in `out` (npad doubles).
-static void extract_x(ck_session_s* s, int b, int c, double* out, cudaStream_t st) {
-  k_extract_x<<<grid256(s->npad), 256, 0, st>>>(s->npad, col_buf(s, b, c), out);
-  CK_CUDA(cudaGetLastError());
-}
 
-// ||Op v|| for an internal plain vector v (witness re-check, condest.hpp:284-289).
+// ||Op v|| for an internal plain vector v (witness re-check, condest.hpp:284-289);
+// v is zero outside the member's range, so the whole-operator norm is the member's.
 static double op_norm(ck_session_s* s, const double* v, cudaStream_t st) {
   if (s->kind == 0) {
     matrix_apply_perm(s->A, v, s->tmp.p, st);
@@ -753,22 +870,24 @@ static double op_norm(ck_session_s* s, const double* v, cudaStream_t st) {
   return device_norm(w, s->n, w + s->n, st);
 }
 
-// Final NormEstimate for column c (condest.hpp:278-296).
-void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness) {
-  if (c < 0 || c >= s->R) fail(CK_ERR_INVALID_ARGUMENT, "column out of range");
+// Final NormEstimate of column k = g * R + c (member g, restart column c),
+// condest.hpp:278-296.
+void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness) {
+  if (k < 0 || k >= s->S * s->R) fail(CK_ERR_INVALID_ARGUMENT, "column out of range");
+  const int g = k / s->R, c = k % s->R;
   cudaStream_t st = s->stream;
   pull_state(s);
-  ColState& cs = s->h_st[c];
-  const int64_t ncp = s->npad;
+  ColState& cs = s->h_st[k];
+  const int64_t ncp = s->npad, off = s->seg_off[g], pad = s->seg_pad[g];
   double* xbest = s->tmp.p + s->thalf;  // plain copy of x_min (internal order)
+  CK_CUDA(cudaMemsetAsync(xbest, 0, sizeof(double) * ncp, st));
   if (cs.pend) {  // x_{t+1} became the best but was never materialised
-    CK_CUDA(cudaMemsetAsync(xbest, 0, sizeof(double) * ncp, st));
-    k_materialise<<<grid256(ncp), 256, 0, st>>>(s->n, col_buf(s, cs.cur, c), cs.rad, cs.ndiv,
-                                                xbest);
-    CK_CUDA(cudaGetLastError());
+    k_materialise<<<grid256(pad), 256, 0, st>>>(s->S == 1 ? s->n : pad, col_buf(s, cs.cur, c) + off,
+                                               cs.rad, cs.ndiv, xbest + off);
   } else {
-    extract_x(s, cs.best, c, xbest, st);
+    k_extract_x<<<grid256(pad), 256, 0, st>>>(pad, col_buf(s, cs.best, c) + off, xbest + off);
   }
+  CK_CUDA(cudaGetLastError());
   res->iterations = cs.t;
   res->converged = cs.converged;
   res->_pad = 0;
@@ -781,15 +900,13 @@ void session_result(ck_session_s* s, int c, ck_norm_result* res, double* witness
     res->value = 0.0;
     res->converged = 0;
   }
-  if (witness) {
-    if (s->perm) {
-      // to_host uses tmp[0, npad) as scratch; xbest lives at tmp + npad
-      to_host(s, xbest, witness, st);
-    } else {
-      CK_CUDA(cudaMemcpyAsync(witness, xbest, sizeof(double) * s->n, cudaMemcpyDeviceToHost, st));
-      CK_CUDA(cudaStreamSynchronize(st));
-    }
-  }
+  if (witness) to_host(s, g, xbest, witness, st);
+}
+
+// x of buffer b / column c as a plain internal vector in `out` (npad doubles).
+static void extract_x(ck_session_s* s, int b, int c, double* out, cudaStream_t st) {
+  k_extract_x<<<grid256(s->npad), 256, 0, st>>>(s->npad, col_buf(s, b, c), out);
+  CK_CUDA(cudaGetLastError());
 }
 
 // Observer mode (AdamObserver, condest.hpp:234-238, 268-271) for column 0:
@@ -814,7 +931,7 @@ void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, doubl
       info->loss_min = s->h_st[0].loss_min;
       return;
     }
-    if (s->h_hdr->nwait > 0) service_restarts(s);
+    if (any_wait(s)) service_restarts(s);
     launch_apply_only(s, st);
     CK_CUDA(cudaGetLastError());
     pull_state(s);
@@ -837,8 +954,8 @@ void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, doubl
     info->x_dot_delta = cs.obs_xd;
     info->delta_norm = cs.obs_dn;
     info->phase = 0;
-    if (x) to_host(s, xnext, x, st);
-    if (x_min) to_host(s, cs.pend ? xnext : xm, x_min, st);
+    if (x) to_host(s, 0, xnext, x, st);
+    if (x_min) to_host(s, 0, cs.pend ? xnext : xm, x_min, st);
     return;
   }
 }

@@ -676,3 +676,66 @@ ck_status ck_grad_inverse(ck_lu f, const double* x, double* g) {
 }
 
 }  // extern "C"
+
+namespace ck {
+void session_create_batch(ck_session_s* s, ck_matrix_s* A, const int64_t* seg_n, int S,
+                          const ck_adam_cfg* cfg, const uint64_t* seeds, int R);
+}
+
+extern "C" {
+
+// S independent operators packed block-diagonally (member g at rows/cols
+// [off_g, off_g + n_g), off_g = sum over h < g of round_up(n_h, 256)): one
+// session advances every member and restart column with one kernel pair.
+ck_status ck_session_create_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg,
+                                  const ck_adam_cfg* cfg, const uint64_t* seeds, int32_t ncols,
+                                  ck_session* out) {
+  return guarded([&] {
+    check_cfg(cfg);
+    auto* s = new ck_session_s();
+    try {
+      session_create_batch(s, M(a), seg_n, nseg, cfg, seeds, ncols);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+// estimate_norm (condest.hpp:301-312) for every member of a packed batch: member
+// g's restarts use seed member_seeds[g] (r = 0) or mix_seed(member_seeds[g], r).
+ck_status ck_estimate_norm_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg,
+                                 const ck_adam_cfg* cfg, const uint64_t* member_seeds,
+                                 uint64_t restarts, ck_norm_result* results) {
+  return guarded([&] {
+    check_cfg(cfg);
+    if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
+    ck_matrix_s* m = M(a);
+    std::vector<char> have((size_t)nseg, 0);
+    for (uint64_t r0 = 0; r0 < restarts; r0 += kMaxCols) {
+      const int R = (int)std::min<uint64_t>(kMaxCols, restarts - r0);
+      std::vector<uint64_t> seeds((size_t)nseg * R);
+      for (int g = 0; g < nseg; ++g)
+        for (int c = 0; c < R; ++c) {
+          const uint64_t r = r0 + c;
+          seeds[(size_t)g * R + c] = r == 0 ? member_seeds[g] : ck_mix_seed(member_seeds[g], r);
+        }
+      ck_session_s s;
+      session_create_batch(&s, m, seg_n, nseg, cfg, seeds.data(), R);
+      int32_t fin = 0;
+      session_run(&s, 0, &fin);
+      for (int g = 0; g < nseg; ++g)
+        for (int c = 0; c < R; ++c) {
+          ck_norm_result e{};
+          session_result(&s, g * R + c, &e, nullptr);
+          if (!have[g] || e.value > results[g].value) {
+            results[g] = e;
+            have[g] = 1;
+          }
+        }
+    }
+  });
+}
+
+}  // extern "C"

@@ -45,9 +45,15 @@ struct LoopArgs {
   double* y;    // [nr_pad][R]    A x~
   double* partA;
   double* partT;
-  ColState* st;
-  Header* hdr;
+  ColState* st;  // [S][R]
+  Header* hdr;   // [S]
   Params prm;
+  // block-diagonal batches (config 5): S members, units own tile ranges
+  int S;
+  const int32_t* unit_seg;
+  const int32_t* unit_t0;
+  const int32_t* unit_t1;
+  const int32_t* seg_u0;  // [S + 1]
 };
 
 // Arguments of the inverse-operator step (ck_inverse.cu).
@@ -85,6 +91,9 @@ struct ck_session_s {
   int64_t n = 0;            // operator dimension (columns of A)
   int64_t npad = 0;         // length of the internal vectors
   int64_t thalf = 0;        // tmp holds two halves of thalf doubles
+  int S = 1;                // members (block-diagonal batch); R columns each
+  std::vector<int64_t> seg_n, seg_off, seg_pad;
+  DBuf<int32_t> units;
   const int32_t* perm = nullptr;  // internal position -> original index (nullptr: identity)
   DBuf<double2> PX, MV;
   DBuf<double> y, partA, partT, tmp, obs;
