@@ -92,6 +92,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def make_ensemble(rank: int, world: int, members: int | None, n: int | None):
+    """Config 5: the members of this rank (round-robin sharding by member index)."""
+    from paper_2409_11515_b200 import batch, configs
+    c = configs.CONFIGS[5]
+    count = members or c["count"]
+    idx = list(range(rank, count, world))
+    mem = [configs.ensemble_member(i, 1, n=n or c["grid"], bw=c["param"]) for i in idx]
+    packed = batch.pack_block_diagonal(mem)
+    name = f"{c['name']}x{count}_restarts{c['restarts']}" + (f"@n{n}" if n else "")
+    return packed, idx, name
+
+
 def make_workload(cfg_id: int, grid: int | None):
     from paper_2409_11515_b200 import configs
     c = configs.CONFIGS[cfg_id]
@@ -100,12 +112,13 @@ def make_workload(cfg_id: int, grid: int | None):
     return a, name
 
 
-def bytes_per_iteration(nnz: int, n: int):
+def bytes_per_iteration(nnz: int, n: int, R: int = 1):
     # algorithmic bytes of the two fused sweeps (fp64 values,
     # int32 indices): k_apply reads A (12 B/nnz), x and delta (16 B/row) and writes
     # y (8); k_transpose reads A^T (12 B/nnz), y (8), x m v delta (32) and writes
-    # x m v delta (32). Total 24 nnz + 96 n (SURVEY.md 8d B_iter).
-    return 12 * nnz + 24 * n, 12 * nnz + 72 * n
+    # x m v delta (32). Total 24 nnz + 96 n per column (SURVEY.md 8d B_iter); R
+    # restart columns share the matrix sweeps.
+    return 12 * nnz + 24 * n * R, 12 * nnz + 72 * n * R
 
 
 def cpu_reference(a, steps_hint: int, threads: int, iters: int):
@@ -192,8 +205,23 @@ def run_ours(args):
         dist[1].all_reduce(t, op=dist[1].ReduceOp.MAX)
         return float(t.item())
 
+    def allsum(v: float) -> float:
+        if not dist:
+            return v
+        t = dist[0].tensor([v], dtype=dist[0].float64, device="cuda")
+        dist[1].all_reduce(t, op=dist[1].ReduceOp.SUM)
+        return float(t.item())
+
     t_gen = time.perf_counter()
-    a, name = make_workload(args.config, args.grid)
+    ensemble = args.config == 5
+    if ensemble:
+        from paper_2409_11515_b200 import batch  # noqa: PLC0415
+        packed, member_idx, name = make_ensemble(rank, world, args.members, args.grid)
+        a = packed[0]
+        R = configs.CONFIGS[5]["restarts"]
+    else:
+        a, name = make_workload(args.config, args.grid)
+        R = 1
     t_gen = time.perf_counter() - t_gen
     seed = 1 if rank == 0 else ck.mix_seed(1, rank)
     total_iters = args.warmup + args.steps + 8
@@ -203,7 +231,12 @@ def run_ours(args):
     dev = a.device()
     t_up = time.perf_counter() - t_up
     info = dev.info()
-    sess = ck.Session(ck.ExplicitOracle(a), cfg, [seed])
+    if ensemble:
+        ms = batch.member_seeds(configs.CONFIGS[5]["count"])
+        seeds = [ms[i] if r == 0 else ck.mix_seed(ms[i], r) for i in member_idx for r in range(R)]
+        sess = batch.BatchSession(packed, cfg, seeds)
+    else:
+        sess = ck.Session(ck.ExplicitOracle(a), cfg, [seed])
     sess.run(args.warmup)
     barrier()
     sampler = ClockSampler(local) if rank == 0 else None
@@ -211,14 +244,16 @@ def run_ours(args):
     barrier()
     clocks = sampler.stop() if sampler else None
     ms_max = allmax(ms_total)
-    value = world * args.steps / (ms_max / 1000.0)
+    runs_per_step = (len(member_idx) * R) if ensemble else 1
+    total_runs = allsum(runs_per_step) if ensemble else world
+    value = total_runs * args.steps / (ms_max / 1000.0)
     sess.close()
 
     n, nnz = a.nrows, a.nnz
-    b_apply, b_tr = bytes_per_iteration(nnz, n)
+    b_apply, b_tr = bytes_per_iteration(nnz, n, R)
     peak, peak_kind = measured_peaks()
-    k_apply = {"name": "k_apply<1>", "ms_avg": ms_apply / args.steps, "bytes": b_apply}
-    k_tr = {"name": "k_transpose<1>", "ms_avg": ms_tr / args.steps, "bytes": b_tr}
+    k_apply = {"name": f"k_apply<{R}>", "ms_avg": ms_apply / args.steps, "bytes": b_apply}
+    k_tr = {"name": f"k_transpose<{R}>", "ms_avg": ms_tr / args.steps, "bytes": b_tr}
     for k in (k_apply, k_tr):
         k["gbs"] = k["bytes"] / (k["ms_avg"] / 1000.0) / 1e9
         k["frac"] = k["gbs"] / peak
@@ -242,7 +277,7 @@ def run_ours(args):
 
     # ---- e2e: the public API call a user makes, from host buffers ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not ensemble:
         a2 = ck.SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices, a.values,
                              validate=False)
         regs = []
@@ -270,7 +305,7 @@ def run_ours(args):
                "seconds": dt, "iterations": est.iterations, "sigma_max": est.value}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not ensemble:
         threads = args.cpu_threads or host_threads_budget(a)
         r = cpu_reference(a, args.steps, threads, args.cpu_iters)
         cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
@@ -286,7 +321,9 @@ def run_ours(args):
             "data": "synthetic (seeded generator, DESIGN.md section 3)",
             "config": {"workload": name, "n": n, "nnz": nnz, "path": "sigma_max",
                        "adam": "alpha=1e-2,beta1=.9,beta2=.999,eps=1e-8",
-                       "parallelism": f"replicas{world} (independent restart streams)",
+                       "runs_per_step": runs_per_step,
+                       "parallelism": (f"members sharded over {world} ranks" if ensemble else
+                                       f"replicas{world} (independent restart streams)"),
                        "l2": f"inputs larger than L2 (matrix {(24 * nnz) / 1e9:.1f} GB "
                              f"per iteration vs 126 MB L2); no flush needed",
                        "sell_padding": (info["sell_entries_a"] - nnz) / max(nnz, 1)},
@@ -319,6 +356,7 @@ def main():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
     p.add_argument("--cpu-iters", type=int, default=3)
+    p.add_argument("--members", type=int, default=None, help="config 5: ensemble size")
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3

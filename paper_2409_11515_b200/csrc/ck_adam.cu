@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
     pro[r] = ph == PH_PRO;
     // prologue: delta is zero, so x~ = x exactly (x - (0 - 0 x) = x)
     rad[r] = pro[r] ? 0.0 : sts[r].rad;
-    xc[r] = a.PX + ((int64_t)sts[r].cur * R + r) * a.nc_pad;
+    xc[r] = a.PX + (int64_t)sts[r].cur * a.nc_pad * R + r;  // row i at xc[r][i * R]
   }
   DD dd[R];
   ES es[R], dn[R];
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (!act[r]) continue;
-        const double2 p = xc[r][i];
+        const double2 p = xc[r][i * R];
         if (OBS && !pro[r]) {
           const double dp = __dsub_rn(p.y, __dmul_rn(rad[r], p.x));
           xd[r] = __fma_rn(p.x, dp, xd[r]);
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
           if (!act[r]) continue;
           double2 g[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) g[u] = __ldg(xc[r] + c[u]);
+          for (int u = 0; u < U; ++u) g[u] = __ldg(xc[r] + (int64_t)c[u] * R);
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xtilde(g[u], rad[r])));
@@ -277,9 +277,9 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     iy2[r] = s.inv_y2;
     mc[r] = s.mc;
     vc[r] = s.vc;
-    xc[r] = a.PX + ((int64_t)s.cur * R + r) * a.nc_pad;
+    xc[r] = a.PX + (int64_t)s.cur * a.nc_pad * R + r;
     // prologue (mat = 0): x stays where it is and only delta is rewritten
-    xn_out[r] = a.PX + ((int64_t)(mat[r] ? s.nxt : s.cur) * R + r) * a.nc_pad;
+    xn_out[r] = a.PX + (int64_t)(mat[r] ? s.nxt : s.cur) * a.nc_pad * R + r;
   }
   const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
   double dot[R];
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
       for (int r = 0; r < R; ++r) {
         if (!act[r]) continue;
         const int64_t e = j * R + r;
-        const double2 px = xc[r][j];
+        const double2 px = xc[r][j * R];
         const double xn = mat[r] ? __ddiv_rn(xtilde(px, rad[r]), ndiv[r]) : px.x;  // :240-247
         const double z = __ddiv_rn(acc[r], ndiv[r]);                               // A^T A x_{t+1}
         const double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(z, iy2[r]));  // :105
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
         const double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
                                    __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));  // :228
         a.MV[e] = make_double2(mm, vv);
-        xn_out[r][j] = make_double2(xn, d);
+        xn_out[r][j * R] = make_double2(xn, d);
         dot[r] = __fma_rn(xn, d, dot[r]);
       }
     }
@@ -376,20 +376,20 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
 }
 
 // x_{t+1} = x~ / N from (x, delta) pairs, into a plain vector (epilogue / observer).
-__global__ void k_materialise(int64_t nc, const double2* __restrict__ px, double rad, double ndiv,
-                              double* out) {
+__global__ void k_materialise(int64_t nc, int R, const double2* __restrict__ px, double rad,
+                              double ndiv, double* out) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j < nc) out[j] = __ddiv_rn(xtilde(px[j], rad), ndiv);
+  if (j < nc) out[j] = __ddiv_rn(xtilde(px[j * R], rad), ndiv);
 }
 
-__global__ void k_extract_x(int64_t n, const double2* __restrict__ px, double* out) {
+__global__ void k_extract_x(int64_t n, int R, const double2* __restrict__ px, double* out) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j < n) out[j] = px[j].x;
+  if (j < n) out[j] = px[j * R].x;
 }
 
-__global__ void k_store_x(int64_t n, const double* __restrict__ x, double2* px) {
+__global__ void k_store_x(int64_t n, int R, const double* __restrict__ x, double2* px) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j < n) px[j] = make_double2(x[j], 0.0);
+  if (j < n) px[j * R] = make_double2(x[j], 0.0);
 }
 
 __global__ void k_zero_moments(int64_t n, int R, int col, double2* mv) {
@@ -494,8 +494,9 @@ static bool any_wait(const ck_session_s* s) {
   return false;
 }
 
+// (x, delta) pairs of buffer b, column c: element i at col_buf(...)[i * R]
 static double2* col_buf(ck_session_s* s, int b, int c) {
-  return s->PX.p + ((int64_t)b * s->R + c) * s->npad;
+  return s->PX.p + (int64_t)b * s->npad * s->R + c;
 }
 
 // host vector of member g (original order, seg_n[g] doubles) -> internal plain
@@ -535,7 +536,7 @@ static void load_start(ck_session_s* s, int g, int c, int b, const double* x) {
   double* plain = s->tmp.p + s->thalf;
   CK_CUDA(cudaMemsetAsync(plain + off, 0, sizeof(double) * pad, st));
   to_internal(s, g, x, plain, st);
-  k_store_x<<<grid256(pad), 256, 0, st>>>(pad, plain + off, col_buf(s, b, c) + off);
+  k_store_x<<<grid256(pad), 256, 0, st>>>(pad, s->R, plain + off, col_buf(s, b, c) + off * s->R);
   k_zero_moments<<<grid256(pad), 256, 0, st>>>(pad, s->R, c, s->MV.p + off * s->R);
   CK_CUDA(cudaGetLastError());
 }
@@ -681,15 +682,15 @@ static void session_create_explicit(ck_session_s* s, ck_matrix_s* A, const ck_ad
     a.units_T = (int)std::min<int64_t>(a.tiles_T, 148 * occ_transpose(R));
     a.unit_seg = a.unit_t0 = a.unit_t1 = a.seg_u0 = nullptr;
   } else {
-    // members are tile-aligned; each unit takes up to 8 consecutive tiles of one member
+    // members are tile-aligned; each unit takes up to 32 consecutive tiles of one member
     std::vector<int32_t> useg, ut0, ut1, su0(S + 1, 0);
     for (int g = 0; g < S; ++g) {
       const int t0 = (int)(s->seg_off[g] / kTile), nt = (int)(s->seg_pad[g] / kTile);
       su0[g] = (int)useg.size();
-      for (int t = 0; t < nt; t += 8) {
+      for (int t = 0; t < nt; t += 32) {
         useg.push_back(g);
         ut0.push_back(t0 + t);
-        ut1.push_back(t0 + std::min(nt, t + 8));
+        ut1.push_back(t0 + std::min(nt, t + 32));
       }
     }
     su0[S] = (int)useg.size();
@@ -882,10 +883,12 @@ void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness
   double* xbest = s->tmp.p + s->thalf;  // plain copy of x_min (internal order)
   CK_CUDA(cudaMemsetAsync(xbest, 0, sizeof(double) * ncp, st));
   if (cs.pend) {  // x_{t+1} became the best but was never materialised
-    k_materialise<<<grid256(pad), 256, 0, st>>>(s->S == 1 ? s->n : pad, col_buf(s, cs.cur, c) + off,
-                                               cs.rad, cs.ndiv, xbest + off);
+    k_materialise<<<grid256(pad), 256, 0, st>>>(s->S == 1 ? s->n : pad, s->R,
+                                               col_buf(s, cs.cur, c) + off * s->R, cs.rad, cs.ndiv,
+                                               xbest + off);
   } else {
-    k_extract_x<<<grid256(pad), 256, 0, st>>>(pad, col_buf(s, cs.best, c) + off, xbest + off);
+    k_extract_x<<<grid256(pad), 256, 0, st>>>(pad, s->R, col_buf(s, cs.best, c) + off * s->R,
+                                             xbest + off);
   }
   CK_CUDA(cudaGetLastError());
   res->iterations = cs.t;
@@ -905,7 +908,7 @@ void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness
 
 // x of buffer b / column c as a plain internal vector in `out` (npad doubles).
 static void extract_x(ck_session_s* s, int b, int c, double* out, cudaStream_t st) {
-  k_extract_x<<<grid256(s->npad), 256, 0, st>>>(s->npad, col_buf(s, b, c), out);
+  k_extract_x<<<grid256(s->npad), 256, 0, st>>>(s->npad, s->R, col_buf(s, b, c), out);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -940,7 +943,7 @@ void session_step_observed(ck_session_s* s, ck_step_info* info, double* x, doubl
     if (reported) {
       // x_{t+1} from the pre-step pair buffer, before the transpose half moves on
       CK_CUDA(cudaMemsetAsync(xnext, 0, sizeof(double) * ncp, st));
-      k_materialise<<<grid256(ncp), 256, 0, st>>>(s->n, col_buf(s, cs.cur, 0), cs.rad, cs.ndiv,
+      k_materialise<<<grid256(ncp), 256, 0, st>>>(s->n, s->R, col_buf(s, cs.cur, 0), cs.rad, cs.ndiv,
                                                   xnext);
       if (!cs.pend) extract_x(s, cs.best, 0, xm, st);
     }

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
     act[r] = ph == PH_PRO || ph == PH_APPLY;
     pro[r] = ph == PH_PRO;
     rad[r] = pro[r] ? 0.0 : a.st[r].rad;
-    xc[r] = a.PX + ((int64_t)a.st[r].cur * R + r) * n;
+    xc[r] = a.PX + (int64_t)a.st[r].cur * n * R + r;  // element i at xc[r][i * R]
     any |= act[r];
   }
   if (any && a.half != 2) {
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
     for (int64_t i = tid; i < n; i += nt) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const double2 p = xc[r][i];
+        const double2 p = xc[r][i * R];
         const double xt = xtilde_inv(p, rad[r]);
         ys[r][i] = xt;
         if (act[r]) {
@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
     iy2[r] = s.inv_y2;
     mc[r] = s.mc;
     vc[r] = s.vc;
-    xc[r] = a.PX + ((int64_t)s.cur * R + r) * n;
-    xn_out[r] = a.PX + ((int64_t)(mat[r] ? s.nxt : s.cur) * R + r) * n;
+    xc[r] = a.PX + (int64_t)s.cur * n * R + r;
+    xn_out[r] = a.PX + (int64_t)(mat[r] ? s.nxt : s.cur) * n * R + r;
     anyg |= grad[r];
   }
   if (anyg && a.half != 1) {
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
       for (int r = 0; r < R; ++r) {
         if (!grad[r]) continue;
         const int64_t e = j * R + r;
-        const double2 px = xc[r][j];
+        const double2 px = xc[r][j * R];
         const double xn = mat[r] ? __ddiv_rn(xtilde_inv(px, rad[r]), ndiv[r]) : px.x;
         const double zz = __ddiv_rn(ys[r][j], ndiv[r]);
         const double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(zz, iy2[r]));
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
         const double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
                                    __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));
         a.MV[e] = make_double2(mm, vv);
-        xn_out[r][j] = make_double2(xn, d);
+        xn_out[r][j * R] = make_double2(xn, d);
         dot[r] = __fma_rn(xn, d, dot[r]);
       }
     }

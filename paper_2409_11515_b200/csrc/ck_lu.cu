@@ -227,6 +227,36 @@ __global__ void __launch_bounds__(256) k_convert_l_blocks(BandView b) {
       }
     }
   }
+  // composite interchange of the block: apply the swaps to an index list of the
+  // touched window positions, then emit (dst, src) for every moved position
+  if (threadIdx.x == 0) {
+    int32_t pos[2 * kLUBlock], src[2 * kLUBlock];
+    int m = 0;
+    auto slot = [&](int32_t q) {
+      for (int k = 0; k < m; ++k)
+        if (pos[k] == q) return k;
+      pos[m] = q;
+      src[m] = q;
+      return m++;
+    };
+    for (int c = 0; c < jb; ++c) {
+      const int32_t p = (int32_t)(b.ipiv[J + c] - J);
+      if (p == c) continue;
+      const int ka = slot(c), kb = slot(p);
+      const int32_t t = src[ka];
+      src[ka] = src[kb];
+      src[kb] = t;
+    }
+    int32_t* out = b.perm + blk * (1 + 4 * kLUBlock);
+    int cnt = 0;
+    for (int k = 0; k < m; ++k)
+      if (src[k] != pos[k]) {
+        out[1 + 2 * cnt] = pos[k];
+        out[2 + 2 * cnt] = src[k];
+        ++cnt;
+      }
+    out[0] = cnt;
+  }
 }
 
 template <int R>
@@ -346,6 +376,7 @@ void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_co
   f->pivot_min = n > 0 ? s.pivot_min : INFINITY;
   const int64_t nblk = ceil_div(n, kLUBlock);
   f->lb.alloc(std::max<int64_t>(1, nblk * kLUBlock * (kLUBlock + f->kl)));
+  f->bperm.alloc(std::max<int64_t>(1, nblk * (1 + 4 * kLUBlock)));
   f->work.alloc(2 * n + 3 * kNormParts + 16);
   b = f->view();
   if (n > 0) k_convert_l_blocks<<<(unsigned)nblk, 256, 0, st>>>(b);

@@ -24,6 +24,9 @@ struct BandView {
   // starts at row 32*blk (see ck_lu.cu, convert_l_blocks).
   double* lb;
   int64_t lb_ld;  // rows per column of lb (= 32 + kl)
+  // per block: [count, (dst, src) x count] window positions of the block's
+  // composite interchange (<= 64 moved positions), 1 + 128 int32 per block
+  int32_t* perm;
 };
 
 struct LUStatus {
@@ -46,7 +49,7 @@ struct ck_lu_s {
   int64_t n = 0, kl = 0, ku = 0;
   double pivot_min = 0.0;
   ck::DBuf<double> ab, lb;
-  ck::DBuf<int32_t> ipiv;
+  ck::DBuf<int32_t> ipiv, bperm;
   ck::DBuf<ck::LUStatus> status;
   ck::DBuf<double> work;  // solve scratch
   ck_lu_s() = default;
@@ -60,6 +63,6 @@ struct ck_lu_s {
   }
   ck::BandView view() {
     return ck::BandView{n, kl, ku, kl + ku, 2 * kl + ku + 1, ab.p, ipiv.p, lb.p,
-                        ck::kLUBlock + kl};
+                        ck::kLUBlock + kl, bperm.p};
   }
 };

@@ -40,7 +40,7 @@ struct LoopArgs {
   int64_t nr, nc, nr_pad, nc_pad;
   int tiles_A, tpu_A, units_A;
   int tiles_T, tpu_T, units_T;
-  double2* PX;  // [3][R][nc_pad] (x, delta) pairs; three rotating iterate buffers
+  double2* PX;  // [3][nc_pad][R] (x, delta) pairs; three rotating iterate buffers
   double2* MV;  // [nc_pad][R]    (m, v) Adam moments
   double* y;    // [nr_pad][R]    A x~
   double* partA;
@@ -61,7 +61,7 @@ struct InvArgs {
   BandView b;
   int64_t n;
   int ring_size;
-  double2* PX;  // [3][R][n]
+  double2* PX;  // [3][n][R]
   double2* MV;  // [n][R]
   double* y;    // [R][n] work vector (solve in place)
   ColState* st;

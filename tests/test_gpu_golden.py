@@ -144,6 +144,8 @@ def test_config4_full_size():
     _cmp_est(ck.norm2(a, configs.baseline_adam(1)), g["c4_projected_adam"])
 
 
+@pytest.mark.skipif(not os.environ.get("CK_SLOW"),
+                    reason="several minutes: sigma_min at n=196k runs one CTA per sweep (set CK_SLOW=1)")
 def test_config2_cond2_full_size():
     g = gold("c2_cond2")["c2_cond2_r1"]
     r = ck.cond2(configs.config(2), configs.baseline_adam(1), 1, 1e-14)
