@@ -15,7 +15,7 @@ import numpy as np
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcondkit_b200.so")
+LIB_PATH = os.environ.get("CK_LIB") or os.path.join(_HERE, "libcondkit_b200.so")
 
 dp = C.POINTER(C.c_double)
 i64p = C.POINTER(C.c_int64)

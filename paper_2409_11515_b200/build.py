@@ -33,21 +33,25 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
+    """prof=True builds the phase-timing variant (-DCK_SWEEP_PROF) next to
+    the library as libcondkit_b200_prof.so (load it with CK_LIB=...)."""
+    out = LIB.replace(".so", "_prof.so") if prof else LIB
+    if not prof and not force and not needs_build():
         return LIB
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
            "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"),
-           "-o", LIB + ".tmp"] + sources() + ["-lpthread"]
+           "-o", out + ".tmp"] + sources() + ["-lpthread"]
+    if prof:
+        cmd.insert(1, "-DCK_SWEEP_PROF")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, prof="--prof" in sys.argv))

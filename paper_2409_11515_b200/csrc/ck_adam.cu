@@ -412,6 +412,7 @@ static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
 void launch_inv_step(const InvArgs& a, int R, cudaStream_t st);
 void prepare_inv_step(const BandView& b, int R);
 int lu_ring_size(const BandView& b);
+int64_t lu_stage_cap(const BandView& b, int R);
 void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st);
 
 static void launch_inv_half(ck_session_s* s, int half, cudaStream_t st) {
@@ -767,6 +768,7 @@ void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg
   a.b = b;
   a.n = s->n;
   a.ring_size = lu_ring_size(b);
+  a.b.stage_cap = lu_stage_cap(b, R);
   a.PX = s->PX.p;
   a.MV = s->MV.p;
   a.y = s->y.p;

@@ -195,10 +195,11 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
 
 size_t inv_step_smem(const BandView& b, int R);
 int lu_ring_size(const BandView& b);
+int64_t lu_stage_cap(const BandView& b, int R);
 
 void prepare_inv_step(const BandView& b, int R) {
   const size_t smem = inv_step_smem(b, R);
-  if (smem > 227 * 1024) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+  if (lu_stage_cap(b, R) < 0) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
   switch (R) {
     case 1: CK_CUDA(cudaFuncSetAttribute(k_inv_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
     case 2: CK_CUDA(cudaFuncSetAttribute(k_inv_step<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;

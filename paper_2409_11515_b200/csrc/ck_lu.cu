@@ -195,6 +195,12 @@ __global__ void __launch_bounds__(512) k_gbtrf_update(BandView b, int64_t j0, in
   }
 }
 
+// RN(1 / U(j, j)) per pivot for the solves' head triangles (ck_lu_sweeps.cuh).
+__global__ void k_pivot_reciprocals(BandView b) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < b.n) b.rdiag[j] = __drcp_rn(b.ab[b.kv + j * b.ldab]);
+}
+
 // L blocks in local pivot order: for block blk (columns J..J+jb-1), column c
 // holds the step-(J+c) multipliers with the later interchanges of the same
 // block applied, at window rows (relative to J) 0 .. 32+kl-1.
@@ -275,8 +281,19 @@ int lu_ring_size(const BandView& b) {
   return s;
 }
 
+// Dynamic shared memory of a solve CTA: rings + dot scratch, then as much of
+// a full TMA stage (32 runs of max(kl, kv) rows) as fits next to the static
+// shared memory (Head, mbarrier, step scratch).
+constexpr size_t kSolveDynMax = 227 * 1024 - 12 * 1024;
+
 size_t lu_solve_smem(const BandView& b, int R) {
-  return sizeof(double) * ((size_t)R * lu_ring_size(b) + (size_t)R * kLUBlock);
+  const int64_t base = stage_offset(R, lu_ring_size(b));
+  const int64_t full = (int64_t)kLUBlock * ((std::max(b.kl, b.kv) + 3) & ~(int64_t)1);
+  return std::min(kSolveDynMax, sizeof(double) * (size_t)(base + full));
+}
+
+int64_t lu_stage_cap(const BandView& b, int R) {
+  return (int64_t)(lu_solve_smem(b, R) / sizeof(double)) - stage_offset(R, lu_ring_size(b));
 }
 
 size_t inv_step_smem(const BandView& b, int R) { return lu_solve_smem(b, R); }
@@ -285,7 +302,8 @@ void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaSt
   BandView b = f->view();
   const int ring = lu_ring_size(b);
   const size_t smem = lu_solve_smem(b, R);
-  if (smem > 227 * 1024) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+  b.stage_cap = lu_stage_cap(b, R);
+  if (b.stage_cap < 0) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
   double* xs[4] = {x[0], R > 1 ? x[1] : nullptr, R > 2 ? x[2] : nullptr, R > 3 ? x[3] : nullptr};
   switch (R) {
 #define CK_SOLVE_CASE(RR)                                                                       \
@@ -375,13 +393,29 @@ void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_co
   }
   f->pivot_min = n > 0 ? s.pivot_min : INFINITY;
   const int64_t nblk = ceil_div(n, kLUBlock);
-  f->lb.alloc(std::max<int64_t>(1, nblk * kLUBlock * (kLUBlock + f->kl)));
+  f->lb.alloc(nblk * kLUBlock * (kLUBlock + f->kl) + 2);  // +2: stage copies round up to 16 B
   f->bperm.alloc(std::max<int64_t>(1, nblk * (1 + 4 * kLUBlock)));
   f->work.alloc(2 * n + 3 * kNormParts + 16);
+  f->rdiag.alloc(std::max<int64_t>(1, n));
   b = f->view();
   if (n > 0) k_convert_l_blocks<<<(unsigned)nblk, 256, 0, st>>>(b);
+  if (n > 0) k_pivot_reciprocals<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b);
   CK_CUDA(cudaGetLastError());
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace ck
+
+#ifdef CK_SWEEP_PROF
+// Profiling build only: read (and optionally reset) the phase cycles of the
+// standalone solves (k_lu_solve, this translation unit's copy).
+extern "C" int ck_debug_sweep_prof(unsigned long long* out32, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out32, ck::g_sweep_prof, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(ck::g_sweep_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -27,6 +27,10 @@ struct BandView {
   // per block: [count, (dst, src) x count] window positions of the block's
   // composite interchange (<= 64 moved positions), 1 + 128 int32 per block
   int32_t* perm;
+  double* rdiag;  // RN(1 / U(j, j)) per pivot
+  // doubles of dynamic shared memory the solve CTA has for its TMA stage
+  // (set by the launcher, see lu_solve_smem)
+  int64_t stage_cap;
 };
 
 struct LUStatus {
@@ -48,7 +52,7 @@ struct ck_lu_s {
   bool own_stream = false;
   int64_t n = 0, kl = 0, ku = 0;
   double pivot_min = 0.0;
-  ck::DBuf<double> ab, lb;
+  ck::DBuf<double> ab, lb, rdiag;
   ck::DBuf<int32_t> ipiv, bperm;
   ck::DBuf<ck::LUStatus> status;
   ck::DBuf<double> work;  // solve scratch
@@ -63,6 +67,6 @@ struct ck_lu_s {
   }
   ck::BandView view() {
     return ck::BandView{n, kl, ku, kl + ku, 2 * kl + ku + 1, ab.p, ipiv.p, lb.p,
-                        ck::kLUBlock + kl, bperm.p};
+                        ck::kLUBlock + kl, bperm.p, rdiag.p, 0};
   }
 };

@@ -1,17 +1,50 @@
 // Triangular sweeps over the device band LU (ck_lu.cu) -- shared by the
 // standalone solves (ck_lu.cu) and the inverse Projected-Adam step
 // (ck_inverse.cu). See ck_lu.cu for the layout and the algorithm.
+//
+// One CTA of kSweepThreads threads walks the blocks of 32 steps in order,
+// with two CTA barriers per block:
+//   * warp 0 solves the block's 32x32 head (and applies the block's composite
+//     interchange) -- the sequential critical path, fully unrolled;
+//   * every warp folds the block into the rows it reaches (L, U: row tails),
+//     or forms the head's dots over the final rows (U^T, L^T).
+// The tail/dot coefficients of a block (32 columns x up to max(kl, kv)
+// rows) are streamed from HBM into a shared-memory stage by TMA bulk copies
+// (cp.async.bulk issued by one thread, completion on an mbarrier) while warp
+// 0 is busy with a head, and the idle warps load the next head triangle,
+// interchange pairs and incoming rows into registers at the same time. Rows
+// beyond the stage capacity (very wide bands) are read directly.
 #pragma once
 #include "ck_device.cuh"
 #include "ck_lu.h"
 
 namespace ck {
 
+// Phase timing of the sweeps (profiling build only, -DCK_SWEEP_PROF):
+// thread 0 accumulates clock64 deltas per (sweep, phase) slot.
+#ifdef CK_SWEEP_PROF
+static __device__ unsigned long long g_sweep_prof[32];  // per translation unit
+#define CK_PROF_INIT long long ck_prof_t = clock64()
+#define CK_PROF(slot)                                                      \
+  do {                                                                     \
+    if (threadIdx.x == 0) {                                                \
+      const long long t = clock64();                                       \
+      atomicAdd(&g_sweep_prof[slot], (unsigned long long)(t - ck_prof_t)); \
+      ck_prof_t = t;                                                       \
+    }                                                                      \
+  } while (0)
+#else
+#define CK_PROF_INIT
+#define CK_PROF(slot)
+#endif
+
+constexpr int kSweepThreads = 1024;  // launch width of every sweep CTA
+constexpr int kIssuer = 32;          // thread that drives the TMA stage (warp 1)
+
 __device__ __forceinline__ double& AB(const BandView& b, int64_t i, int64_t j) {
   return b.ab[(b.kv + i - j) + j * b.ldab];
 }
 
-// ----------------------------------------------------------- solves
 // Ring-buffer view of the active rows of one right-hand side.
 struct Ring {
   double* w;
@@ -19,74 +52,291 @@ struct Ring {
   __device__ __forceinline__ double& operator[](int64_t row) const { return w[row & mask]; }
 };
 
-// 32x32 staging buffer for a block's head triangle (shared by the sweeps).
+// 32x32 staging buffer for a block's head triangle (+ the U diagonal's
+// reciprocals for the U sweeps).
 struct Head {
   double v[kLUBlock][kLUBlock + 1];
+  double rd[kLUBlock];
 };
 
-// Composite interchange of block blk, precomputed by k_convert_l_blocks:
-// window position dst (relative to the block start) receives the value of
-// position src; at most 64 moved positions per block.
-__device__ __forceinline__ void block_perm(const BandView& b, int64_t blk, int& np,
-                                           const int32_t*& pairs) {
-  const int32_t* p = b.perm + blk * (1 + 2 * 2 * kLUBlock);
-  np = p[0];
-  pairs = p + 1;
+// ------------------------------------------------------------ TMA stage
+// Column c of a block's coefficients is a contiguous run of doubles in HBM
+// starting at element first(c) (the two run kinds are below). The stage
+// holds rows [0, srows) of each run at st[c * sld + (first(c) & 1) + m]: the
+// bulk copy starts at the 16-byte boundary below the run.
+struct Stage {
+  double* st = nullptr;
+  uint64_t* bar = nullptr;
+  int64_t srows = 0, sld = 2;
+  uint32_t parity = 0;
+
+  __device__ void layout(int64_t cap, int64_t len) {
+    const int64_t rows_fit = ((cap / kLUBlock) & ~(int64_t)1) - 2;
+    srows = lmax(0, lmin(len, rows_fit));
+    sld = (srows + 3) & ~(int64_t)1;
+  }
+  __device__ __forceinline__ uint32_t copy_bytes(int64_t first) const {
+    return srows == 0 ? 0u : (uint32_t)(8 * (((first & 1) + srows + 1) & ~(int64_t)1));
+  }
+  // One thread: arm the barrier and bulk-copy columns c < ncols of runs first(c).
+  template <class First>
+  __device__ void issue(const double* src, int ncols, First first) const {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t bytes = 0;
+    for (int c = 0; c < ncols; ++c) bytes += copy_bytes(first(c));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    for (int c = 0; c < ncols; ++c) {
+      const int64_t f = first(c);
+      const uint32_t n8 = copy_bytes(f);
+      if (n8 == 0) continue;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(st + (int64_t)c * sld);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+          "l"(src + (f & ~(int64_t)1)), "r"(n8), "r"(b)
+          : "memory");
+    }
+  }
+  // Every thread: wait for the stage issued last.
+  __device__ void wait() {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done)
+          : "r"(b), "r"(parity)
+          : "memory");
+    }
+    parity ^= 1u;
+  }
+  __device__ __forceinline__ double at(int c, int off, int64_t m) const { return st[c * sld + off + m]; }
+};
+
+// L run of block blk, column c: lb rows 32 .. 32+kl-1 (the tail multipliers).
+__device__ __forceinline__ int64_t l_run_first(const BandView& b, int64_t blk, int c) {
+  return (blk * kLUBlock + c) * b.lb_ld + kLUBlock;
+}
+// U run of block J, column c: band entries of column J+c for rows
+// J-kv+m, m in [0, kv); rows m < c lie outside the band (masked by users).
+__device__ __forceinline__ int64_t u_run_first(const BandView& b, int64_t J, int c) {
+  return (J + c) * b.ldab - c;
 }
 
-// x := (L-part)^{-1} x, i.e. LAPACK gbtrs 'N' first half: for every step j
-// interchange rows j, ipiv[j], then eliminate below j. Rows are staged through
-// the ring. Per block, warp 0 applies the block's composite interchange and
-// solves the 32x32 unit-lower head; then all warps update the tail while the
-// next block's head multipliers and incoming rows are already being loaded --
-// two CTA barriers per block.
+// ---------------------------------------------------------- interchanges
+// Composite interchange of block blk (precomputed by k_convert_l_blocks):
+// window position dst (relative to the block start) receives the value of
+// position src; at most 64 moved positions, two per lane of warp 0.
+struct Perm {
+  int np;
+  int2 p[2];  // (dst, src) for t = lane, lane + 32
+};
+
+__device__ __forceinline__ Perm load_perm(const BandView& b, int64_t blk, int lane) {
+  const int32_t* p = b.perm + blk * (1 + 2 * 2 * kLUBlock);
+  Perm q;
+  q.np = p[0];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = lane + 32 * h;
+    q.p[h] = t < q.np ? make_int2(p[1 + 2 * t], p[2 + 2 * t]) : make_int2(0, 0);
+  }
+  return q;
+}
+
+// Warp-wide gather: ring[J + dst] := ring[J + src] (inverse: roles swapped).
+template <int R, bool kInverse>
+__device__ __forceinline__ void apply_perm(const Perm& q, const Ring* ring, int64_t J, int lane) {
+  double pv[2][R];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (lane + 32 * h < q.np)
+#pragma unroll
+      for (int r = 0; r < R; ++r) pv[h][r] = ring[r][J + (kInverse ? q.p[h].x : q.p[h].y)];
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (lane + 32 * h < q.np)
+#pragma unroll
+      for (int r = 0; r < R; ++r) ring[r][J + (kInverse ? q.p[h].y : q.p[h].x)] = pv[h][r];
+  __syncwarp();
+}
+
+// a / d, correctly rounded, from rd = RN(1/d) (precomputed per pivot at
+// factorisation): multiply plus one FMA correction (Markstein) -- a full
+// division is ~380 cycles of dependent latency on the head solve's chain.
+__device__ __forceinline__ double div_rcp(double a, double d, double rd) {
+  const double q = __dmul_rn(a, rd);
+  return __fma_rn(__fma_rn(-q, d, a), rd, q);
+}
+
+// Element q of the head triangles: U's 32x32 diagonal block of block J as
+// H.v[c][r] = U(J+r, J+c) for r <= c (zero elsewhere); L's from lb.
+// Columns c >= jb of a partial last block are padded with the identity, so
+// the unrolled head solves need no bounds.
+__device__ __forceinline__ double u_head_elem(const BandView& b, int64_t J, int jb, int q) {
+  const int c = q >> 5, r = q & 31;
+  if (c >= jb) return r == c ? 1.0 : 0.0;
+  return (r <= c && c - r <= b.kv) ? AB(b, J + r, J + c) : 0.0;
+}
+__device__ __forceinline__ double u_head_rd(const BandView& b, int64_t J, int jb, int c) {
+  return c < jb ? b.rdiag[J + c] : 1.0;
+}
+__device__ __forceinline__ double l_head_elem(const BandView& b, int64_t blk, int q) {
+  return b.lb[(blk * kLUBlock + (q >> 5)) * b.lb_ld + (q & 31)];
+}
+
+// Next-block head prefetch by warps 1..31: elements q = tid-32 and, for
+// warp 1, q + 992.
+struct HeadPrefetch {
+  double v[3];
+  template <class F>
+  __device__ __forceinline__ void load(F elem) {
+    const int q = (int)threadIdx.x - 32;
+    if (q >= 0) {
+      v[0] = elem(q);
+      if (q < 32) v[1] = elem(q + 992);
+    }
+  }
+  template <class F, class G>
+  __device__ __forceinline__ void load(F elem, G rd) {
+    load(elem);
+    const int q = (int)threadIdx.x - 32;
+    if (q >= 0 && q < 32) v[2] = rd(q);
+  }
+  __device__ __forceinline__ void commit(Head& H, bool with_rd = false) const {
+    const int q = (int)threadIdx.x - 32;
+    if (q >= 0) {
+      H.v[q >> 5][q & 31] = v[0];
+      if (q < 32) {
+        H.v[(q + 992) >> 5][(q + 992) & 31] = v[1];
+        if (with_rd) H.rd[q] = v[2];
+      }
+    }
+  }
+};
+
+// Incoming rows [r0, r1) (at most 32) by warp 1.
 template <int R>
-__device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring, Head& H) {
+struct RowPrefetch {
+  double v[R];
+  __device__ __forceinline__ void load(double* const* x, int64_t r0, int64_t r1) {
+    const int t = (int)threadIdx.x - 32;
+    if (t >= 0 && t < 32 && r0 + t < r1)
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = x[r][r0 + t];
+  }
+  __device__ __forceinline__ void commit(const Ring* ring, int64_t r0, int64_t r1) const {
+    const int t = (int)threadIdx.x - 32;
+    if (t >= 0 && t < 32 && r0 + t < r1)
+#pragma unroll
+      for (int r = 0; r < R; ++r) ring[r][r0 + t] = v[r];
+  }
+};
+
+// --------------------------------------------------------------- tails
+// Lanes per row for a tail of `rows` rows: up to 4 (8 columns per lane)
+// while the rows still fit one pass of the CTA. Fewer lanes per row keeps
+// the issue count low -- warps without rows skip the tail altogether.
+__device__ __forceinline__ int tail_log_lanes(int64_t rows) {
+  int lg = 0;
+  while (lg < 2 && ((int64_t)kSweepThreads >> (lg + 1)) >= rows) ++lg;
+  return lg;
+}
+
+// ring[base + m] -= sum_{c < jb} coef(m, c) * ring[J + c] for m in [m0, m1):
+// 2^lg lanes share a row (rows fastest within a warp), each summing every
+// 2^lg-th column; the partial sums meet by shuffles.
+template <int R, class Coef>
+__device__ __forceinline__ void tail_update(int64_t base, int64_t m0, int64_t m1, int64_t J, int jb,
+                                            int lg, const Ring* ring, Coef coef) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rs_bits = 5 - lg, G = 1 << lg;
+  const int g = lane >> rs_bits, rs = lane & ((1 << rs_bits) - 1);
+  const int64_t per_pass = (int64_t)kSweepThreads >> lg;
+  for (int64_t mb = m0; mb < m1; mb += per_pass) {
+    if (mb + ((int64_t)warp << rs_bits) >= m1) continue;  // warp-uniform
+    const int64_t m = mb + ((int64_t)warp << rs_bits) + rs;
+    const bool act = m < m1;
+    double sm[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[r] = 0.0;
+    if (act) {
+#pragma unroll 8
+      for (int c = g; c < jb; c += G) {
+        const double l = coef(m, c);
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[r] = __fma_rn(l, ring[r][J + c], sm[r]);
+      }
+    }
+    for (int o = 16; o >= (1 << rs_bits); o >>= 1)
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[r] = __dadd_rn(sm[r], __shfl_xor_sync(0xffffffffu, sm[r], o));
+    if (act && g == 0)
+#pragma unroll
+      for (int r = 0; r < R; ++r) ring[r][base + m] = __dsub_rn(ring[r][base + m], sm[r]);
+  }
+}
+
+// Warp c's dot s_c = sum_m coef(m) * ring[base + m], m in [m0, m1).
+template <int R, class Coef>
+__device__ __forceinline__ void warp_dot(int64_t base, int64_t m0, int64_t m1, const Ring* ring,
+                                         double* s_dot, int c, Coef coef) {
+  const int lane = threadIdx.x & 31;
+  double sm[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) sm[r] = 0.0;
+#pragma unroll 4
+  for (int64_t m = m0 + lane; m < m1; m += 32) {
+    const double u = coef(m);
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[r] = __fma_rn(u, ring[r][base + m], sm[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double t = warp_sum(sm[r]);
+    if (lane == 0) s_dot[r * kLUBlock + c] = t;
+  }
+}
+
+// ------------------------------------------------------------ L forward
+// x := (L-part)^{-1} x, i.e. LAPACK gbtrs 'N' first half: for every step j
+// interchange rows j, ipiv[j], then eliminate below j.
+template <int R>
+__device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S) {
   const int64_t n = b.n;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  // initial window: rows [0, min(n, 32 + kl)) and block 0's head
-  int64_t hi = lmin(n, kLUBlock + b.kl);
+  const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
+  if (n == 0) return;
+  const int lg = tail_log_lanes(b.kl);
+  Perm pq;
+  HeadPrefetch ph;
+  RowPrefetch<R> px;
+  int64_t hi = lmin(n, kLUBlock + b.kl);  // rows [.., hi) are in the ring
   for (int64_t i = tid; i < hi; i += nt)
 #pragma unroll
     for (int r = 0; r < R; ++r) ring[r][i] = x[r][i];
-  for (int q = tid; q < kLUBlock * kLUBlock; q += nt) H.v[q >> 5][q & 31] = b.lb[(int64_t)(q >> 5) * b.lb_ld + (q & 31)];
+  H.v[tid >> 5][tid & 31] = l_head_elem(b, 0, tid);
+  if (warp == 0) pq = load_perm(b, 0, lane);
   __syncthreads();
+  CK_PROF_INIT;
   for (int64_t J = 0; J < n; J += kLUBlock) {
     const int64_t blk = J / kLUBlock;
     const int jb = (int)lmin(kLUBlock, n - J);
     const int64_t wend = lmin(n, J + kLUBlock + b.kl);
-    const double* lb = b.lb + blk * kLUBlock * b.lb_ld;
+    const int64_t nend = lmin(n, J + 2 * kLUBlock + b.kl);
+    const bool more = J + kLUBlock < n;
+    const bool tail = wend > J + jb;
     if (warp == 0) {
-      int np;
-      const int32_t* pairs;
-      block_perm(b, blk, np, pairs);
-      double pv[2][R];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int t = lane + 32 * h;
-        if (t < np)
-#pragma unroll
-          for (int r = 0; r < R; ++r) pv[h][r] = ring[r][J + pairs[2 * t + 1]];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int t = lane + 32 * h;
-        if (t < np)
-#pragma unroll
-          for (int r = 0; r < R; ++r) ring[r][J + pairs[2 * t]] = pv[h][r];
-      }
-      __syncwarp();
+      apply_perm<R, false>(pq, ring, J, lane);
+      if (more) pq = load_perm(b, blk + 1, lane);
       double hv[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) hv[r] = lane < jb ? ring[r][J + lane] : 0.0;
-      for (int c = 0; c < jb; ++c) {
-        const double l = lane > c && lane < jb ? H.v[c][lane] : 0.0;
+      // branch-free: lanes <= c subtract 0 * y (lb is zero past the block)
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double y = __shfl_sync(0xffffffffu, hv[r], c);
-          if (lane > c && lane < jb) hv[r] = __dsub_rn(hv[r], __dmul_rn(l, y));
-        }
+      for (int c = 0; c < kLUBlock; ++c) {
+        const double l = lane > c ? H.v[c][lane] : 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) hv[r] = __dsub_rn(hv[r], __dmul_rn(l, __shfl_sync(0xffffffffu, hv[r], c)));
       }
       if (lane < jb)
 #pragma unroll
@@ -94,58 +344,46 @@ __device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring,
           ring[r][J + lane] = hv[r];
           x[r][J + lane] = hv[r];  // head rows are final
         }
-    }
-    __syncthreads();
-    // prefetch: the next block's head multipliers and its incoming rows
-    const bool more = J + kLUBlock < n;
-    const int64_t nend = lmin(n, J + 2 * kLUBlock + b.kl);
-    double pf_h = 0.0, pf_x[R];
-    if (more) {
-      const int q = tid;
-      if (q < kLUBlock * kLUBlock) pf_h = lb[(int64_t)kLUBlock * b.lb_ld + (int64_t)(q >> 5) * b.lb_ld + (q & 31)];
-      if (hi + tid < nend)
-#pragma unroll
-        for (int r = 0; r < R; ++r) pf_x[r] = x[r][hi + tid];
-    }
-    // tail: rows J+jb .. wend-1 minus the block's contributions (column order)
-    for (int64_t i = J + jb + tid; i < wend; i += nt) {
-      double acc[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = ring[r][i];
-      for (int c = 0; c < jb; ++c) {
-        const double l = lb[(int64_t)c * b.lb_ld + (i - J)];
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = __dsub_rn(acc[r], __dmul_rn(l, ring[r][J + c]));
+    } else {
+      if (tid == kIssuer && tail) S.issue(b.lb, jb, [&](int c) { return l_run_first(b, blk, c); });
+      if (more) {
+        ph.load([&](int q) { return l_head_elem(b, blk + 1, q); });
+        px.load(x, hi, nend);
       }
-#pragma unroll
-      for (int r = 0; r < R; ++r) ring[r][i] = acc[r];
+    }
+    CK_PROF(0);
+    __syncthreads();
+    CK_PROF(1);
+    if (tail) {
+      S.wait();
+      const double* lbk = b.lb + blk * kLUBlock * b.lb_ld;
+      tail_update<R>(J + kLUBlock, 0, wend - J - kLUBlock, J, jb, lg, ring, [&](int64_t m, int c) {
+        return m < S.srows ? S.at(c, (int)((c * b.lb_ld) & 1), m) : lbk[c * b.lb_ld + kLUBlock + m];
+      });
     }
     if (more) {
-      if (tid < kLUBlock * kLUBlock) H.v[tid >> 5][tid & 31] = pf_h;
-      if (hi + tid < nend)
-#pragma unroll
-        for (int r = 0; r < R; ++r) ring[r][hi + tid] = pf_x[r];
+      ph.commit(H);
+      px.commit(ring, hi, nend);
       hi = nend;
     }
+    CK_PROF(4);
     __syncthreads();
+    CK_PROF(5);
   }
 }
 
-// Element q (0..1023) of U's 32x32 diagonal block of block J, staged as
-// H.v[c][r] = U(J+r, J+c) for r <= c (zero elsewhere).
-__device__ __forceinline__ double u_head_elem(const BandView& b, int64_t J, int jb, int q) {
-  const int c = q >> 5, r = q & 31;
-  return (r <= c && c < jb && c - r <= b.kv) ? AB(b, J + r, J + c) : 0.0;
-}
-
-// x := U^{-1} x (backward), U of bandwidth kv above the diagonal. Same
-// two-barrier pipeline as sweep_l_forward, blocks in reverse.
+// ----------------------------------------------------------- U backward
+// x := U^{-1} x (backward), U of bandwidth kv above the diagonal; blocks in
+// reverse, same two phases as sweep_l_forward.
 template <int R>
-__device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring, Head& H) {
+__device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S) {
   const int64_t n = b.n;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = (n + kLUBlock - 1) / kLUBlock;
   if (nblk == 0) return;
+  const int lg = tail_log_lanes(b.kv);
+  HeadPrefetch ph;
+  RowPrefetch<R> px;
   int64_t lo;  // rows [lo, n) are in the ring
   {
     const int64_t J = (nblk - 1) * kLUBlock;
@@ -154,24 +392,30 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
 #pragma unroll
       for (int r = 0; r < R; ++r) ring[r][i] = x[r][i];
     H.v[tid >> 5][tid & 31] = u_head_elem(b, J, (int)(n - J), tid);
+    if (tid < kLUBlock) H.rd[tid] = u_head_rd(b, J, (int)(n - J), tid);
   }
   __syncthreads();
+  CK_PROF_INIT;
   for (int64_t blk = nblk - 1; blk >= 0; --blk) {
     const int64_t J = blk * kLUBlock;
     const int jb = (int)lmin(kLUBlock, n - J);
     const int64_t wbeg = lmax(0, J - b.kv);
+    const int64_t nlo = lmax(0, J - kLUBlock - b.kv);
+    const bool more = blk > 0;
+    const bool tail = J > wbeg;
     if (warp == 0) {
       double h[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) h[r] = lane < jb ? ring[r][J + lane] : 0.0;
-      for (int c = jb - 1; c >= 0; --c) {
-        const double d = H.v[c][c];
+#pragma unroll
+      for (int c = kLUBlock - 1; c >= 0; --c) {
+        const double d = H.v[c][c], rd = H.rd[c];
         const double u = lane < c ? H.v[c][lane] : 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const double y = __ddiv_rn(__shfl_sync(0xffffffffu, h[r], c), d);
-          if (lane == c) h[r] = y;
-          if (lane < c) h[r] = __dsub_rn(h[r], __dmul_rn(u, y));
+          const double y = div_rcp(__shfl_sync(0xffffffffu, h[r], c), d, rd);
+          const double t = __dsub_rn(h[r], __dmul_rn(u, y));
+          h[r] = lane == c ? y : t;
         }
       }
       if (lane < jb)
@@ -180,106 +424,93 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
           ring[r][J + lane] = h[r];
           x[r][J + lane] = h[r];
         }
-    }
-    __syncthreads();
-    const bool more = blk > 0;
-    const int64_t nlo = lmax(0, J - kLUBlock - b.kv);
-    double pf_h = 0.0, pf_x[R];
-    if (more) {
-      pf_h = u_head_elem(b, J - kLUBlock, kLUBlock, tid);
-      if (nlo + tid < lo)
-#pragma unroll
-        for (int r = 0; r < R; ++r) pf_x[r] = x[r][nlo + tid];
-    }
-    for (int64_t i = wbeg + tid; i < J; i += nt) {
-      double acc[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = ring[r][i];
-      const int cend = (int)lmin(jb, i + b.kv - J + 1);  // U(i, J+c) in band
-      for (int c = 0; c < cend; ++c) {
-        const int64_t k = J + c;
-        const double u = AB(b, i, k);
-        if (u != 0.0)
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = __dsub_rn(acc[r], __dmul_rn(u, ring[r][k]));
+    } else {
+      if (tid == kIssuer && tail) S.issue(b.ab, jb, [&](int c) { return u_run_first(b, J, c); });
+      if (more) {
+        ph.load([&](int q) { return u_head_elem(b, J - kLUBlock, kLUBlock, q); },
+                [&](int c) { return u_head_rd(b, J - kLUBlock, kLUBlock, c); });
+        px.load(x, nlo, lo);
       }
-#pragma unroll
-      for (int r = 0; r < R; ++r) ring[r][i] = acc[r];
+    }
+    CK_PROF(8);
+    __syncthreads();
+    CK_PROF(9);
+    if (tail) {
+      S.wait();
+      // tail row i = J - kv + m; U(i, J+c) lies in the band for m >= c
+      tail_update<R>(J - b.kv, wbeg - (J - b.kv), b.kv, J, jb, lg, ring, [&](int64_t m, int c) {
+        if (m < c) return 0.0;
+        const int64_t f = u_run_first(b, J, c);
+        return m < S.srows ? S.at(c, (int)(f & 1), m) : b.ab[f + m];
+      });
     }
     if (more) {
-      H.v[tid >> 5][tid & 31] = pf_h;
-      if (nlo + tid < lo)
-#pragma unroll
-        for (int r = 0; r < R; ++r) ring[r][nlo + tid] = pf_x[r];
+      ph.commit(H, true);
+      px.commit(ring, nlo, lo);
       lo = nlo;
     }
+    CK_PROF(12);
     __syncthreads();
+    CK_PROF(13);
   }
 }
 
+// ---------------------------------------------------------- U^T forward
 // x := U^{-T} x (forward): w_k = (x_k - sum_{i<k} U(i,k) w_i) / U(k,k).
-// Phase 1: commit the block's staged head and rows, start loading the next
-// block's, one warp per head row forms its dot over the final rows below J.
-// Phase 2: warp 0 solves the head triangle.
+// Phase 1: warp c forms head row c's dot over the final rows below J (from
+// the stage). Phase 2: warp 0 solves the head triangle while the stage and
+// the idle warps fetch the next block.
 template <int R>
 __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring, double* s_dot,
-                                 Head& H) {
+                                 Head& H, Stage& S) {
   const int64_t n = b.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double pf_h = 0.0, pf_x[R];
-  if (n > 0) {
-    pf_h = u_head_elem(b, 0, (int)lmin(kLUBlock, n), tid);
-    if (tid < lmin(kLUBlock, n))
+  if (n == 0) return;
+  HeadPrefetch ph;
+  RowPrefetch<R> px;
+  // block 0: head and rows straight in
+  H.v[tid >> 5][tid & 31] = u_head_elem(b, 0, (int)lmin(kLUBlock, n), tid);
+  if (tid < kLUBlock) H.rd[tid] = u_head_rd(b, 0, (int)lmin(kLUBlock, n), tid);
+  if (tid < lmin(kLUBlock, n))
 #pragma unroll
-      for (int r = 0; r < R; ++r) pf_x[r] = x[r][tid];
-  }
+    for (int r = 0; r < R; ++r) ring[r][tid] = x[r][tid];
+  __syncthreads();
+  CK_PROF_INIT;
   for (int64_t J = 0; J < n; J += kLUBlock) {
     const int jb = (int)lmin(kLUBlock, n - J);
-    H.v[tid >> 5][tid & 31] = pf_h;
-    if (tid < jb)
-#pragma unroll
-      for (int r = 0; r < R; ++r) ring[r][J + tid] = pf_x[r];
     const int64_t J1 = J + kLUBlock;
-    if (J1 < n) {
-      const int jb1 = (int)lmin(kLUBlock, n - J1);
-      pf_h = u_head_elem(b, J1, jb1, tid);
-      if (tid < jb1)
-#pragma unroll
-        for (int r = 0; r < R; ++r) pf_x[r] = x[r][J1 + tid];
-    }
-    if (warp < jb) {
-      const int c = warp;
-      const int64_t k = J + c;
-      const int64_t i0 = lmax(0, k - b.kv);
-      double sm[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) sm[r] = 0.0;
-      for (int64_t i = i0 + lane; i < J; i += 32) {
-        const double u = AB(b, i, k);
-#pragma unroll
-        for (int r = 0; r < R; ++r) sm[r] = __fma_rn(u, ring[r][i], sm[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double t = warp_sum(sm[r]);
-        if (lane == 0) s_dot[r * kLUBlock + c] = t;
+    const bool dots = J > 0;
+    if (dots) {
+      S.wait();
+      if (warp < jb) {
+        const int c = warp;
+        // rows i = J - kv + m of column J+c: in the band for m >= c, i >= 0
+        const int64_t f = u_run_first(b, J, c);
+        warp_dot<R>(J - b.kv, lmax(c, b.kv - J), b.kv, ring, s_dot, c, [&](int64_t m) {
+          return m < S.srows ? S.at(c, (int)(f & 1), m) : b.ab[f + m];
+        });
       }
     }
+    CK_PROF(16);
     __syncthreads();
+    CK_PROF(17);
     if (warp == 0) {
       double h[R];
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        h[r] = lane < jb ? __dsub_rn(ring[r][J + lane], s_dot[r * kLUBlock + lane]) : 0.0;
-      for (int c = 0; c < jb; ++c) {
-        const double d = H.v[c][c];
+        h[r] = lane < jb ? (dots ? __dsub_rn(ring[r][J + lane], s_dot[r * kLUBlock + lane])
+                                 : ring[r][J + lane])
+                         : 0.0;
+#pragma unroll
+      for (int c = 0; c < kLUBlock; ++c) {
+        const double d = H.v[c][c], rd = H.rd[c];
         // U(J+c, J+lane) for lane > c: column J+lane, row J+c
-        const double u = lane > c && lane < jb ? H.v[lane][c] : 0.0;
+        const double u = lane > c ? H.v[lane][c] : 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const double w = __ddiv_rn(__shfl_sync(0xffffffffu, h[r], c), d);
-          if (lane == c) h[r] = w;
-          if (lane > c) h[r] = __dsub_rn(h[r], __dmul_rn(u, w));
+          const double w = div_rcp(__shfl_sync(0xffffffffu, h[r], c), d, rd);
+          const double t = __dsub_rn(h[r], __dmul_rn(u, w));
+          h[r] = lane == c ? w : t;
         }
       }
       if (lane < jb)
@@ -288,109 +519,108 @@ __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring
           ring[r][J + lane] = h[r];
           x[r][J + lane] = h[r];
         }
+    } else if (J1 < n) {
+      const int jb1 = (int)lmin(kLUBlock, n - J1);
+      if (tid == kIssuer) S.issue(b.ab, jb1, [&](int c) { return u_run_first(b, J1, c); });
+      ph.load([&](int q) { return u_head_elem(b, J1, jb1, q); },
+              [&](int c) { return u_head_rd(b, J1, jb1, c); });
+      px.load(x, J1, J1 + jb1);
     }
+    CK_PROF(20);
     __syncthreads();
+    CK_PROF(21);
+    if (J1 < n) {
+      ph.commit(H, true);
+      px.commit(ring, J1, lmin(n, J1 + kLUBlock));
+    }
   }
+  __syncthreads();
 }
 
+// --------------------------------------------------------- L^T backward
 // x := (L-part)^{-T} x: LAPACK gbtrs 'T' second half, blocks in reverse.
-// Phase 1: commit the block's head multipliers and head rows, write out the
-// rows the previous block finalised, start the next block's loads, one warp
-// per head column forms its dot over the tail. Phase 2: warp 0 solves the
-// head and applies the block's inverse interchange.
+// Phase 1: warp c forms head column c's dot over the block's tail (from the
+// stage) and the rows the previous block finalised go out. Phase 2: warp 0
+// solves the head and applies the block's inverse interchange while the
+// stage and the idle warps fetch the next block.
 template <int R>
 __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring, double* s_dot,
-                                 Head& H) {
+                                 Head& H, Stage& S) {
   const int64_t n = b.n;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = (n + kLUBlock - 1) / kLUBlock;
   if (nblk == 0) return;
-  double pf_h, pf_x[R];
+  Perm pq;
+  HeadPrefetch ph;
+  RowPrefetch<R> px;
   {
     const int64_t J = (nblk - 1) * kLUBlock;
-    pf_h = b.lb[J * b.lb_ld + (int64_t)(tid >> 5) * b.lb_ld + (tid & 31)];
+    H.v[tid >> 5][tid & 31] = l_head_elem(b, nblk - 1, tid);
     if (J + tid < n)
 #pragma unroll
-      for (int r = 0; r < R; ++r) pf_x[r] = x[r][J + tid];
+      for (int r = 0; r < R; ++r) ring[r][J + tid] = x[r][J + tid];
+    if (warp == 0) pq = load_perm(b, nblk - 1, lane);
   }
+  __syncthreads();
+  CK_PROF_INIT;
   for (int64_t blk = nblk - 1; blk >= 0; --blk) {
     const int64_t J = blk * kLUBlock;
     const int jb = (int)lmin(kLUBlock, n - J);
     const int64_t wend = lmin(n, J + kLUBlock + b.kl);
-    const double* lb = b.lb + blk * kLUBlock * b.lb_ld;
-    H.v[tid >> 5][tid & 31] = pf_h;
-    if (tid < jb)
-#pragma unroll
-      for (int r = 0; r < R; ++r) ring[r][J + tid] = pf_x[r];
+    const bool dots = wend > J + jb;
     if (blk + 1 < nblk) {  // rows block blk+1 finalised: [J1 + kl, wend1)
       const int64_t J1 = J + kLUBlock;
       for (int64_t i = J1 + b.kl + tid; i < lmin(n, J1 + kLUBlock + b.kl); i += nt)
 #pragma unroll
         for (int r = 0; r < R; ++r) x[r][i] = ring[r][i];
     }
-    if (blk > 0) {
-      pf_h = lb[-(int64_t)kLUBlock * b.lb_ld + (int64_t)(tid >> 5) * b.lb_ld + (tid & 31)];
-      if (tid < kLUBlock)
-#pragma unroll
-        for (int r = 0; r < R; ++r) pf_x[r] = x[r][J - kLUBlock + tid];
-    }
-    if (warp < jb) {
-      const int c = warp;
-      double sm[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) sm[r] = 0.0;
-      for (int64_t i = J + jb + lane; i < wend; i += 32) {
-        const double l = lb[(int64_t)c * b.lb_ld + (i - J)];
-#pragma unroll
-        for (int r = 0; r < R; ++r) sm[r] = __fma_rn(l, ring[r][i], sm[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double t = warp_sum(sm[r]);
-        if (lane == 0) s_dot[r * kLUBlock + c] = t;
+    if (dots) {
+      S.wait();
+      if (warp < jb) {
+        const int c = warp;
+        const double* col = b.lb + l_run_first(b, blk, c);
+        const int off = (int)((c * b.lb_ld) & 1);
+        warp_dot<R>(J + kLUBlock, 0, wend - J - kLUBlock, ring, s_dot, c,
+                    [&](int64_t m) { return m < S.srows ? S.at(c, off, m) : col[m]; });
       }
     }
+    CK_PROF(24);
     __syncthreads();
+    CK_PROF(25);
     if (warp == 0) {
       double h[R];
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        h[r] = lane < jb ? __dsub_rn(ring[r][J + lane], s_dot[r * kLUBlock + lane]) : 0.0;
-      for (int c = jb - 1; c >= 0; --c) {
+        h[r] = lane < jb ? (dots ? __dsub_rn(ring[r][J + lane], s_dot[r * kLUBlock + lane])
+                                 : ring[r][J + lane])
+                         : 0.0;
+#pragma unroll
+      for (int c = kLUBlock - 1; c >= 0; --c) {
         // u_c is final; push -l(c, lane) u_c into the columns lane < c
         const double l = lane < c ? H.v[lane][c] : 0.0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double u = __shfl_sync(0xffffffffu, h[r], c);
-          if (lane < c) h[r] = __dsub_rn(h[r], __dmul_rn(l, u));
-        }
+        for (int r = 0; r < R; ++r) h[r] = __dsub_rn(h[r], __dmul_rn(l, __shfl_sync(0xffffffffu, h[r], c)));
       }
       if (lane < jb)
 #pragma unroll
         for (int r = 0; r < R; ++r) ring[r][J + lane] = h[r];
       __syncwarp();
-      // inverse block interchange as one warp-wide scatter
-      int np;
-      const int32_t* pairs;
-      block_perm(b, blk, np, pairs);
-      double pv[2][R];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int t = lane + 32 * q;
-        if (t < np)
-#pragma unroll
-          for (int r = 0; r < R; ++r) pv[q][r] = ring[r][J + pairs[2 * t]];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int t = lane + 32 * q;
-        if (t < np)
-#pragma unroll
-          for (int r = 0; r < R; ++r) ring[r][J + pairs[2 * t + 1]] = pv[q][r];
-      }
+      apply_perm<R, true>(pq, ring, J, lane);
+      if (blk > 0) pq = load_perm(b, blk - 1, lane);
+    } else if (blk > 0) {
+      const int64_t Jp = J - kLUBlock;
+      if (tid == kIssuer && lmin(n, Jp + kLUBlock + b.kl) > J)
+        S.issue(b.lb, kLUBlock, [&](int c) { return l_run_first(b, blk - 1, c); });
+      ph.load([&](int q) { return l_head_elem(b, blk - 1, q); });
+      px.load(x, Jp, J);
     }
+    CK_PROF(28);
     __syncthreads();
+    CK_PROF(29);
+    if (blk > 0) {
+      ph.commit(H);
+      px.commit(ring, J - kLUBlock, J);
+    }
   }
   // rows no step can touch any more: everything below kl + 32
   for (int64_t i = tid; i < lmin(n, kLUBlock + b.kl); i += nt)
@@ -399,22 +629,42 @@ __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring
   __syncthreads();
 }
 
+// Dynamic shared memory of a solve CTA, in doubles: R rings of ring_size,
+// R*32 dot scratch, then the stage (16-byte aligned, b.stage_cap doubles).
+__host__ __device__ __forceinline__ int64_t stage_offset(int R, int ring_size) {
+  return (int64_t)R * ring_size + (int64_t)R * kLUBlock;
+}
+
 // x := A^{-1} x (transpose = false) or A^{-T} x, for R right-hand sides, by the
-// calling CTA; smem holds R rings of ring_size doubles plus R*32 dot scratch.
+// calling CTA of kSweepThreads threads.
 template <int R>
 __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, double* smem,
                                           int ring_size, bool transpose) {
   __shared__ Head H;
+  __shared__ alignas(8) uint64_t mbar;
   Ring ring[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) ring[r] = Ring{smem + (int64_t)r * ring_size, ring_size - 1};
   double* s_dot = smem + (int64_t)R * ring_size;
+  if (threadIdx.x == 0) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(&mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  Stage S;
+  S.st = smem + stage_offset(R, ring_size);
+  S.bar = &mbar;
   if (!transpose) {
-    sweep_l_forward<R>(b, x, ring, H);
-    sweep_u_backward<R>(b, x, ring, H);
+    S.layout(b.stage_cap, b.kl);
+    sweep_l_forward<R>(b, x, ring, H, S);
+    S.layout(b.stage_cap, b.kv);
+    sweep_u_backward<R>(b, x, ring, H, S);
   } else {
-    sweep_ut_forward<R>(b, x, ring, s_dot, H);
-    sweep_l_backward<R>(b, x, ring, s_dot, H);
+    S.layout(b.stage_cap, b.kv);
+    sweep_ut_forward<R>(b, x, ring, s_dot, H, S);
+    S.layout(b.stage_cap, b.kl);
+    sweep_l_backward<R>(b, x, ring, s_dot, H, S);
   }
 }
 
