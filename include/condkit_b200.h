@@ -203,6 +203,18 @@ ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restart
                                ck_norm_result* res, double* witness);
 ck_status ck_session_create_inverse(ck_lu f, const ck_adam_cfg* cfg, const uint64_t* seeds,
                                     int32_t ncols, ck_session* out);
+/* Ensembles on A^-1 (the sigma_min half of cond2 per member, config 5): nmem
+ * independent factorisations, one device CTA per member per step. Column
+ * k = g * ncols + c in ck_session_result; seeds has nmem * ncols entries.
+ * Replaces running InverseOracle/estimate_norm (condest.hpp:156-175, 301-312)
+ * once per matrix as run_bench does (bench.hpp:435). */
+ck_status ck_session_create_inverse_batch(const ck_lu* lus, int32_t nmem, const ck_adam_cfg* cfg,
+                                          const uint64_t* seeds, int32_t ncols, ck_session* out);
+/* estimate_norm on every A_g^-1; member g's restarts seeded as in
+ * ck_estimate_norm_batch; results[g] is the best of member g. */
+ck_status ck_inv_estimate_norm_batch(const ck_lu* lus, int32_t nmem, const ck_adam_cfg* cfg,
+                                     const uint64_t* member_seeds, uint64_t restarts,
+                                     ck_norm_result* results);
 /* cond2(A, cfg, restarts, pivot_tol), condest.hpp:341-365 (Cond2Result without the
  * factors: has_factors reports whether they were formed). */
 ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, double pivot_tol,

@@ -100,6 +100,11 @@ _SIGS = {
                                           C.c_int32, C.POINTER(C.c_void_p)]),
     "ck_estimate_norm_batch": (C.c_int, [C.c_void_p, i64p, C.c_int32, C.POINTER(AdamCfg), u64p,
                                          C.c_uint64, C.POINTER(NormResult)]),
+    "ck_session_create_inverse_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32,
+                                                  C.POINTER(AdamCfg), u64p, C.c_int32,
+                                                  C.POINTER(C.c_void_p)]),
+    "ck_inv_estimate_norm_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(AdamCfg),
+                                             u64p, C.c_uint64, C.POINTER(NormResult)]),
     "ck_generate": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_uint64, i64p, i64p, i64p, i32p,
                               dp]),
 }

@@ -16,6 +16,7 @@ import numpy as np
 
 from . import _lib
 from .condest import AdamConfig, NormEstimate, Session
+from .errors import NumericallySingular, StructurallySingular
 from .rng import mix_seed
 from .sparse import SparseMatrix
 
@@ -95,3 +96,104 @@ class BatchSession(Session):
         _lib.check(_lib.load().ck_session_result(self.handle, g * self.ncols + c, C.byref(r),
                                                  _lib.dptr(w)), "ck_session_result")
         return NormEstimate(r.value, w, int(r.iterations), bool(r.converged))
+
+
+# ------------------------------------------------------------ sigma_min side
+def lu_factorize_many(members: Sequence[SparseMatrix], pivot_tol: float = 1e-14,
+                      threads: int = 8) -> list:
+    """lu_factorize for every member, several factorisations in flight on the
+    device at once (each runs on its own stream; the C calls release the GIL).
+    Singular members give the exception instance instead of factors."""
+    from concurrent.futures import ThreadPoolExecutor  # noqa: PLC0415
+    from .inverse import lu_factorize  # noqa: PLC0415
+
+    def one(m):
+        try:
+            return lu_factorize(m, pivot_tol)
+        except (StructurallySingular, NumericallySingular) as e:
+            return e
+
+    if threads <= 1 or len(members) <= 1:
+        return [one(m) for m in members]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(one, members))
+
+
+def _lu_handles(factors):
+    arr = (C.c_void_p * len(factors))()
+    for g, f in enumerate(factors):
+        arr[g] = f.handle
+    return arr
+
+
+def inv_estimate_norm_batch(factors, cfg: Optional[AdamConfig] = None, restarts: int = 4,
+                            seeds: Optional[Sequence[int]] = None) -> list[NormEstimate]:
+    """estimate_norm on A_g^-1 (InverseOracle, condest.hpp:156-175, 301-312) for
+    every member, one device CTA per member per step."""
+    cfg = cfg or AdamConfig()
+    seeds = np.ascontiguousarray(seeds if seeds is not None else [cfg.seed] * len(factors),
+                                 np.uint64)
+    res = (_lib.NormResult * len(factors))()
+    c = _lib.cfg_struct(cfg)
+    _lib.check(_lib.load().ck_inv_estimate_norm_batch(
+        _lu_handles(factors), len(factors), C.byref(c), seeds.ctypes.data_as(_lib.u64p), restarts,
+        res), "inv_estimate_norm_batch")
+    return [NormEstimate(r.value, np.zeros(0), int(r.iterations), bool(r.converged)) for r in res]
+
+
+class InverseBatchSession(Session):
+    """Device loop over many factorisations: members x restart columns."""
+
+    def __init__(self, factors, cfg: AdamConfig, seeds_per_member_column):
+        self.factors = list(factors)  # keeps the factors alive
+        self.seg_n = np.array([f.n for f in self.factors], np.int64)
+        self.n = int(self.seg_n.max())
+        seeds = np.ascontiguousarray(seeds_per_member_column, np.uint64)
+        self.ncols = seeds.size // len(self.factors)
+        lib = _lib.load()
+        self._cfg = _lib.cfg_struct(cfg)
+        h = C.c_void_p()
+        _lib.check(lib.ck_session_create_inverse_batch(
+            _lu_handles(self.factors), len(self.factors), C.byref(self._cfg),
+            seeds.ctypes.data_as(_lib.u64p), self.ncols, C.byref(h)),
+            "ck_session_create_inverse_batch")
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.ck_session_free, h)
+
+    def member_result(self, g: int, c: int = 0) -> NormEstimate:
+        r = _lib.NormResult()
+        w = np.empty(int(self.seg_n[g]))
+        _lib.check(_lib.load().ck_session_result(self.handle, g * self.ncols + c, C.byref(r),
+                                                 _lib.dptr(w)), "ck_session_result")
+        return NormEstimate(r.value, w, int(r.iterations), bool(r.converged))
+
+
+def cond2_batch(members: Sequence[SparseMatrix], cfg: Optional[AdamConfig] = None,
+                restarts: int = 4, pivot_tol: float = 1e-14,
+                seeds: Optional[Sequence[int]] = None, wave: int = 32, threads: int = 8):
+    """cond2 (condest.hpp:341-365) of every member, as run_bench computes it per
+    matrix with seed seeds[g] (default: member_seeds): ||A_g|| for the whole
+    ensemble in one packed device sweep, then the factorisations and ||A_g^-1||
+    in waves of `wave` members (bounded device memory), one CTA per member."""
+    from .inverse import Cond2Result  # noqa: PLC0415
+    cfg = cfg or AdamConfig()
+    seeds = list(seeds) if seeds is not None else member_seeds(len(members), cfg.seed)
+    fwd = estimate_norm_batch(members, cfg, restarts, seeds)
+    out = [Cond2Result(operator_norm=e) for e in fwd]
+    for w0 in range(0, len(members), wave):
+        idx = list(range(w0, min(len(members), w0 + wave)))
+        facs = lu_factorize_many([members[g] for g in idx], pivot_tol, threads)
+        ok = [g for g, f in zip(idx, facs) if not isinstance(f, Exception)]
+        for g, f in zip(idx, facs):
+            if isinstance(f, Exception):
+                out[g].inverse_norm = NormEstimate(value=float("inf"))
+                out[g].kappa = float("inf")
+        if ok:
+            fs = [facs[g - w0] for g in ok]
+            inv = inv_estimate_norm_batch(fs, cfg, restarts,
+                                          [mix_seed(seeds[g], 0x1234) for g in ok])
+            for g, e in zip(ok, inv):
+                out[g].inverse_norm = e
+                out[g].kappa = out[g].operator_norm.value * e.value
+        del facs
+    return out

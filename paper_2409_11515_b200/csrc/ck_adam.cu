@@ -409,16 +409,15 @@ static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
     k_apply<R, false><<<s->args.units_A, kTile, 0, st>>>(s->args);
 }
 
-void launch_inv_step(const InvArgs& a, int R, cudaStream_t st);
-void prepare_inv_step(const BandView& b, int R);
+void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st);
+void prepare_inv_step(size_t smem, int R);
+size_t inv_step_smem(const BandView& b, int R);
 int lu_ring_size(const BandView& b);
 int64_t lu_stage_cap(const BandView& b, int R);
 void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st);
 
 static void launch_inv_half(ck_session_s* s, int half, cudaStream_t st) {
-  InvArgs a = s->iargs;
-  a.half = half;
-  launch_inv_step(a, s->R, st);
+  launch_inv_step(s->dargs.p, s->S, s->R, s->inv_smem, half, st);
 }
 
 static void launch_apply_only(ck_session_s* s, cudaStream_t st) {
@@ -737,47 +736,79 @@ void session_create_batch(ck_session_s* s, ck_matrix_s* A, const int64_t* seg_n,
   session_create_explicit(s, A, cfg, seeds, R, seg_n, S);
 }
 
-void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg,
-                            const uint64_t* seeds, int R) {
+// InverseOracle session over S >= 1 independent factorisations (member g's
+// vectors at [off_g, off_g + n_g) of the internal vectors, off_g = sum of
+// round_up(n_h, 32)); one CTA per member advances its R columns.
+void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
+                                  const ck_adam_cfg* cfg, const uint64_t* seeds, int R) {
   if (R < 1 || R > kMaxCols) fail(CK_ERR_INVALID_ARGUMENT, "session columns must be 1..4");
-  if (lu->n == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
+  if (S < 1) fail(CK_ERR_INVALID_ARGUMENT, "at least one member");
+  for (int g = 0; g < S; ++g) {
+    if (lus[g]->n == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
+    if (lus[g]->device != lus[0]->device) fail(CK_ERR_INVALID_ARGUMENT, "members on different devices");
+  }
   s->kind = 1;
-  s->lu = lu;
+  s->lus.assign(lus, lus + S);
+  s->lu = lus[0];
   s->A = nullptr;
   s->R = R;
-  s->S = 1;
-  s->stream = lu->stream;
-  s->device = lu->device;
-  s->n = lu->n;
-  s->npad = lu->n;
+  s->S = S;
+  s->stream = lus[0]->stream;
+  s->device = lus[0]->device;
   s->perm = nullptr;
-  s->seg_n.assign(1, lu->n);
-  s->seg_off.assign(1, 0);
-  s->seg_pad.assign(1, lu->n);
+  s->seg_n.assign(S, 0);
+  s->seg_off.assign(S, 0);
+  s->seg_pad.assign(S, 0);
+  int64_t off = 0;
+  size_t smem = 0;
+  double bytes_per_step = 0.0;
+  for (int g = 0; g < S; ++g) {
+    const int64_t n = lus[g]->n;
+    s->seg_n[g] = n;
+    s->seg_off[g] = off;
+    s->seg_pad[g] = S == 1 ? n : ceil_div(n, 32) * 32;
+    off += s->seg_pad[g];
+    smem = std::max(smem, inv_step_smem(lus[g]->view(), R));
+    bytes_per_step += 8.0 * 4.0 * (double)(2 * lus[g]->kl + lus[g]->ku + 1) * (double)n;
+  }
+  s->npad = off;
+  s->n = S == 1 ? s->seg_n[0] : off;
   s->prm = Params{cfg->alpha, cfg->beta1, cfg->beta2, cfg->eps_stab, cfg->rel_tol, cfg->max_iter,
                   cfg->patience};
-  const BandView b = lu->view();
-  prepare_inv_step(b, R);
-  const int64_t yw = s->n * R;
+  s->inv_smem = smem;
+  prepare_inv_step(smem, R);
+  const int64_t yw = s->npad * R;
   s->PX.alloc(3 * R * s->npad);
   s->MV.alloc(s->npad * R);
   s->y.alloc(yw);
-  s->st.alloc(R);
-  s->hdr.alloc(1);
-  InvArgs& a = s->iargs;
-  a.b = b;
-  a.n = s->n;
-  a.ring_size = lu_ring_size(b);
-  a.b.stage_cap = lu_stage_cap(b, R);
-  a.PX = s->PX.p;
-  a.MV = s->MV.p;
-  a.y = s->y.p;
-  a.st = s->st.p;
-  a.hdr = s->hdr.p;
-  a.prm = s->prm;
-  a.half = 0;
-  const double bytes_per_step = 8.0 * 4.0 * (double)(2 * lu->kl + lu->ku + 1) * (double)lu->n;
+  s->st.alloc((int64_t)S * R);
+  s->hdr.alloc(S);
+  std::vector<InvArgs> h((size_t)S);
+  for (int g = 0; g < S; ++g) {
+    InvArgs& a = h[g];
+    const BandView b = lus[g]->view();
+    const int64_t o = s->seg_off[g];
+    a.b = b;
+    a.n = s->seg_n[g];
+    a.ring_size = lu_ring_size(b);
+    a.b.stage_cap = (int64_t)(smem / sizeof(double)) - stage_offset(R, a.ring_size);
+    if (a.b.stage_cap < 0) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+    a.PX = s->PX.p + o * R;
+    a.pstride = s->npad * R;
+    a.MV = s->MV.p + o * R;
+    a.y = s->y.p + o * R;
+    a.st = s->st.p + (int64_t)g * R;
+    a.hdr = s->hdr.p + g;
+    a.prm = s->prm;
+  }
+  s->dargs.alloc(S);
+  CK_CUDA(cudaMemcpy(s->dargs.p, h.data(), sizeof(InvArgs) * S, cudaMemcpyHostToDevice));
   session_init_common(s, cfg, seeds, yw, bytes_per_step * 50.0);
+}
+
+void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg,
+                            const uint64_t* seeds, int R) {
+  session_create_inverse_batch(s, &lu, 1, cfg, seeds, R);
 }
 
 void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished) {
@@ -861,16 +892,18 @@ void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_tota
 
 // ||Op v|| for an internal plain vector v (witness re-check, condest.hpp:284-289);
 // v is zero outside the member's range, so the whole-operator norm is the member's.
-static double op_norm(ck_session_s* s, const double* v, cudaStream_t st) {
+static double op_norm(ck_session_s* s, int g, const double* v, cudaStream_t st) {
   if (s->kind == 0) {
     matrix_apply_perm(s->A, v, s->tmp.p, st);
     return device_norm(s->tmp.p, s->A->a.nrows_pad, s->A->s_red.p, st);
   }
-  double* w = s->lu->work.p;
-  CK_CUDA(cudaMemcpyAsync(w, v, sizeof(double) * s->n, cudaMemcpyDeviceToDevice, st));
+  ck_lu_s* lu = s->lus[g];
+  const int64_t n = s->seg_n[g];
+  double* w = lu->work.p;
+  CK_CUDA(cudaMemcpyAsync(w, v + s->seg_off[g], sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   double* xs[1] = {w};
-  lu_solve_launch(s->lu, xs, 1, false, st);
-  return device_norm(w, s->n, w + s->n, st);
+  lu_solve_launch(lu, xs, 1, false, st);
+  return device_norm(w, n, w + n, st);
 }
 
 // Final NormEstimate of column k = g * R + c (member g, restart column c),
@@ -898,7 +931,7 @@ void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness
   res->_pad = 0;
   if (std::isfinite(cs.loss_min)) {
     res->value = std::exp(-cs.loss_min);
-    const double chk = op_norm(s, xbest, st);
+    const double chk = op_norm(s, g, xbest, st);
     if (!(std::fabs(chk - res->value) <= 1e-12 * std::max(res->value, chk)))
       fail(CK_ERR_LOGIC, "norm estimate does not match ||Op witness||");
   } else {

@@ -680,6 +680,8 @@ ck_status ck_grad_inverse(ck_lu f, const double* x, double* g) {
 namespace ck {
 void session_create_batch(ck_session_s* s, ck_matrix_s* A, const int64_t* seg_n, int S,
                           const ck_adam_cfg* cfg, const uint64_t* seeds, int R);
+void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
+                                  const ck_adam_cfg* cfg, const uint64_t* seeds, int R);
 }
 
 extern "C" {
@@ -726,6 +728,63 @@ ck_status ck_estimate_norm_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg
       int32_t fin = 0;
       session_run(&s, 0, &fin);
       for (int g = 0; g < nseg; ++g)
+        for (int c = 0; c < R; ++c) {
+          ck_norm_result e{};
+          session_result(&s, g * R + c, &e, nullptr);
+          if (!have[g] || e.value > results[g].value) {
+            results[g] = e;
+            have[g] = 1;
+          }
+        }
+    }
+  });
+}
+
+// InverseOracle over S independent factorisations: one session, one CTA per
+// member per step (the sigma_min half of cond2 for an ensemble, config 5).
+ck_status ck_session_create_inverse_batch(const ck_lu* lus, int32_t nmem, const ck_adam_cfg* cfg,
+                                          const uint64_t* seeds, int32_t ncols, ck_session* out) {
+  return guarded([&] {
+    check_cfg(cfg);
+    if (nmem < 1) fail(CK_ERR_INVALID_ARGUMENT, "at least one member");
+    std::vector<ck_lu_s*> f((size_t)nmem);
+    for (int g = 0; g < nmem; ++g) f[g] = LU(lus[g]);
+    auto* s = new ck_session_s();
+    try {
+      session_create_inverse_batch(s, f.data(), nmem, cfg, seeds, ncols);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+// estimate_norm on A_g^{-1} for every member g (restart seeds as in
+// ck_estimate_norm_batch).
+ck_status ck_inv_estimate_norm_batch(const ck_lu* lus, int32_t nmem, const ck_adam_cfg* cfg,
+                                     const uint64_t* member_seeds, uint64_t restarts,
+                                     ck_norm_result* results) {
+  return guarded([&] {
+    check_cfg(cfg);
+    if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
+    if (nmem < 1) fail(CK_ERR_INVALID_ARGUMENT, "at least one member");
+    std::vector<ck_lu_s*> f((size_t)nmem);
+    for (int g = 0; g < nmem; ++g) f[g] = LU(lus[g]);
+    std::vector<char> have((size_t)nmem, 0);
+    for (uint64_t r0 = 0; r0 < restarts; r0 += kMaxCols) {
+      const int R = (int)std::min<uint64_t>(kMaxCols, restarts - r0);
+      std::vector<uint64_t> seeds((size_t)nmem * R);
+      for (int g = 0; g < nmem; ++g)
+        for (int c = 0; c < R; ++c) {
+          const uint64_t r = r0 + c;
+          seeds[(size_t)g * R + c] = r == 0 ? member_seeds[g] : ck_mix_seed(member_seeds[g], r);
+        }
+      ck_session_s s;
+      session_create_inverse_batch(&s, f.data(), nmem, cfg, seeds.data(), R);
+      int32_t fin = 0;
+      session_run(&s, 0, &fin);
+      for (int g = 0; g < nmem; ++g)
         for (int c = 0; c < R; ++c) {
           ck_norm_result e{};
           session_result(&s, g * R + c, &e, nullptr);

@@ -25,8 +25,11 @@ __device__ __forceinline__ double xtilde_inv(double2 p, double rad) {
   return __dsub_rn(p.x, __dsub_rn(p.y, __dmul_rn(rad, p.x)));
 }
 
+// One CTA per member: blockIdx.x selects the member's arguments. half: 0 the
+// whole step, 1 the apply half only, 2 the transpose half only (observer).
 template <int R>
-__global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvArgs a) {
+__global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ args, int half) {
+  const InvArgs& a = args[blockIdx.x];
   extern __shared__ double smem[];
   __shared__ double s_h[32], s_l[32];
   __shared__ int s_e[32], s_f[32];
@@ -48,10 +51,10 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
     act[r] = ph == PH_PRO || ph == PH_APPLY;
     pro[r] = ph == PH_PRO;
     rad[r] = pro[r] ? 0.0 : a.st[r].rad;
-    xc[r] = a.PX + (int64_t)a.st[r].cur * n * R + r;  // element i at xc[r][i * R]
+    xc[r] = a.PX + a.st[r].cur * a.pstride + r;  // element i at xc[r][i * R]
     any |= act[r];
   }
-  if (any && a.half != 2) {
+  if (any && half != 2) {
     DD dd[R];
     ES dn[R];
     double xd[R];
@@ -130,11 +133,11 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
     iy2[r] = s.inv_y2;
     mc[r] = s.mc;
     vc[r] = s.vc;
-    xc[r] = a.PX + (int64_t)s.cur * n * R + r;
-    xn_out[r] = a.PX + (int64_t)(mat[r] ? s.nxt : s.cur) * n * R + r;
+    xc[r] = a.PX + s.cur * a.pstride + r;
+    xn_out[r] = a.PX + (mat[r] ? s.nxt : s.cur) * a.pstride + r;
     anyg |= grad[r];
   }
-  if (anyg && a.half != 1) {
+  if (anyg && half != 1) {
     inv_solve<R>(a.b, ys, smem, a.ring_size, true);
     __syncthreads();
     const Params& p = a.prm;
@@ -193,27 +196,21 @@ __global__ void __launch_bounds__(1024) k_inv_step(const __grid_constant__ InvAr
   }
 }
 
-size_t inv_step_smem(const BandView& b, int R);
-int lu_ring_size(const BandView& b);
-int64_t lu_stage_cap(const BandView& b, int R);
-
-void prepare_inv_step(const BandView& b, int R) {
-  const size_t smem = inv_step_smem(b, R);
-  if (lu_stage_cap(b, R) < 0) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+void prepare_inv_step(size_t smem, int R) {
   switch (R) {
-    case 1: CK_CUDA(cudaFuncSetAttribute(k_inv_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
-    case 2: CK_CUDA(cudaFuncSetAttribute(k_inv_step<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
-    case 3: CK_CUDA(cudaFuncSetAttribute(k_inv_step<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
-    default: CK_CUDA(cudaFuncSetAttribute(k_inv_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); break;
+    case 1: CK_CUDA(allow_max_dynamic_smem(k_inv_step<1>)); break;
+    case 2: CK_CUDA(allow_max_dynamic_smem(k_inv_step<2>)); break;
+    case 3: CK_CUDA(allow_max_dynamic_smem(k_inv_step<3>)); break;
+    default: CK_CUDA(allow_max_dynamic_smem(k_inv_step<4>)); break;
   }
 }
 
-void launch_inv_step(const InvArgs& a, int R, cudaStream_t st) {
-  const size_t smem = inv_step_smem(a.b, R);
+// S members, one CTA each, smem bytes of dynamic shared memory per CTA.
+void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st) {
   switch (R) {
 #define CK_INV_CASE(RR)                                                                        \
   case RR:                                                                                     \
-    k_inv_step<RR><<<1, 1024, smem, st>>>(a);                                                  \
+    k_inv_step<RR><<<S, 1024, smem, st>>>(args, half);                                         \
     break;
     CK_INV_CASE(1)
     CK_INV_CASE(2)

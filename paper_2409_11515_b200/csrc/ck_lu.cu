@@ -308,8 +308,7 @@ void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaSt
   switch (R) {
 #define CK_SOLVE_CASE(RR)                                                                       \
   case RR:                                                                                      \
-    CK_CUDA(cudaFuncSetAttribute(k_lu_solve<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                 (int)smem));                                                   \
+    CK_CUDA(allow_max_dynamic_smem(k_lu_solve<RR>));                                            \
     k_lu_solve<RR><<<1, 1024, smem, st>>>(b, xs[0], xs[1], xs[2], xs[3], transpose ? 1 : 0, ring); \
     break;
     CK_SOLVE_CASE(1)
@@ -360,7 +359,7 @@ void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_co
   CK_CUDA(cudaGetLastError());
   const size_t usmem = sizeof(double) * kLUBlock * (size_t)(f->kl + 1);
   if (usmem > 227 * 1024) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip panel update");
-  CK_CUDA(cudaFuncSetAttribute(k_gbtrf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem));
+  CK_CUDA(allow_max_dynamic_smem(k_gbtrf_update));
   const int64_t maxcols = f->kl + f->ku + 1;
   const unsigned ublocks = (unsigned)std::min<int64_t>(148, std::max<int64_t>(1, ceil_div(maxcols, 16)));
   for (int64_t j0 = 0; j0 < n; j0 += kLUBlock) {

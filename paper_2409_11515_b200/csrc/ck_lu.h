@@ -44,6 +44,25 @@ struct LUStatus {
 
 constexpr int kLUBlock = 32;  // panel width / solve block
 
+// Raise a kernel's dynamic shared-memory ceiling to everything the SM has
+// left beside its static shared memory. Always the same value, so concurrent
+// host threads (factorisations of an ensemble) never race a smaller ceiling
+// in under each other's launches.
+template <class K>
+inline cudaError_t allow_max_dynamic_smem(K* kernel) {
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(227 * 1024 - fa.sharedSizeBytes));
+}
+
+// Dynamic shared memory of a solve CTA, in doubles: R rings of ring_size,
+// R*32 dot scratch, then the TMA stage (16-byte aligned, stage_cap doubles).
+__host__ __device__ __forceinline__ int64_t stage_offset(int R, int ring_size) {
+  return (int64_t)R * ring_size + (int64_t)R * kLUBlock;
+}
+
 }  // namespace ck
 
 struct ck_lu_s {

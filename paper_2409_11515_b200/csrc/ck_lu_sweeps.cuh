@@ -629,12 +629,6 @@ __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring
   __syncthreads();
 }
 
-// Dynamic shared memory of a solve CTA, in doubles: R rings of ring_size,
-// R*32 dot scratch, then the stage (16-byte aligned, b.stage_cap doubles).
-__host__ __device__ __forceinline__ int64_t stage_offset(int R, int ring_size) {
-  return (int64_t)R * ring_size + (int64_t)R * kLUBlock;
-}
-
 // x := A^{-1} x (transpose = false) or A^{-T} x, for R right-hand sides, by the
 // calling CTA of kSweepThreads threads.
 template <int R>

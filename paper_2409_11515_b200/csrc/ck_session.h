@@ -57,17 +57,19 @@ struct LoopArgs {
 };
 
 // Arguments of the inverse-operator step (ck_inverse.cu).
+// Per-member arguments of the inverse step (one CTA per member; a batch of
+// S members keeps S of these in device memory).
 struct InvArgs {
   BandView b;
   int64_t n;
   int ring_size;
-  double2* PX;  // [3][n][R]
-  double2* MV;  // [n][R]
-  double* y;    // [R][n] work vector (solve in place)
-  ColState* st;
+  double2* PX;      // member's [n][R] slice of buffer 0; buffer k at PX + k * pstride
+  int64_t pstride;  // double2 elements per PX buffer (whole session)
+  double2* MV;      // [n][R]
+  double* y;        // [R][n] work vector (solve in place)
+  ColState* st;     // R columns
   Header* hdr;
   Params prm;
-  int half;  // 0 whole step, 1 apply half only, 2 transpose half only (observer)
 };
 
 }  // namespace ck
@@ -84,8 +86,10 @@ struct ck_session_s {
   Params prm{};
   LoopArgs args{};
   int kind = 0;              // 0: ExplicitOracle (ck_matrix), 1: InverseOracle (ck_lu)
-  ck_lu_s* lu = nullptr;
-  ck::InvArgs iargs{};
+  ck_lu_s* lu = nullptr;      // kind 1: the factors of member 0
+  std::vector<ck_lu_s*> lus;  // kind 1: factors per member
+  DBuf<ck::InvArgs> dargs;    // kind 1: per-member step arguments
+  size_t inv_smem = 0;        // kind 1: dynamic shared memory of the step CTA
   cudaStream_t stream = nullptr;
   int device = 0;
   int64_t n = 0;            // operator dimension (columns of A)

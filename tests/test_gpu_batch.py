@@ -70,3 +70,59 @@ def test_batch_session_witnesses(port):
                                                       seed=seeds[g * 2 + c]))
             assert e.value == pytest.approx(o.value, rel=1e-9)
             assert np.linalg.norm(m.to_dense() @ e.witness) == pytest.approx(e.value, rel=1e-12)
+
+
+# ---------------------------------------------------------- sigma_min side
+def _inv_members(port):
+    return [M.random_sparse(port, 60, 0.2, 4), configs.ensemble_member(0, 1, n=1000, bw=64),
+            M.row_scaled(M.laplacian2d(16), port, 2), configs.ensemble_member(1, 1, n=513, bw=40),
+            M.diag_matrix([3.0, 1.0, 1e-3])]
+
+
+def test_inverse_batch_matches_members(port):
+    # one CTA per member: every member's run is the single-member run
+    mem = _inv_members(port)
+    facs = batch.lu_factorize_many(mem, 1e-14, threads=4)
+    cfg = M.cfg(alpha=1e-2, max_iter=300, patience=300)
+    seeds = batch.member_seeds(len(mem), 5)
+    got = batch.inv_estimate_norm_batch(facs, cfg, restarts=3, seeds=seeds)
+    for m, f, g, sd in zip(mem, facs, got, seeds):
+        c = M.cfg(alpha=1e-2, max_iter=300, patience=300, seed=sd)
+        alone = ck.estimate_norm(ck.InverseOracle(f), c, 3)
+        assert g.value == alone.value and g.iterations == alone.iterations
+        o = port.estimate_norm_inverse(port.lu_factorize(m, 1e-14), c, 3)
+        assert g.iterations == o.iterations and g.converged == o.converged
+        assert g.value == pytest.approx(o.value, rel=1e-9)
+
+
+def test_inverse_batch_session_witnesses(port):
+    mem = _inv_members(port)[:3]
+    facs = batch.lu_factorize_many(mem, 1e-14, threads=1)
+    cfg = M.cfg(alpha=1e-2, max_iter=150, patience=150)
+    seeds = [21 + k for k in range(len(mem) * 2)]
+    s = batch.InverseBatchSession(facs, cfg, seeds)
+    assert s.run()
+    for g, (m, f) in enumerate(zip(mem, facs)):
+        for c in range(2):
+            e = s.member_result(g, c)
+            alone = ck.projected_adam(ck.InverseOracle(f), M.cfg(alpha=1e-2, max_iter=150,
+                                                                  patience=150, seed=seeds[g * 2 + c]))
+            assert e.value == alone.value and np.array_equal(e.witness, alone.witness)
+            assert np.linalg.norm(f.solve(e.witness)) == pytest.approx(e.value, rel=1e-12)
+
+
+def test_cond2_batch_matches_cond2(port):
+    # bench.hpp:435 per-matrix cond2 with member seeds; a singular member -> inf
+    dup = ck.SparseMatrix.from_triplets(3, 3, [(0, 0, 1.0), (0, 1, 2.0), (1, 0, 1.0), (1, 1, 2.0),
+                                               (2, 2, 5.0)])
+    mem = _inv_members(port)[:4] + [dup]
+    cfg = M.cfg(alpha=1e-2, max_iter=300, patience=300)
+    seeds = batch.member_seeds(len(mem), 3)
+    got = batch.cond2_batch(mem, cfg, restarts=2, seeds=seeds, wave=2, threads=2)
+    for m, r, sd in zip(mem[:4], got, seeds):
+        c = M.cfg(alpha=1e-2, max_iter=300, patience=300, seed=sd)
+        want = ck.cond2(m, c, restarts=2)
+        assert r.kappa == want.kappa
+        o = port.cond2(m, c, restarts=2)
+        assert r.kappa == pytest.approx(o["kappa"], rel=1e-9)
+    assert got[4].kappa == float("inf")
