@@ -38,6 +38,8 @@ typedef enum {
   CK_ERR_NUM_SINGULAR = 5,     /* NumericallySingular         lu.hpp:32-40 */
   CK_ERR_ZERO_RHS = 6,         /* ZeroRHS                     error_bounds.hpp:33-35 */
   CK_ERR_ZERO_SOLUTION = 7,    /* ZeroSolution                error_bounds.hpp:37-39 */
+  CK_ERR_ZERO_COLUMN = 8,      /* ZeroColumn                  sparse.hpp:29-33 */
+  CK_ERR_ZERO_ROW = 9,         /* ZeroRow                     sparse.hpp:35-39 */
   CK_ERR_CUDA = 20,            /* CUDA runtime failure (no reference analogue) */
   CK_ERR_NO_DEVICE = 21,       /* no sm_100 device visible */
   CK_ERR_UNSUPPORTED = 22,     /* input outside this build's limits (e.g. nnz >= 2^32) */
@@ -203,6 +205,21 @@ ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restart
                                ck_norm_result* res, double* witness);
 ck_status ck_session_create_inverse(ck_lu f, const ck_adam_cfg* cfg, const uint64_t* seeds,
                                     int32_t ncols, ck_session* out);
+/* Column / row scaling (sparse.hpp:244-313) on the device, for the `cond
+ * --scale column|row` path (condkit_cli.cpp:151-160). Norms are bit-identical
+ * to column_norms / two_norm per row. The CSR arrays are the ones `a` was
+ * uploaded from (host); va_out receives the scaled values in CSR order.
+ * ZeroColumn / ZeroRow report the first zero-norm index in *zero_index. */
+ck_status ck_column_norms(ck_matrix a, double* norms);
+ck_status ck_row_norms(ck_matrix a, double* norms);
+ck_status ck_column_scale(ck_matrix a, const int32_t* col_indices, const double* values,
+                          double* values_out, double* norms, int64_t* zero_index);
+ck_status ck_row_scale(ck_matrix a, const int64_t* row_offsets, const double* values,
+                       double* values_out, const double* b, double* b_out, double* norms,
+                       int64_t* zero_index);
+/* unscale_solution (sparse.hpp:287-293): x = y / d componentwise. */
+ck_status ck_unscale_solution(int64_t n, const double* y, const double* d, double* x);
+
 /* Ensembles on A^-1 (the sigma_min half of cond2 per member, config 5): nmem
  * independent factorisations, one device CTA per member per step. Column
  * k = g * ncols + c in ck_session_result; seeds has nmem * ncols entries.

@@ -50,6 +50,16 @@ struct ZeroRHS : std::invalid_argument {
 struct ZeroSolution : std::invalid_argument {
   ZeroSolution() : std::invalid_argument("candidate solution has zero norm") {}
 };
+struct ZeroColumn : std::runtime_error {
+  explicit ZeroColumn(std::size_t j)
+      : std::runtime_error("column " + std::to_string(j) + " has zero norm"), column(j) {}
+  std::size_t column;
+};
+struct ZeroRow : std::runtime_error {
+  explicit ZeroRow(std::size_t i)
+      : std::runtime_error("row " + std::to_string(i) + " has zero norm"), row(i) {}
+  std::size_t row;
+};
 struct DeviceError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -84,6 +94,8 @@ inline void check(ck_status s, int64_t col = -1, double piv = 0.0) {
     case CK_ERR_NUM_SINGULAR: throw NumericallySingular(m, static_cast<std::size_t>(col), piv);
     case CK_ERR_ZERO_RHS: throw ZeroRHS();
     case CK_ERR_ZERO_SOLUTION: throw ZeroSolution();
+    case CK_ERR_ZERO_COLUMN: throw ZeroColumn(static_cast<std::size_t>(col));
+    case CK_ERR_ZERO_ROW: throw ZeroRow(static_cast<std::size_t>(col));
     default: throw DeviceError(m);
   }
 }
@@ -334,6 +346,35 @@ inline BoundsReport verify_solution(const DeviceMatrix& a, const DenseVector& xh
   else
     rep.verdict = rep.tight_upper <= rep.threshold ? Verdict::accepted : Verdict::rejected;
   return rep;
+}
+
+// column_norms / column_scale / unscale_solution (sparse.hpp:244-293) with the
+// norms on the device. column_scale returns the scaled values in the CSR
+// order of `a` (the structure is unchanged) and the column norms D.
+template <class Csr, class = decltype(std::declval<const Csr&>().row_offsets())>
+DenseVector column_norms(const Csr& a) {
+  DeviceMatrix d(a);
+  DenseVector out(a.ncols());
+  detail::check(ck_column_norms(d.handle(), out.data()));
+  return out;
+}
+template <class Csr, class = decltype(std::declval<const Csr&>().row_offsets())>
+std::pair<DenseVector, DenseVector> column_scale_values(const Csr& a) {
+  DeviceMatrix d(a);
+  const auto& ci = a.col_indices();
+  std::vector<int32_t> c(ci.begin(), ci.end());
+  DenseVector vals(a.values().size()), norms(a.ncols());
+  int64_t zero = -1;
+  detail::check(ck_column_scale(d.handle(), c.data(), a.values().data(), vals.data(), norms.data(),
+                                &zero),
+                zero);
+  return {std::move(vals), std::move(norms)};
+}
+inline DenseVector unscale_solution(const DenseVector& y, const DenseVector& d) {
+  if (y.size() != d.size()) throw DimensionMismatch("unscale_solution: length mismatch");
+  DenseVector x(y.size());
+  detail::check(ck_unscale_solution(static_cast<int64_t>(y.size()), y.data(), d.data(), x.data()));
+  return x;
 }
 
 // Convenience overloads taking the CSR type directly (one upload per call).

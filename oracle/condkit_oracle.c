@@ -156,6 +156,34 @@ void cko_transpose_matvec(int64_t nrows, int64_t ncols, const int64_t* rp, const
     for (int64_t k = rp[i]; k < rp[i + 1]; ++k) y[ci[k]] += va[k] * x[i];
 }
 
+/* column_norms, sparse.hpp:244-268: per-column max magnitude, then the
+ * scaled sum of squares accumulated row by row. */
+void cko_column_norms(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
+                      const double* va, double* out) {
+  double* amax = (double*)calloc((size_t)(ncols ? ncols : 1), sizeof(double));
+  double* sums = (double*)calloc((size_t)(ncols ? ncols : 1), sizeof(double));
+  for (int64_t i = 0; i < nrows; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const double a = fabs(va[k]);
+      if (amax[ci[k]] < a) amax[ci[k]] = a;
+    }
+  for (int64_t i = 0; i < nrows; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int32_t j = ci[k];
+      if (amax[j] == 0.0) continue;
+      const double q = va[k] / amax[j];
+      sums[j] += q * q;
+    }
+  for (int64_t j = 0; j < ncols; ++j) out[j] = amax[j] * sqrt(sums[j]);
+  free(amax);
+  free(sums);
+}
+
+/* two_norm of every row (the row_scale factors, sparse.hpp:295-311). */
+void cko_row_norms(int64_t nrows, const int64_t* rp, const double* va, double* out) {
+  for (int64_t i = 0; i < nrows; ++i) out[i] = cko_two_norm(rp[i + 1] - rp[i], va + rp[i]);
+}
+
 /* ------------------------------------------------------------- lu.hpp */
 
 struct cko_lu {

@@ -70,6 +70,9 @@ double cko_dot(int64_t n, const double* a, const double* b);
 double cko_compensated_norm(int64_t n, const double* v);
 void cko_matvec(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
                 const double* va, const double* x, double* y);
+void cko_column_norms(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
+                      const double* va, double* out);
+void cko_row_norms(int64_t nrows, const int64_t* rp, const double* va, double* out);
 void cko_transpose_matvec(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
                           const double* va, const double* x, double* y);
 

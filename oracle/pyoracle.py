@@ -192,6 +192,28 @@ class Oracle:
                           ci.ctypes.data_as(_i32p), _d(va), _d(x), _d(y))
         return y
 
+    def generate_illconditioned(self, n: int, seed: int):
+        """Reference only: bench.hpp generate_illconditioned (default spec) as CSR."""
+        f = self._f("generate_illconditioned")
+        f.restype = C.c_int64
+        nnz = f(C.c_int64(n), C.c_uint64(seed), None, None, None)
+        rp, ci, va = np.zeros(n + 1, np.int64), np.zeros(nnz, np.int32), np.zeros(nnz)
+        f(C.c_int64(n), C.c_uint64(seed), rp.ctypes.data_as(_i64p), ci.ctypes.data_as(_i32p), _d(va))
+        return n, rp, ci, va
+
+    def column_norms(self, a) -> np.ndarray:
+        nr, nc, rp, ci, va = _csr(a)
+        out = np.zeros(nc)
+        self._f("column_norms")(C.c_int64(nr), C.c_int64(nc), rp.ctypes.data_as(_i64p),
+                                ci.ctypes.data_as(_i32p), _d(va), _d(out))
+        return out
+
+    def row_norms(self, a) -> np.ndarray:
+        nr, nc, rp, ci, va = _csr(a)
+        out = np.zeros(nr)
+        self._f("row_norms")(C.c_int64(nr), rp.ctypes.data_as(_i64p), _d(va), _d(out))
+        return out
+
     def transpose_matvec(self, a, x) -> np.ndarray:
         nr, nc, rp, ci, va = _csr(a)
         x = np.ascontiguousarray(x, np.float64)

@@ -13,6 +13,7 @@
 #include <condkit/lu.hpp>
 #include <condkit/rng.hpp>
 #include <condkit/sparse.hpp>
+#include <condkit/bench.hpp>
 
 #include <cstring>
 #include <random>
@@ -133,6 +134,35 @@ void ckref_transpose_matvec(int64_t nr, int64_t nc, const int64_t* rp, const int
                             const double* va, const double* x, double* y) {
   DenseVector r = transpose_matvec(to_sparse(nr, nc, rp, ci, va), DenseVector(x, x + nr));
   std::memcpy(y, r.data(), r.size() * sizeof(double));
+}
+
+// generate_illconditioned (bench.hpp:35-127) with the default spec at (n, seed):
+// the two-plateau matrix of acceptance criterion 5. rp == nullptr: nnz only.
+int64_t ckref_generate_illconditioned(int64_t n, uint64_t seed, int64_t* rp, int32_t* ci,
+                                      double* va) {
+  GeneratorSpec g;
+  g.n = (std::size_t)n;
+  g.seed = seed;
+  SparseMatrix a = generate_illconditioned(g);
+  if (rp) {
+    for (std::size_t i = 0; i <= a.nrows(); ++i) rp[i] = (int64_t)a.row_offsets()[i];
+    for (std::size_t k = 0; k < a.nnz(); ++k) {
+      ci[k] = (int32_t)a.col_indices()[k];
+      va[k] = a.values()[k];
+    }
+  }
+  return (int64_t)a.nnz();
+}
+
+void ckref_column_norms(int64_t nr, int64_t nc, const int64_t* rp, const int32_t* ci,
+                        const double* va, double* out) {
+  DenseVector r = column_norms(to_sparse(nr, nc, rp, ci, va));
+  std::memcpy(out, r.data(), r.size() * sizeof(double));
+}
+
+// row_scale's factors: two_norm of each row (sparse.hpp:295-311)
+void ckref_row_norms(int64_t nr, const int64_t* rp, const double* va, double* out) {
+  for (int64_t i = 0; i < nr; ++i) out[i] = two_norm(DenseVector(va + rp[i], va + rp[i + 1]));
 }
 
 int ckref_loss_explicit(int64_t nr, int64_t nc, const int64_t* rp, const int32_t* ci,

@@ -10,13 +10,14 @@ from .condest import (AdamConfig, AdamState, AdamStepInfo, ExplicitOracle, Gradi
                       projected_adam)
 from .errors import (CondkitError, DegenerateDirection, DeviceUnavailable, DimensionMismatch,
                      InvalidArgument, LogicError, NativeLibraryMissing, NumericallySingular,
-                     StructurallySingular, ZeroRHS, ZeroSolution)
+                     StructurallySingular, ZeroColumn, ZeroRHS, ZeroRow, ZeroSolution)
 from .error_bounds import (Bounds, BoundsReport, Verdict, VerifyOptions, kEpsMach, loose_bounds,
                            propagate_bound, singularity_bound, tight_bounds, verify_solution)
 from .inverse import (Cond2Result, InverseOracle, LUFactors, cond2, grad_inverse, inv_norm2,
                       lu_factorize, lu_solve, lu_transpose_solve)
 from .rng import mix_seed, random_unit_vector, random_unit_vectors
-from .sparse import DeviceMatrix, SparseMatrix, matvec, transpose_matvec
+from .sparse import (DeviceMatrix, ScalingDiagonal, SparseMatrix, column_norms, column_scale,
+                     matvec, row_norms, row_scale, transpose_matvec, unscale_solution)
 
 __all__ = [
     "AdamConfig", "AdamState", "AdamStepInfo", "ExplicitOracle", "GradientOracle",
@@ -28,5 +29,6 @@ __all__ = [
     "transpose_matvec", "Bounds", "BoundsReport", "Verdict", "VerifyOptions", "kEpsMach",
     "loose_bounds", "propagate_bound", "singularity_bound", "tight_bounds", "verify_solution",
     "Cond2Result", "InverseOracle", "LUFactors", "cond2", "grad_inverse", "inv_norm2",
-    "lu_factorize", "lu_solve", "lu_transpose_solve",
+    "lu_factorize", "lu_solve", "lu_transpose_solve", "ScalingDiagonal", "column_norms",
+    "column_scale", "row_norms", "row_scale", "unscale_solution", "ZeroColumn", "ZeroRow",
 ]

@@ -100,6 +100,11 @@ _SIGS = {
                                           C.c_int32, C.POINTER(C.c_void_p)]),
     "ck_estimate_norm_batch": (C.c_int, [C.c_void_p, i64p, C.c_int32, C.POINTER(AdamCfg), u64p,
                                          C.c_uint64, C.POINTER(NormResult)]),
+    "ck_column_norms": (C.c_int, [C.c_void_p, dp]),
+    "ck_row_norms": (C.c_int, [C.c_void_p, dp]),
+    "ck_column_scale": (C.c_int, [C.c_void_p, i32p, dp, dp, dp, i64p]),
+    "ck_row_scale": (C.c_int, [C.c_void_p, i64p, dp, dp, dp, dp, dp, i64p]),
+    "ck_unscale_solution": (C.c_int, [C.c_int64, dp, dp, dp]),
     "ck_session_create_inverse_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32,
                                                   C.POINTER(AdamCfg), u64p, C.c_int32,
                                                   C.POINTER(C.c_void_p)]),

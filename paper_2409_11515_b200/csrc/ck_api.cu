@@ -797,4 +797,75 @@ ck_status ck_inv_estimate_norm_batch(const ck_lu* lus, int32_t nmem, const ck_ad
   });
 }
 
+// ---------------------------------------------------------------- scaling
+ck_status ck_column_norms(ck_matrix a, double* norms) {
+  return guarded([&] {
+    ck_matrix_s* m = M(a);
+    DBuf<double> d(std::max<int64_t>(1, m->ncols));
+    matrix_norms(m, true, d.p);
+    CK_CUDA(cudaMemcpy(norms, d.p, sizeof(double) * m->ncols, cudaMemcpyDeviceToHost));
+  });
+}
+
+ck_status ck_row_norms(ck_matrix a, double* norms) {
+  return guarded([&] {
+    ck_matrix_s* m = M(a);
+    DBuf<double> d(std::max<int64_t>(1, m->nrows));
+    matrix_norms(m, false, d.p);
+    CK_CUDA(cudaMemcpy(norms, d.p, sizeof(double) * m->nrows, cudaMemcpyDeviceToHost));
+  });
+}
+
+// column_scale, sparse.hpp:271-284
+ck_status ck_column_scale(ck_matrix a, const int32_t* col_indices, const double* values,
+                          double* values_out, double* norms, int64_t* zero_index) {
+  return guarded([&] {
+    ck_matrix_s* m = M(a);
+    if (zero_index) *zero_index = -1;
+    DBuf<double> d(std::max<int64_t>(1, m->ncols));
+    matrix_norms(m, true, d.p);
+    std::vector<double> h((size_t)m->ncols);
+    CK_CUDA(cudaMemcpy(h.data(), d.p, sizeof(double) * m->ncols, cudaMemcpyDeviceToHost));
+    for (int64_t j = 0; j < m->ncols; ++j)
+      if (h[j] == 0.0) {
+        if (zero_index) *zero_index = j;
+        fail(CK_ERR_ZERO_COLUMN, "column " + std::to_string(j) + " has zero norm");
+      }
+    if (norms) std::memcpy(norms, h.data(), sizeof(double) * m->ncols);
+    csr_divide(m, true, nullptr, col_indices, values, d.p, values_out);
+  });
+}
+
+// row_scale, sparse.hpp:295-311
+ck_status ck_row_scale(ck_matrix a, const int64_t* row_offsets, const double* values,
+                       double* values_out, const double* b, double* b_out, double* norms,
+                       int64_t* zero_index) {
+  return guarded([&] {
+    ck_matrix_s* m = M(a);
+    if (zero_index) *zero_index = -1;
+    DBuf<double> d(std::max<int64_t>(1, m->nrows));
+    matrix_norms(m, false, d.p);
+    std::vector<double> h((size_t)m->nrows);
+    CK_CUDA(cudaMemcpy(h.data(), d.p, sizeof(double) * m->nrows, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < m->nrows; ++i)
+      if (h[i] == 0.0) {
+        if (zero_index) *zero_index = i;
+        fail(CK_ERR_ZERO_ROW, "row " + std::to_string(i) + " has zero norm");
+      }
+    if (norms) std::memcpy(norms, h.data(), sizeof(double) * m->nrows);
+    csr_divide(m, false, row_offsets, nullptr, values, d.p, values_out);
+    if (b && b_out) vector_divide(m->nrows, b, h.data(), b_out, m->stream);
+  });
+}
+
+ck_status ck_unscale_solution(int64_t n, const double* y, const double* d, double* x) {
+  return guarded([&] {
+    if (n < 0) fail(CK_ERR_INVALID_ARGUMENT, "negative length");
+    int cnt = 0;
+    if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0) fail(CK_ERR_NO_DEVICE, "no CUDA device");
+    cudaStream_t st = nullptr;
+    vector_divide(n, y, d, x, st);
+  });
+}
+
 }  // extern "C"

@@ -24,6 +24,12 @@ void residual_norms(ck_matrix_s* m, const double* x, const double* b, double* rn
 double loss_explicit_dev(ck_matrix_s* m, const double* x, bool* degenerate);
 void grad_explicit_dev(ck_matrix_s* m, const double* x, double* g, bool* degenerate);
 
+// Column / row norms and scalings (ck_scale.cu).
+void matrix_norms(ck_matrix_s* m, bool column, double* out_dev);
+void csr_divide(ck_matrix_s* m, bool column, const int64_t* h_rp, const int32_t* h_ci,
+                const double* h_va, const double* d_norms, double* h_out);
+void vector_divide(int64_t n, const double* h_y, const double* h_d, double* h_out, cudaStream_t st);
+
 // Host mirror of random_unit_vector (rng.hpp:68-77) on a caller-owned engine
 // state; bit-identical to the reference, Box-Muller transform multithreaded.
 struct Mt64;

@@ -49,6 +49,24 @@ class ZeroSolution(InvalidArgument):
     status = 7
 
 
+class ZeroColumn(CondkitError, RuntimeError):
+    """column_scale on an empty or zero-norm column (sparse.hpp:29-33)."""
+    status = 8
+
+    def __init__(self, msg: str = "", column: int = -1):
+        super().__init__(msg)
+        self.column = column
+
+
+class ZeroRow(CondkitError, RuntimeError):
+    """row_scale on a zero-norm row (sparse.hpp:35-39)."""
+    status = 9
+
+    def __init__(self, msg: str = "", row: int = -1):
+        super().__init__(msg)
+        self.row = row
+
+
 class CudaError(CondkitError, RuntimeError):
     status = 20
 
@@ -75,7 +93,8 @@ class DegenerateDirection(CondkitError, RuntimeError):
 
 _BY_STATUS = {c.status: c for c in (DimensionMismatch, InvalidArgument, LogicError,
                                      StructurallySingular, NumericallySingular, ZeroRHS,
-                                     ZeroSolution, CudaError, DeviceUnavailable, Unsupported,
+                                     ZeroSolution, ZeroColumn, ZeroRow, CudaError,
+                                     DeviceUnavailable, Unsupported,
                                      DeviceOutOfMemory)}
 
 

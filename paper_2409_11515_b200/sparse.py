@@ -17,7 +17,7 @@ import weakref
 import numpy as np
 
 from . import _lib
-from .errors import DimensionMismatch, Unsupported
+from .errors import DimensionMismatch, InvalidArgument, Unsupported, ZeroColumn, ZeroRow
 
 
 class SparseMatrix:
@@ -198,3 +198,89 @@ def transpose_matvec(a: SparseMatrix, x) -> np.ndarray:
         raise DimensionMismatch(
             f"transpose_matvec: vector length {np.asarray(x).size} != nrows {a.nrows}")
     return a.device().transpose_matvec(x)
+
+
+# ------------------------------------------------------------------ scaling
+class ScalingDiagonal:
+    """Positive finite diagonal scaling factors (sparse.hpp:154-171)."""
+
+    def __init__(self, factors):
+        f = np.ascontiguousarray(factors, np.float64)
+        bad = np.flatnonzero(~((f > 0.0) & np.isfinite(f)))
+        if bad.size:
+            raise InvalidArgument(f"scaling factor {int(bad[0])} is not positive and finite")
+        self._f = f
+
+    def __len__(self) -> int:
+        return self._f.size
+
+    def size(self) -> int:
+        return self._f.size
+
+    def __getitem__(self, i):
+        return self._f[i]
+
+    @property
+    def factors(self) -> np.ndarray:
+        return self._f
+
+
+def column_norms(a: SparseMatrix) -> np.ndarray:
+    """Euclidean norm of every column on the device (sparse.hpp:244-268), bit-identical."""
+    out = np.empty(a.ncols)
+    _lib.check(_lib.load().ck_column_norms(a.device().handle, _lib.dptr(out)), "column_norms")
+    return out
+
+
+def row_norms(a: SparseMatrix) -> np.ndarray:
+    """two_norm of every row on the device (the row_scale factors)."""
+    out = np.empty(a.nrows)
+    _lib.check(_lib.load().ck_row_norms(a.device().handle, _lib.dptr(out)), "row_norms")
+    return out
+
+
+def column_scale(a: SparseMatrix):
+    """(A D^-1, D) with D the column norms (sparse.hpp:270-284); ZeroColumn on the
+    first zero-norm column."""
+    vals = np.empty(a.nnz)
+    norms = np.empty(a.ncols)
+    zi = C.c_int64(-1)
+    st = _lib.load().ck_column_scale(a.device().handle, _lib.i32ptr(a.col_indices),
+                                     _lib.dptr(a.values), _lib.dptr(vals), _lib.dptr(norms),
+                                     C.byref(zi))
+    if st == ZeroColumn.status:
+        raise ZeroColumn(_lib.load().ck_last_error().decode(), column=zi.value)
+    _lib.check(st, "column_scale")
+    scaled = SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices, vals, validate=False)
+    return scaled, ScalingDiagonal(norms)
+
+
+def row_scale(a: SparseMatrix, b):
+    """(D_r^-1 A, D_r^-1 b) with D_r the row norms (sparse.hpp:295-311); ZeroRow on
+    the first zero-norm row."""
+    b = np.ascontiguousarray(b, np.float64)
+    if b.size != a.nrows:
+        raise DimensionMismatch("row_scale: rhs length != nrows")
+    vals = np.empty(a.nnz)
+    bs = np.empty(a.nrows)
+    norms = np.empty(a.nrows)
+    zi = C.c_int64(-1)
+    st = _lib.load().ck_row_scale(a.device().handle, _lib.i64ptr(a.row_offsets),
+                                  _lib.dptr(a.values), _lib.dptr(vals), _lib.dptr(b),
+                                  _lib.dptr(bs), _lib.dptr(norms), C.byref(zi))
+    if st == ZeroRow.status:
+        raise ZeroRow(_lib.load().ck_last_error().decode(), row=zi.value)
+    _lib.check(st, "row_scale")
+    return SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices, vals, validate=False), bs
+
+
+def unscale_solution(y, d: ScalingDiagonal) -> np.ndarray:
+    """x = D^-1 y componentwise (sparse.hpp:286-293)."""
+    y = np.ascontiguousarray(y, np.float64)
+    f = d.factors if isinstance(d, ScalingDiagonal) else np.ascontiguousarray(d, np.float64)
+    if y.size != f.size:
+        raise DimensionMismatch("unscale_solution: length mismatch")
+    x = np.empty(y.size)
+    _lib.check(_lib.load().ck_unscale_solution(y.size, _lib.dptr(y), _lib.dptr(f), _lib.dptr(x)),
+               "unscale_solution")
+    return x

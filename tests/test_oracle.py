@@ -59,6 +59,19 @@ def test_spmv_bitwise_port_vs_ref(port, ref):
     assert np.array_equal(port.transpose_matvec(a, x), ref.transpose_matvec(a, x))
 
 
+def test_column_and_row_norms_port_vs_ref(port, ref):
+    # column_norms (sparse.hpp:244-268) and row two_norms (row_scale factors)
+    mats = [M.random_sparse(port, 50, 0.2, 3), M.row_scaled(M.laplacian2d(12), port, 4),
+            M.SparseMatrix.from_triplets(3, 3, [(0, 0, 1.0), (1, 1, 1.0), (2, 2, 0.0)])]
+    n, rp, ci, va = ref.generate_illconditioned(60, 11)
+    mats.append(M.SparseMatrix(n, n, rp, ci, va))
+    for a in mats:
+        assert np.array_equal(port.column_norms(a), ref.column_norms(a))
+        assert np.array_equal(port.row_norms(a), ref.row_norms(a))
+    a = M.SparseMatrix.from_triplets(2, 2, [(0, 0, 2.0), (1, 1, 3.0)])  # test_sparse.cpp:102-106
+    assert list(port.column_norms(a)) == [2.0, 3.0]
+
+
 @pytest.mark.parametrize("seed", [1, 7])
 def test_projected_adam_bitwise_port_vs_ref(port, ref, seed):
     a = M.row_scaled(M.laplacian2d(12), port, seed)
