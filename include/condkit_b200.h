@@ -220,6 +220,53 @@ ck_status ck_row_scale(ck_matrix a, const int64_t* row_offsets, const double* va
 /* unscale_solution (sparse.hpp:287-293): x = y / d componentwise. */
 ck_status ck_unscale_solution(int64_t n, const double* y, const double* d, double* x);
 
+/* Row-block partition of one operator across ranks (replaces
+ * running projected_adam on the whole matrix, condest.hpp:184-297, for grids
+ * that are split across GPUs). Rank p owns global rows/columns
+ * [g0, g0 + n_loc). Its extended local operator (CSR, ext_rows x ext_cols)
+ * orders both index spaces by global index as [left halo | own block, padded
+ * to whole 256-row tiles | right halo]; the own block is tiles [tile0, tile1).
+ * Rows: the own rows of A (complete) and the halo rows -- rows of A outside
+ * the block with entries in own columns, restricted to those columns.
+ * Halo lists (per peer q, offsets [q], [q+1] into the index arrays):
+ *   xs: own columns q needs (extended column positions), xr: where the
+ *   values from q land (extended halo column positions), ys/yr: the same for
+ *   rows (y' = A x~). ext_global[e]: global column of extended position e, or
+ *   -1 for padding (start vectors are drawn globally and sliced).
+ * nccl_id != NULL: NCCL backend, one rank per process (ck_dist_nccl_id on
+ * rank 0, broadcast by the caller). nccl_id == NULL: every rank in this
+ * process on the current device, stepped in lockstep. */
+typedef struct ck_dist_part {
+  int64_t n_global;
+  int64_t tile0, tile1;
+  int64_t ext_rows, ext_cols;
+  const int64_t* rp;
+  const int32_t* ci;
+  const double* va;
+  const int64_t* xs_off;
+  const int32_t* xs_idx;
+  const int64_t* xr_off;
+  const int32_t* xr_idx;
+  const int64_t* ys_off;
+  const int32_t* ys_idx;
+  const int64_t* yr_off;
+  const int32_t* yr_idx;
+  const int64_t* ext_global;
+} ck_dist_part;
+typedef struct ck_dist_s* ck_dist;
+ck_status ck_dist_nccl_id(void* id128);
+ck_status ck_dist_create(const ck_dist_part* parts, int32_t nparts, int32_t rank0, int32_t nranks,
+                         const void* nccl_id, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                         int32_t ncols, ck_dist* out);
+ck_status ck_dist_run(ck_dist d, uint64_t max_steps, int32_t* finished);
+/* device time of `steps` iterations (graph replay on the NCCL backend) */
+ck_status ck_dist_time(ck_dist d, uint64_t steps, double* ms);
+/* NormEstimate of restart column col; witness = local rank `part`'s
+ * extended-order slice (ext_cols doubles), NULL to skip. Collective. */
+ck_status ck_dist_result(ck_dist d, int32_t col, int32_t part, ck_norm_result* res,
+                         double* witness);
+ck_status ck_dist_free(ck_dist d);
+
 /* Ensembles on A^-1 (the sigma_min half of cond2 per member, config 5): nmem
  * independent factorisations, one device CTA per member per step. Column
  * k = g * ncols + c in ck_session_result; seeds has nmem * ncols entries.

@@ -100,6 +100,13 @@ _SIGS = {
                                           C.c_int32, C.POINTER(C.c_void_p)]),
     "ck_estimate_norm_batch": (C.c_int, [C.c_void_p, i64p, C.c_int32, C.POINTER(AdamCfg), u64p,
                                          C.c_uint64, C.POINTER(NormResult)]),
+    "ck_dist_nccl_id": (C.c_int, [C.c_void_p]),
+    "ck_dist_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                 C.POINTER(AdamCfg), u64p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "ck_dist_run": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32)]),
+    "ck_dist_time": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_double)]),
+    "ck_dist_result": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(NormResult), dp]),
+    "ck_dist_free": (C.c_int, [C.c_void_p]),
     "ck_column_norms": (C.c_int, [C.c_void_p, dp]),
     "ck_row_norms": (C.c_int, [C.c_void_p, dp]),
     "ck_column_scale": (C.c_int, [C.c_void_p, i32p, dp, dp, dp, i64p]),

@@ -62,7 +62,7 @@ __device__ __forceinline__ void unit_range(const LoopArgs& a, int unit, int tile
                                            int& t0, int& tend, int& stride, int& u0, int& u1) {
   if (a.S == 1) {
     seg = 0;
-    t0 = unit;
+    t0 = a.tile_base + unit;
     tend = tiles;
     stride = gridDim.x;
     u0 = 0;
@@ -80,6 +80,54 @@ __device__ __forceinline__ void unit_range(const LoopArgs& a, int unit, int tile
 // x~ from a stored (x, delta) pair: x - (delta - r x)  (:232, :240)
 __device__ __forceinline__ double xtilde(double2 p, double rad) {
   return __dsub_rn(p.x, __dsub_rn(p.y, __dmul_rn(rad, p.x)));
+}
+
+// Control step after the apply sweep (condest.hpp:251-275 via control_apply)
+// from the global scalars res[r] = {||x~||, ||y'||, x.delta, ||delta||}; one
+// thread. Shared by the fused kernel and the partition combine kernel.
+template <int R, bool OBS>
+__device__ __forceinline__ void control_tail_apply(ColState* sts, Header* hdr, const Params& prm,
+                                                   const double (*res)[4]) {
+  int needT = 0, nwait = 0, ndone = 0;
+  for (int r = 0; r < R; ++r) {
+    ColState* s = sts + r;
+    const int ph = s->phase;
+    if (ph == PH_PRO || ph == PH_APPLY) {
+      if (OBS && ph == PH_APPLY) {
+        s->obs_xd = res[r][2];
+        s->obs_dn = res[r][3];
+      }
+      control_apply(s, &prm, res[r][0], res[r][1]);
+    }
+    needT |= s->phase == PH_GRAD;
+    nwait += s->phase == PH_WAIT;
+    ndone += s->phase == PH_DONE;
+  }
+  hdr->needT = needT;
+  hdr->needA = 0;
+  hdr->nwait = nwait;
+  hdr->ndone = ndone;
+}
+
+// After the transpose sweep: publish r = x.delta (condest.hpp:231) and move
+// every gradient column on to its apply half; one thread.
+template <int R>
+__device__ __forceinline__ void control_tail_transpose(ColState* sts, Header* hdr, const double* rad) {
+  int needA = 0;
+  for (int r = 0; r < R; ++r) {
+    ColState* s = sts + r;
+    if (s->phase == PH_GRAD) {
+      s->rad = rad[r];
+      if (s->mat) {
+        s->cur = s->nxt;
+        s->pend = 0;
+      }
+      s->phase = PH_APPLY;
+    }
+    needA |= s->phase == PH_APPLY;
+  }
+  hdr->needA = needA;
+  hdr->needT = 0;
 }
 
 template <int R, bool OBS, int U = (R == 1 ? 8 : 4)>
@@ -200,7 +248,8 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
   }
   if (!elect_last_block(&hdr->cntA, (unsigned)(u1 - u0))) return;
 
-  // Last CTA (of this member): fixed-order merge of its partials, then control.
+  // Last CTA (of this member): fixed-order merge of its partials, then control
+  // (or, for a partition rank, publish the merged partials).
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     DD d = dd_zero();
@@ -222,33 +271,26 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
       e2 = block_es(e2, s_h, s_e, s_f);
     }
     if (threadIdx.x == 0) {
-      s_res[r][0] = sqrt(__dadd_rn(d.hi, d.lo));
-      s_res[r][1] = es_norm(e);
-      s_res[r][2] = x2;
-      s_res[r][3] = es_norm(e2);
-    }
-  }
-  if (threadIdx.x == 0) {
-    int needT = 0, nwait = 0, ndone = 0;
-    for (int r = 0; r < R; ++r) {
-      ColState* s = sts + r;
-      const int ph = s->phase;
-      if (ph == PH_PRO || ph == PH_APPLY) {
-        if (OBS && ph == PH_APPLY) {
-          s->obs_xd = s_res[r][2];
-          s->obs_dn = s_res[r][3];
-        }
-        control_apply(s, &a.prm, s_res[r][0], s_res[r][1]);
+      if (a.dist) {
+        double* q = a.rank_part + r * kPA;
+        q[0] = d.hi;
+        q[1] = d.lo;
+        q[2] = e.s;
+        q[3] = (double)e.e;
+        q[4] = (double)e.flags;
+        q[5] = x2;
+        q[6] = e2.s;
+        q[7] = (double)e2.e;
+        q[8] = (double)e2.flags;
+      } else {
+        s_res[r][0] = sqrt(__dadd_rn(d.hi, d.lo));
+        s_res[r][1] = es_norm(e);
+        s_res[r][2] = x2;
+        s_res[r][3] = es_norm(e2);
       }
-      needT |= s->phase == PH_GRAD;
-      nwait += s->phase == PH_WAIT;
-      ndone += s->phase == PH_DONE;
     }
-    hdr->needT = needT;
-    hdr->needA = 0;
-    hdr->nwait = nwait;
-    hdr->ndone = ndone;
   }
+  if (threadIdx.x == 0 && !a.dist) control_tail_apply<R, OBS>(sts, hdr, a.prm, s_res);
 }
 
 template <int R, int U = (R <= 2 ? 8 : 4)>
@@ -354,25 +396,50 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     for (int u = u0 + threadIdx.x; u < u1; u += kTile)
       s = __dadd_rn(s, __ldcg(a.partT + (int64_t)u * R + r));
     s = block_sum(s, s_h);
-    if (threadIdx.x == 0) s_res[r] = s;
-  }
-  if (threadIdx.x == 0) {
-    int needA = 0;
-    for (int r = 0; r < R; ++r) {
-      ColState* s = sts + r;
-      if (s->phase == PH_GRAD) {
-        s->rad = s_res[r];
-        if (s->mat) {
-          s->cur = s->nxt;
-          s->pend = 0;
-        }
-        s->phase = PH_APPLY;
-      }
-      needA |= s->phase == PH_APPLY;
+    if (threadIdx.x == 0) {
+      if (a.dist)
+        a.rank_part[R * kPA + r] = s;  // after the apply partials
+      else
+        s_res[r] = s;
     }
-    hdr->needA = needA;
-    hdr->needT = 0;
   }
+  if (threadIdx.x == 0 && !a.dist) control_tail_transpose<R>(sts, hdr, s_res);
+}
+
+// ------------------------------------------------ row-block partition combine
+// Every rank merges the gathered per-rank partials in rank order (identical
+// on all ranks, so every rank takes the same control decisions), then runs the
+// control step of the single-device kernels. One thread; g holds per rank the
+// R*kPA apply partials followed by the R transpose partials.
+template <int R>
+__global__ void k_dist_control_apply(LoopArgs a, const double* __restrict__ g, int nranks) {
+  if (threadIdx.x != 0 || !a.hdr->needA) return;
+  double res[R][4];
+  for (int r = 0; r < R; ++r) {
+    DD d = dd_zero();
+    ES e = es_zero();
+    for (int q = 0; q < nranks; ++q) {
+      const double* p = g + (int64_t)q * R * (kPA + 1) + r * kPA;
+      dd_merge(d, DD{p[0], p[1]});
+      es_merge(e, ES{p[2], (int)p[3], (int)p[4]});
+    }
+    res[r][0] = sqrt(__dadd_rn(d.hi, d.lo));
+    res[r][1] = es_norm(e);
+    res[r][2] = res[r][3] = 0.0;
+  }
+  control_tail_apply<R, false>(a.st, a.hdr, a.prm, res);
+}
+
+template <int R>
+__global__ void k_dist_control_transpose(LoopArgs a, const double* __restrict__ g, int nranks) {
+  if (threadIdx.x != 0 || !a.hdr->needT) return;
+  double rad[R];
+  for (int r = 0; r < R; ++r) {
+    double s = 0.0;
+    for (int q = 0; q < nranks; ++q) s = __dadd_rn(s, g[(int64_t)q * R * (kPA + 1) + R * kPA + r]);
+    rad[r] = s;
+  }
+  control_tail_transpose<R>(a.st, a.hdr, rad);
 }
 
 // x_{t+1} = x~ / N from (x, delta) pairs, into a plain vector (epilogue / observer).
@@ -420,7 +487,7 @@ static void launch_inv_half(ck_session_s* s, int half, cudaStream_t st) {
   launch_inv_step(s->dargs.p, s->S, s->R, s->inv_smem, half, st);
 }
 
-static void launch_apply_only(ck_session_s* s, cudaStream_t st) {
+void launch_apply_only(ck_session_s* s, cudaStream_t st) {
   if (s->kind == 1) {
     launch_inv_half(s, 1, st);
     return;
@@ -433,7 +500,7 @@ static void launch_apply_only(ck_session_s* s, cudaStream_t st) {
   }
 }
 
-static void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
+void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
   if (s->kind == 1) {
     launch_inv_half(s, 2, st);
     return;
@@ -447,7 +514,11 @@ static void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
   }
 }
 
-static void launch_step(ck_session_s* s, cudaStream_t st) {
+void launch_step(ck_session_s* s, cudaStream_t st) {
+  if (s->dist) {
+    dist_step(s, st);
+    return;
+  }
   if (s->kind == 1) {
     launch_inv_half(s, 0, st);
     return;
@@ -466,7 +537,37 @@ static int occ_transpose(int R) {
                   : Occ<4>::transpose;
 }
 
-static void pull_state(ck_session_s* s) {
+// Partition ranks: own tiles [t0, t1) of the extended local operator.
+void session_set_tiles(ck_session_s* s, int t0, int t1) {
+  LoopArgs& a = s->args;
+  a.tile_base = t0;
+  a.tiles_A = a.tiles_T = t1;
+  a.units_A = std::max(1, std::min(t1 - t0, 148 * occ_apply(s->R)));
+  a.units_T = std::max(1, std::min(t1 - t0, 148 * occ_transpose(s->R)));
+}
+
+void launch_dist_control(ck_session_s* s, bool apply, const double* gathered, int nranks,
+                         cudaStream_t st) {
+  const LoopArgs& a = s->args;
+#define CK_DC(RR)                                                                   \
+  case RR:                                                                          \
+    if (apply)                                                                      \
+      k_dist_control_apply<RR><<<1, 32, 0, st>>>(a, gathered, nranks);             \
+    else                                                                            \
+      k_dist_control_transpose<RR><<<1, 32, 0, st>>>(a, gathered, nranks);         \
+    break;
+  switch (s->R) {
+    CK_DC(1)
+    CK_DC(2)
+    CK_DC(3)
+    CK_DC(4)
+  }
+#undef CK_DC
+}
+
+int partial_words(int R) { return R * (kPA + 1); }
+
+void pull_state(ck_session_s* s) {
   cudaStream_t st = s->stream;
   CK_CUDA(cudaMemcpyAsync(s->h_st, s->st.p, sizeof(ColState) * s->S * s->R,
                           cudaMemcpyDeviceToHost, st));
@@ -474,7 +575,7 @@ static void pull_state(ck_session_s* s) {
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
-static void push_state(ck_session_s* s) {
+void push_state(ck_session_s* s) {
   cudaStream_t st = s->stream;
   CK_CUDA(cudaMemcpyAsync(s->st.p, s->h_st, sizeof(ColState) * s->S * s->R,
                           cudaMemcpyHostToDevice, st));
@@ -482,20 +583,20 @@ static void push_state(ck_session_s* s) {
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
-static int64_t total_done(const ck_session_s* s) {
+int64_t total_done(const ck_session_s* s) {
   int64_t d = 0;
   for (int g = 0; g < s->S; ++g) d += s->h_hdr[g].ndone;
   return d;
 }
 
-static bool any_wait(const ck_session_s* s) {
+bool any_wait(const ck_session_s* s) {
   for (int g = 0; g < s->S; ++g)
     if (s->h_hdr[g].nwait > 0) return true;
   return false;
 }
 
 // (x, delta) pairs of buffer b, column c: element i at col_buf(...)[i * R]
-static double2* col_buf(ck_session_s* s, int b, int c) {
+double2* col_buf(ck_session_s* s, int b, int c) {
   return s->PX.p + (int64_t)b * s->npad * s->R + c;
 }
 
@@ -516,7 +617,7 @@ static void to_internal(ck_session_s* s, int g, const double* host, double* dst,
 }
 
 // internal plain vector -> host vector of member g (original order)
-static void to_host(ck_session_s* s, int g, const double* src, double* host, cudaStream_t st) {
+void to_host(ck_session_s* s, int g, const double* src, double* host, cudaStream_t st) {
   const int64_t off = s->seg_off[g], pad = s->seg_pad[g];
   const double* out = src + off;
   if (s->perm) {
@@ -530,7 +631,7 @@ static void to_host(ck_session_s* s, int g, const double* src, double* host, cud
 
 // Upload a fresh start vector for member g, column c into buffer b: (x,
 // delta = 0) pairs in the internal (permuted) space, m = v = 0.
-static void load_start(ck_session_s* s, int g, int c, int b, const double* x) {
+void load_start(ck_session_s* s, int g, int c, int b, const double* x) {
   cudaStream_t st = s->stream;
   const int64_t off = s->seg_off[g], pad = s->seg_pad[g];
   double* plain = s->tmp.p + s->thalf;
@@ -543,14 +644,29 @@ static void load_start(ck_session_s* s, int g, int c, int b, const double* x) {
 
 // restart(), condest.hpp:201-207: the next vector of the column's own stream,
 // m = v = 0, bias powers reset; x_min and the patience counters are kept.
-static void service_restarts(ck_session_s* s) {
+// Next start vector of column k (member g) into `out` (the member's
+// original-order vector): random_unit_vector from the column's own stream; a
+// partition rank draws the global vector and keeps its extended slice.
+static void draw_start(ck_session_s* s, int k, int g, double* out) {
+  if (!s->dist) {
+    random_unit_vector_host(&s->gens[k], s->seg_n[g], out);
+    return;
+  }
+  const DistPart& d = *s->dist;
+  std::vector<double> full((size_t)d.n_global);
+  random_unit_vector_host(&s->gens[k], d.n_global, full.data());
+  for (size_t e = 0; e < d.ext_global.size(); ++e)
+    out[e] = d.ext_global[e] >= 0 ? full[(size_t)d.ext_global[e]] : 0.0;
+}
+
+void service_restarts(ck_session_s* s) {
   bool any = false;
   for (int g = 0; g < s->S; ++g) {
     for (int c = 0; c < s->R; ++c) {
       const int k = g * s->R + c;
       ColState& cs = s->h_st[k];
       if (cs.phase != PH_WAIT) continue;
-      random_unit_vector_host(&s->gens[k], s->seg_n[g], s->hx.data());
+      draw_start(s, k, g, s->hx.data());
       const int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
       load_start(s, g, c, b, s->hx.data());
       cs.cur = b;
@@ -571,7 +687,8 @@ static void service_restarts(ck_session_s* s) {
   }
 }
 
-static void build_graph(ck_session_s* s, int steps) {
+void build_graph(ck_session_s* s, int steps) {
+  if (s->dist && !s->dist->nccl) return;  // in-process partitions: the group drives every step
   cudaStream_t st = s->stream;
   cudaGraph_t g;
   CK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -583,7 +700,7 @@ static void build_graph(ck_session_s* s, int steps) {
 }
 
 // Common part of session creation: state buffers, x0 per (member, column), graphs.
-static void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t* seeds,
+void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t* seeds,
                                 int64_t ywords, double bytes_per_step) {
   cudaStream_t st = s->stream;
   const int R = s->R, S = s->S;
@@ -602,7 +719,7 @@ static void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const u
   for (int g = 0; g < S; ++g) {
     for (int c = 0; c < R; ++c) {
       s->gens.emplace_back(seeds[g * R + c]);
-      random_unit_vector_host(&s->gens.back(), s->seg_n[g], s->hx.data());  // x0, rng.hpp:68-77
+      draw_start(s, g * R + c, g, s->hx.data());  // x0, rng.hpp:68-77
       load_start(s, g, c, 0, s->hx.data());
       CK_CUDA(cudaStreamSynchronize(st));  // hx is reused for the next upload
       ColState cs{};
@@ -632,8 +749,8 @@ static void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const u
 // Explicit-operator session over S >= 1 square-or-rectangular members packed
 // block-diagonally in A (member g occupies rows/cols [off_g, off_g + n_g) with
 // off_g = sum of round_up(n_h, 256), h < g). S == 1 is a single operator.
-static void session_create_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
-                                    const uint64_t* seeds, int R, const int64_t* seg_n, int S) {
+void session_setup_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg, int R,
+                            const int64_t* seg_n, int S) {
   if (R < 1 || R > kMaxCols) fail(CK_ERR_INVALID_ARGUMENT, "session columns must be 1..4");
   if (A->ncols == 0) fail(CK_ERR_INVALID_ARGUMENT, "projected_adam: zero-dimensional operator");
   if (S < 1) fail(CK_ERR_INVALID_ARGUMENT, "at least one member");
@@ -722,6 +839,15 @@ static void session_create_explicit(ck_session_s* s, ck_matrix_s* A, const ck_ad
   a.partT = s->partT.p;
   a.st = s->st.p;
   a.hdr = s->hdr.p;
+  a.dist = 0;
+  a.rank_part = nullptr;
+  a.tile_base = 0;
+}
+
+static void session_create_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg,
+                                    const uint64_t* seeds, int R, const int64_t* seg_n, int S) {
+  session_setup_explicit(s, A, cfg, R, seg_n, S);
+  const int64_t yw = std::max(s->args.nr_pad, s->args.nc_pad) * R;
   const double bytes_per_step = 24.0 * (double)A->nnz + 100.0 * (double)A->ncols * R;
   session_init_common(s, cfg, seeds, yw, bytes_per_step);
 }
@@ -931,9 +1057,13 @@ void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness
   res->_pad = 0;
   if (std::isfinite(cs.loss_min)) {
     res->value = std::exp(-cs.loss_min);
-    const double chk = op_norm(s, g, xbest, st);
-    if (!(std::fabs(chk - res->value) <= 1e-12 * std::max(res->value, chk)))
-      fail(CK_ERR_LOGIC, "norm estimate does not match ||Op witness||");
+    if (s->dist) {
+      dist_op_norm(s, xbest, st);  // this rank's part; ck_dist checks the combined norm
+    } else {
+      const double chk = op_norm(s, g, xbest, st);
+      if (!(std::fabs(chk - res->value) <= 1e-12 * std::max(res->value, chk)))
+        fail(CK_ERR_LOGIC, "norm estimate does not match ||Op witness||");
+    }
   } else {
     res->value = 0.0;
     res->converged = 0;

@@ -868,4 +868,52 @@ ck_status ck_unscale_solution(int64_t n, const double* y, const double* d, doubl
   });
 }
 
+// ------------------------------------------------------ row-block partitions
+ck_status ck_dist_nccl_id(void* id128) {
+  return guarded([&] { dist_nccl_id(id128); });
+}
+
+ck_status ck_dist_create(const ck_dist_part* parts, int32_t nparts, int32_t rank0, int32_t nranks,
+                         const void* nccl_id, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                         int32_t ncols, ck_dist* out) {
+  return guarded([&] {
+    check_cfg(cfg);
+    ck_dist_s* D = dist_new();
+    try {
+      dist_create(D, parts, nparts, rank0, nranks, nccl_id, cfg, seeds, ncols);
+    } catch (...) {
+      dist_free(D);
+      throw;
+    }
+    *out = D;
+  });
+}
+
+ck_status ck_dist_run(ck_dist d, uint64_t max_steps, int32_t* finished) {
+  return guarded([&] {
+    if (!d) fail(CK_ERR_INVALID_ARGUMENT, "dist handle is NULL");
+    dist_run(d, max_steps, finished);
+  });
+}
+
+ck_status ck_dist_time(ck_dist d, uint64_t steps, double* ms) {
+  return guarded([&] {
+    if (!d) fail(CK_ERR_INVALID_ARGUMENT, "dist handle is NULL");
+    *ms = dist_time(d, steps);
+  });
+}
+
+ck_status ck_dist_result(ck_dist d, int32_t col, int32_t part, ck_norm_result* res, double* witness) {
+  return guarded([&] {
+    if (!d) fail(CK_ERR_INVALID_ARGUMENT, "dist handle is NULL");
+    dist_result(d, col, part, res, witness);
+  });
+}
+
+ck_status ck_dist_free(ck_dist d) {
+  return guarded([&] {
+    if (d) dist_free(d);
+  });
+}
+
 }  // extern "C"

@@ -10,6 +10,8 @@
 #include "ck_common.h"
 #include "ck_lu.h"
 
+struct ck_session_s;
+
 namespace ck {
 
 enum Phase : int32_t { PH_PRO = 0, PH_GRAD = 1, PH_APPLY = 2, PH_WAIT = 3, PH_DONE = 4 };
@@ -54,6 +56,11 @@ struct LoopArgs {
   const int32_t* unit_t0;
   const int32_t* unit_t1;
   const int32_t* seg_u0;  // [S + 1]
+  // row-block partition (ck_dist.cu): the last CTA publishes this rank's
+  // merged partials in rank_part instead of running the control step
+  int dist;
+  double* rank_part;
+  int tile_base;  // S == 1: first own tile (a partition rank's local block)
 };
 
 // Arguments of the inverse-operator step (ck_inverse.cu).
@@ -70,6 +77,25 @@ struct InvArgs {
   ColState* st;     // R columns
   Header* hdr;
   Params prm;
+};
+
+// Row-block partition rank (ck_dist.cu): this rank owns global rows/columns
+// [g0, g0 + n_loc), the fused kernels run over its own tiles and exchange
+// halos and per-rank partials with the other ranks every half step.
+struct DistPart {
+  int rank = 0, nranks = 1;
+  bool nccl = false;
+  void* comm = nullptr;             // ncclComm_t (nccl backend)
+  ck_session_s* const* group = nullptr;  // in-process backend: every rank's session
+  int64_t n_global = 0;
+  std::vector<int64_t> ext_global;  // extended column position -> global index (-1: padding)
+  std::vector<int64_t> xs_off, xr_off, ys_off, yr_off;  // [nranks + 1] per-peer offsets
+  DBuf<int32_t> xs_pos, xr_pos, ys_pos, yr_pos;         // permuted positions
+  DBuf<double2> xs_buf, xr_buf;                         // [count][R]
+  DBuf<double> ys_buf, yr_buf;                          // [count][R]
+  DBuf<double> part, gather;  // [R*(kPA+1)] this rank, [nranks][R*(kPA+1)] gathered
+  DBuf<double> chk;           // witness-norm exchange
+  double chk_local = 0.0;     // ||(A x_min) on this rank's rows||
 };
 
 }  // namespace ck
@@ -110,6 +136,7 @@ struct ck_session_s {
   int gsteps = 0;
   std::vector<double> hx;
   bool observe_on = false;
+  ck::DistPart* dist = nullptr;  // owned by the ck_dist group
 
   ~ck_session_s() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -118,3 +145,45 @@ struct ck_session_s {
   }
 };
 
+// Session internals shared by ck_adam.cu (single device, batches, inverse)
+// and ck_dist.cu (row-block partitions).
+namespace ck {
+void launch_apply_only(ck_session_s* s, cudaStream_t st);
+void launch_transpose_only(ck_session_s* s, cudaStream_t st);
+void launch_step(ck_session_s* s, cudaStream_t st);
+void pull_state(ck_session_s* s);
+void push_state(ck_session_s* s);
+int64_t total_done(const ck_session_s* s);
+bool any_wait(const ck_session_s* s);
+double2* col_buf(ck_session_s* s, int b, int c);
+void to_host(ck_session_s* s, int g, const double* src, double* host, cudaStream_t st);
+void load_start(ck_session_s* s, int g, int c, int b, const double* x);
+void service_restarts(ck_session_s* s);
+void build_graph(ck_session_s* s, int steps);
+void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t* seeds,
+                         int64_t ywords, double bytes_per_step);
+void session_setup_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* cfg, int R,
+                            const int64_t* seg_n, int S);
+void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness);
+void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished);
+void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_total,
+                  double* ms_apply, double* ms_transpose);
+void session_set_tiles(ck_session_s* s, int t0, int t1);
+void launch_dist_control(ck_session_s* s, bool apply, const double* gathered, int nranks,
+                         cudaStream_t st);
+int partial_words(int R);
+void dist_step(ck_session_s* s, cudaStream_t st);
+double dist_op_norm(ck_session_s* s, const double* xbest_internal, cudaStream_t st);
+}  // namespace ck
+
+struct ck_dist_s;
+namespace ck {
+void dist_nccl_id(void* out128);
+ck_dist_s* dist_new();
+void dist_free(ck_dist_s* D);
+void dist_create(ck_dist_s* D, const ck_dist_part* parts, int np, int rank0, int nranks,
+                 const void* nccl_id, const ck_adam_cfg* cfg, const uint64_t* seeds, int R);
+void dist_run(ck_dist_s* D, uint64_t max_steps, int32_t* finished);
+double dist_time(ck_dist_s* D, uint64_t steps);
+void dist_result(ck_dist_s* D, int col, int part, ck_norm_result* res, double* witness);
+}  // namespace ck
