@@ -49,15 +49,6 @@ def partition_rows(a: SparseMatrix, nparts: int) -> np.ndarray:
     return b
 
 
-def transpose_csr(a: SparseMatrix):
-    """(rp, row indices, values) of A^T, each column in increasing row order."""
-    rows = np.repeat(np.arange(a.nrows, dtype=np.int64), np.diff(a.row_offsets))
-    order = np.argsort(a.col_indices, kind="stable")
-    cnt = np.bincount(a.col_indices, minlength=a.ncols)
-    rp = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
-    return rp, rows[order], a.values[order]
-
-
 @dataclass
 class Part:
     """Rank p's extended local operator and halo needs (global indices)."""
@@ -111,19 +102,34 @@ class Part:
         return out
 
 
-def build_part(a: SparseMatrix, bounds: np.ndarray, p: int, at=None) -> Part:
+def _runs(starts: np.ndarray, lens: np.ndarray) -> np.ndarray:
+    """Concatenated index ranges [starts[k], starts[k] + lens[k])."""
+    total = int(lens.sum())
+    if total == 0:
+        return np.zeros(0, np.int64)
+    first = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    return np.repeat(starts - first, lens) + np.arange(total, dtype=np.int64)
+
+
+def build_part(a: SparseMatrix, bounds: np.ndarray, p: int) -> Part:
     """Rank p's extended operator: own rows (complete) and the halo rows
-    restricted to own columns, in increasing global order on both axes."""
+    restricted to own columns, in increasing global order on both axes.
+    One vectorised pass over the column indices finds the halo rows (rows
+    with entries in own columns); their own-column entries are one
+    contiguous run of each (sorted) row."""
     n = a.nrows
     g0, g1 = int(bounds[p]), int(bounds[p + 1])
-    rp, ci, va = a.row_offsets, a.col_indices.astype(np.int64), a.values
-    if at is None:
-        at = transpose_csr(a)
-    trp, tri, tva = at
-    own_ci = ci[rp[g0]:rp[g1]]
+    rp, ci, va = a.row_offsets, a.col_indices, a.values
+    own_ci = ci[rp[g0]:rp[g1]].astype(np.int64)
     hx = np.unique(own_ci[(own_ci < g0) | (own_ci >= g1)])
-    own_ri = tri[trp[g0]:trp[g1]]  # rows with entries in own columns
-    hy = np.unique(own_ri[(own_ri < g0) | (own_ri >= g1)])
+    inside = (ci >= g0) & (ci < g1)
+    before = ci < g0
+    cin = np.concatenate([[0], np.cumsum(inside, dtype=np.int64)])
+    cbe = np.concatenate([[0], np.cumsum(before, dtype=np.int64)])
+    del inside, before
+    cnt = cin[rp[1:]] - cin[rp[:-1]]  # own-column entries per row
+    rows_hit = np.flatnonzero(cnt)
+    hy = rows_hit[(rows_hit < g0) | (rows_hit >= g1)].astype(np.int64)
     nl = g1 - g0
     lx, ly = int((hx < g0).sum()), int((hy < g0).sum())
     tile0 = max(-(-lx // TILE), -(-ly // TILE))
@@ -131,27 +137,22 @@ def build_part(a: SparseMatrix, bounds: np.ndarray, p: int, at=None) -> Part:
     part = Part(p, n, g0, g1, tile0, tile1, tile1 * TILE + int((hy >= g1).sum()),
                 tile1 * TILE + int((hx >= g1).sum()), None, None, None, None, hx, hy)
     lens = np.zeros(part.ext_rows, np.int64)
-    # own rows: every entry (columns mapped to extended positions)
-    seg = slice(rp[g0], rp[g1])
-    own_cols = part.col_position(ci[seg])
     lens[part.own_offset():part.own_offset() + nl] = np.diff(rp[g0:g1 + 1])
-    # halo rows: entries in own columns only; A's entries of row i, columns in
-    # [g0, g1), are a contiguous run of the (sorted) row
-    hrows = np.concatenate([hy[hy < g0], hy[hy >= g1]])
-    hpos = part.row_position(hrows)
-    lo = np.array([rp[i] + np.searchsorted(ci[rp[i]:rp[i + 1]], g0) for i in hrows], np.int64)
-    hi = np.array([rp[i] + np.searchsorted(ci[rp[i]:rp[i + 1]], g1) for i in hrows], np.int64)
-    lens[hpos] = hi - lo
+    hpos = part.row_position(hy)
+    hlo = rp[hy] + (cbe[rp[hy + 1]] - cbe[rp[hy]])  # first own-column entry of each halo row
+    hlen = cnt[hy]
+    lens[hpos] = hlen
     out_rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     out_ci = np.empty(out_rp[-1], np.int64)
     out_va = np.empty(out_rp[-1])
     o0 = out_rp[part.own_offset()]
-    out_ci[o0:o0 + own_cols.size] = own_cols
-    out_va[o0:o0 + own_cols.size] = va[seg]
-    for r, a0, a1 in zip(hpos, lo, hi):
-        d0 = out_rp[r]
-        out_ci[d0:d0 + (a1 - a0)] = part.col_position(ci[a0:a1])
-        out_va[d0:d0 + (a1 - a0)] = va[a0:a1]
+    seg = slice(rp[g0], rp[g1])
+    out_ci[o0:o0 + (rp[g1] - rp[g0])] = part.col_position(own_ci)
+    out_va[o0:o0 + (rp[g1] - rp[g0])] = va[seg]
+    src = _runs(hlo, hlen)
+    dst = _runs(out_rp[hpos], hlen)
+    out_ci[dst] = part.col_position(ci[src])
+    out_va[dst] = va[src]
     part.rp, part.ci, part.va = out_rp, out_ci.astype(np.int32), out_va
     eg = np.full(part.ext_cols, -1, np.int64)
     cols_all = np.concatenate([hx[hx < g0], np.arange(g0, g1, dtype=np.int64), hx[hx >= g1]])
@@ -194,18 +195,18 @@ def halo_lists(parts_needs: Sequence[tuple], bounds: np.ndarray, me: Part) -> di
 def build_partition(a: SparseMatrix, nparts: int) -> list[Part]:
     """Every rank's part and halo lists (in-process backend / tests)."""
     b = partition_rows(a, nparts)
-    at = transpose_csr(a)
-    parts = [build_part(a, b, p, at) for p in range(nparts)]
+    parts = [build_part(a, b, p) for p in range(nparts)]
     needs = [(p.hx, p.hy) for p in parts]
     for p in parts:
         p.lists = halo_lists(needs, b, p)
     return parts
 
 
-def build_rank(a: SparseMatrix, nparts: int, rank: int, all_gather_object) -> Part:
+def build_rank(a: SparseMatrix, nparts: int, rank: int, all_gather_object,
+               bounds: Optional[np.ndarray] = None) -> Part:
     """This rank's part; the halo needs of all ranks are exchanged with
     `all_gather_object(obj) -> list` (e.g. torch.distributed's)."""
-    b = partition_rows(a, nparts)
+    b = partition_rows(a, nparts) if bounds is None else np.asarray(bounds, np.int64)
     me = build_part(a, b, rank)
     needs = all_gather_object((me.hx, me.hy))
     me.lists = halo_lists(needs, b, me)
