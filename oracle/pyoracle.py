@@ -201,6 +201,19 @@ class Oracle:
         f(C.c_int64(n), C.c_uint64(seed), rp.ctypes.data_as(_i64p), ci.ctypes.data_as(_i32p), _d(va))
         return n, rp, ci, va
 
+    def read_matrix_market(self, path: str):
+        """Reference only: read_matrix_market of a file -> (nrows, ncols, rp, ci, va) or None."""
+        f = self._f("read_matrix_market")
+        f.restype = C.c_int64
+        nr, nc = C.c_int64(), C.c_int64()
+        nnz = f(path.encode(), C.byref(nr), C.byref(nc), None, None, None)
+        if nnz < 0:
+            return None
+        rp, ci, va = np.zeros(nr.value + 1, np.int64), np.zeros(nnz, np.int32), np.zeros(nnz)
+        f(path.encode(), C.byref(nr), C.byref(nc), rp.ctypes.data_as(_i64p), ci.ctypes.data_as(_i32p),
+          _d(va))
+        return nr.value, nc.value, rp, ci, va
+
     def column_norms(self, a) -> np.ndarray:
         nr, nc, rp, ci, va = _csr(a)
         out = np.zeros(nc)

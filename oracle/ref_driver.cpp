@@ -14,6 +14,8 @@
 #include <condkit/rng.hpp>
 #include <condkit/sparse.hpp>
 #include <condkit/bench.hpp>
+#include <condkit/matrix_market.hpp>
+#include <fstream>
 
 #include <cstring>
 #include <random>
@@ -152,6 +154,28 @@ int64_t ckref_generate_illconditioned(int64_t n, uint64_t seed, int64_t* rp, int
     }
   }
   return (int64_t)a.nnz();
+}
+
+// read_matrix_market (matrix_market.hpp:118-209) of a file: rp == nullptr
+// returns nnz (and the shape); -1 on a parse error.
+int64_t ckref_read_matrix_market(const char* path, int64_t* nr, int64_t* nc, int64_t* rp, int32_t* ci,
+                                 double* va) {
+  try {
+    std::ifstream in(path);
+    SparseMatrix a = read_matrix_market(in);
+    *nr = (int64_t)a.nrows();
+    *nc = (int64_t)a.ncols();
+    if (rp) {
+      for (std::size_t i = 0; i <= a.nrows(); ++i) rp[i] = (int64_t)a.row_offsets()[i];
+      for (std::size_t k = 0; k < a.nnz(); ++k) {
+        ci[k] = (int32_t)a.col_indices()[k];
+        va[k] = a.values()[k];
+      }
+    }
+    return (int64_t)a.nnz();
+  } catch (...) {
+    return -1;
+  }
 }
 
 void ckref_column_norms(int64_t nr, int64_t nc, const int64_t* rp, const int32_t* ci,

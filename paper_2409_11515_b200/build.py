@@ -50,7 +50,24 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
     os.replace(out + ".tmp", out)
+    if not prof:
+        build_cli()
     return out
+
+
+CLI = os.path.join(ROOT, "tools", "condkit_b200_cli")
+
+
+def build_cli() -> str:
+    """tools/condkit_b200_cli: the cond/norm/verify/convert front end (C++,
+    over include/condkit_b200.hpp and the in-tree library)."""
+    src = os.path.join(ROOT, "tools", "condkit_b200_cli.cpp")
+    cmd = ["g++", "-O2", "-std=c++20", "-I", os.path.join(ROOT, "include"), src, "-o",
+           CLI + ".tmp", "-L", PKG, "-lcondkit_b200", f"-Wl,-rpath,{PKG}",
+           "-Wl,-rpath,$ORIGIN/../paper_2409_11515_b200"]
+    subprocess.run(cmd, check=True)
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
 
 
 if __name__ == "__main__":

@@ -50,7 +50,7 @@ constexpr int kPT = 1;  // per-column partials of k_transpose
 template <int R>
 struct Occ {
   static constexpr int apply = R == 1 ? 4 : 2;
-  static constexpr int transpose = R <= 2 ? 4 : 2;
+  static constexpr int transpose = R <= 2 ? 4 : 3;  // R >= 3: latency-bound, 3 CTAs beat the spill-free 2
 };
 
 // Work assignment of CTA `unit`. One operator (S == 1): the tiles are dealt
