@@ -116,13 +116,17 @@ def make_workload(cfg_id: int, grid: int | None):
     return a, name
 
 
-def bytes_per_iteration(nnz: int, n: int, R: int = 1):
-    # algorithmic bytes of the two fused sweeps (fp64 values,
-    # int32 indices): k_apply reads A (12 B/nnz), x and delta (16 B/row) and writes
-    # y (8); k_transpose reads A^T (12 B/nnz), y (8), x m v delta (32) and writes
-    # x m v delta (32). Total 24 nnz + 96 n per column (SURVEY.md 8d B_iter); R
-    # restart columns share the matrix sweeps.
-    return 12 * nnz + 24 * n * R, 12 * nnz + 72 * n * R
+def bytes_per_iteration(nnz: int, n: int, R: int = 1, col_format: int = 0):
+    # algorithmic bytes of the two fused sweeps. Per stored
+    # nonzero: the fp64 value plus its column index, int32 (12 B) or, in the narrow
+    # format (col_format bit0 for A, bit1 for A^T), a uint16 offset (10 B).
+    # k_apply reads A, x and delta (16 B/row) and writes y (8); k_transpose reads
+    # A^T, y (8), x m v delta (32) and writes x m v delta (32). Wide: 24 nnz + 96 n
+    # per column (SURVEY.md 8d B_iter); narrow: 20 nnz + 96 n. R restart columns
+    # share the matrix sweeps.
+    ea = 10 if col_format & 1 else 12
+    et = 10 if col_format & 2 else 12
+    return ea * nnz + 24 * n * R, et * nnz + 72 * n * R
 
 
 def cpu_reference(a, steps_hint: int, threads: int, iters: int):
@@ -228,10 +232,10 @@ def run_partition(args, rank, world, local, dist, barrier, allmax):
     clocks = sampler.stop() if sampler else None
     ms_max = allmax(ms)
     value = args.steps / (ms_max / 1000.0)
+    b_apply, b_tr = bytes_per_iteration(int(a.row_offsets[me.g1] - a.row_offsets[me.g0]), me.n_loc,
+                                        1, sess.info(0)["col_format"])
     sess.free()
     n, nnz = a.nrows, a.nnz
-    own_nnz = int(a.row_offsets[me.g1] - a.row_offsets[me.g0])
-    b_apply, b_tr = bytes_per_iteration(own_nnz, me.n_loc, 1)
     per_gpu = (b_apply + b_tr) / (ms / args.steps / 1000.0) / 1e9
     peak, peak_kind = measured_peaks()
     halo = {"x_entries": int(me.lists["xr_off"][-1]), "y_entries": int(me.lists["yr_off"][-1])}
@@ -362,7 +366,7 @@ def run_ours(args):
     sess.close()
 
     n, nnz = a.nrows, a.nnz
-    b_apply, b_tr = bytes_per_iteration(nnz, n, R)
+    b_apply, b_tr = bytes_per_iteration(nnz, n, R, info["col_format"])
     peak, peak_kind = measured_peaks()
     k_apply = {"name": f"k_apply<{R}>", "ms_avg": ms_apply / args.steps, "bytes": b_apply}
     k_tr = {"name": f"k_transpose<{R}>", "ms_avg": ms_tr / args.steps, "bytes": b_tr}
@@ -436,7 +440,9 @@ def run_ours(args):
                        "runs_per_step": runs_per_step,
                        "parallelism": (f"members sharded over {world} ranks" if ensemble else
                                        f"replicas{world} (independent restart streams)"),
-                       "l2": f"inputs larger than L2 (matrix {(24 * nnz) / 1e9:.1f} GB "
+                       "col_format": {0: "int32", 1: "A uint16", 2: "A^T uint16",
+                                      3: "uint16 offsets"}[info["col_format"]],
+                       "l2": f"inputs larger than L2 ({(b_apply + b_tr) / 1e9:.1f} GB moved "
                              f"per iteration vs 126 MB L2); no flush needed",
                        "sell_padding": (info["sell_entries_a"] - nnz) / max(nnz, 1)},
             "roofline": roofline,

@@ -77,7 +77,10 @@ typedef struct {
   int64_t sell_entries_a, sell_entries_at; /* stored entries incl. slice padding */
   int64_t device_bytes;
   int32_t device;
-  int32_t _pad;
+  /* column-index format of the device layouts: bit0 = A narrow, bit1 = A^T
+   * narrow (uint16 offsets from a per-slice base, 10 B per stored entry with
+   * the value; otherwise int32, 12 B). */
+  int32_t col_format;
 } ck_matrix_info;
 
 typedef struct ck_matrix_s* ck_matrix;
@@ -265,6 +268,8 @@ ck_status ck_dist_time(ck_dist d, uint64_t steps, double* ms);
  * extended-order slice (ext_cols doubles), NULL to skip. Collective. */
 ck_status ck_dist_result(ck_dist d, int32_t col, int32_t part, ck_norm_result* res,
                          double* witness);
+/* Device layout of part `part`'s extended local operator (ck_matrix_get_info). */
+ck_status ck_dist_part_info(ck_dist d, int32_t part, ck_matrix_info* info);
 ck_status ck_dist_free(ck_dist d);
 
 /* Ensembles on A^-1 (the sigma_min half of cond2 per member, config 5): nmem

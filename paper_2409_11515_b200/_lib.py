@@ -43,7 +43,7 @@ class StepInfo(C.Structure):
 class MatrixInfo(C.Structure):
     _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
                 ("sell_entries_a", C.c_int64), ("sell_entries_at", C.c_int64),
-                ("device_bytes", C.c_int64), ("device", C.c_int32), ("_pad", C.c_int32)]
+                ("device_bytes", C.c_int64), ("device", C.c_int32), ("col_format", C.c_int32)]
 
 
 # name -> (restype, argtypes)
@@ -106,6 +106,7 @@ _SIGS = {
     "ck_dist_run": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32)]),
     "ck_dist_time": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_double)]),
     "ck_dist_result": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(NormResult), dp]),
+    "ck_dist_part_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(MatrixInfo)]),
     "ck_dist_free": (C.c_int, [C.c_void_p]),
     "ck_column_norms": (C.c_int, [C.c_void_p, dp]),
     "ck_row_norms": (C.c_int, [C.c_void_p, dp]),

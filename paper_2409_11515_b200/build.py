@@ -35,20 +35,35 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
     """prof=True builds the phase-timing variant (-DCK_SWEEP_PROF) next to
-    the library as libcondkit_b200_prof.so (load it with CK_LIB=...)."""
+    the library as libcondkit_b200_prof.so (load it with CK_LIB=...).
+
+    Each translation unit compiles to its own object in parallel (build/),
+    then nvcc links the shared library."""
     out = LIB.replace(".so", "_prof.so") if prof else LIB
     if not prof and not force and not needs_build():
         return LIB
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
-           "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"),
-           "-o", out + ".tmp"] + sources() + ["-lpthread"]
+    flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+             "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc")]
     if prof:
-        cmd.insert(1, "-DCK_SWEEP_PROF")
+        flags.insert(0, "-DCK_SWEEP_PROF")
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+        flags.insert(0, "-Xptxas=-v")
+    objdir = os.path.join(ROOT, "build", "prof" if prof else "lib")
+    os.makedirs(objdir, exist_ok=True)
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        objs.append(obj)
+        cmd = [NVCC] + flags + ["-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd))
+        procs.append((src, subprocess.Popen(cmd)))
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {failed}")
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                    "-o", out + ".tmp"] + objs + ["-lpthread"], check=True)
     os.replace(out + ".tmp", out)
     if not prof:
         build_cli()

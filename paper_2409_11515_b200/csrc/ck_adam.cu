@@ -130,7 +130,7 @@ __device__ __forceinline__ void control_tail_transpose(ColState* sts, Header* hd
   hdr->needT = 0;
 }
 
-template <int R, bool OBS, int U = (R == 1 ? 8 : 4)>
+template <int R, bool OBS, bool NW, int U = (R == 1 ? 8 : 4)>
 __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_constant__ LoopArgs a) {
   int seg, tile0, tend, stride, u0, u1;
   unit_range(a, blockIdx.x, a.tiles_A, seg, tile0, tend, stride, u0, u1);
@@ -166,21 +166,23 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
   int64_t i = (int64_t)tile0 * kTile + threadIdx.x;
   const int64_t istep = (int64_t)stride * kTile;
   int64_t sp0 = 0, sp1 = 0;
-  int L = 0;
+  int L = 0, cb = 0;
   if (tile0 < tend && i < a.nr_pad) {
     sp0 = a.A.sp[i >> 5];
     sp1 = a.A.sp[(i >> 5) + 1];
     L = a.A.len[i];
+    cb = slice_cbase<NW>(a.A, i >> 5);
   }
   for (int tile = tile0; tile < tend; tile += stride, i += istep) {
     const int64_t base = sp0 + (i & 31);
     const int w = (int)((sp1 - sp0) >> 5);  // slice width: uniform across the warp
-    const int Lc = L;
+    const int Lc = L, cbc = cb;
     const int64_t inext = i + istep;
     if (tile + stride < tend && inext < a.nr_pad) {
       sp0 = a.A.sp[inext >> 5];
       sp1 = a.A.sp[(inext >> 5) + 1];
       L = a.A.len[inext];
+      cb = slice_cbase<NW>(a.A, inext >> 5);
     }
     if (i < a.nc) {  // own column-space element: ||x~||^2 (and observer stats)
 #pragma unroll
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
       for (int j0 = 0; j0 < w; j0 += U) {
         int c[U];
         double v[U];
-        load_chunk<U>(a.A, base, j0, w, c, v);
+        load_chunk<U, NW>(a.A, base, cbc, j0, w, c, v);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!act[r]) continue;
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
   if (threadIdx.x == 0 && !a.dist) control_tail_apply<R, OBS>(sts, hdr, a.prm, s_res);
 }
 
-template <int R, int U = (R <= 2 ? 8 : 4)>
+template <int R, bool NW, int U = (R <= 2 ? 8 : 4)>
 __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     k_transpose(const __grid_constant__ LoopArgs a) {
   int seg, tile0, tend, stride, u0, u1;
@@ -330,21 +332,23 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
   const int64_t jstep = (int64_t)stride * kTile;
   int64_t j = (int64_t)tile0 * kTile + threadIdx.x;
   int64_t sp0 = 0, sp1 = 0;
-  int L = 0;
+  int L = 0, cb = 0;
   if (tile0 < tend) {
     sp0 = a.AT.sp[j >> 5];
     sp1 = a.AT.sp[(j >> 5) + 1];
     L = a.AT.len[j];
+    cb = slice_cbase<NW>(a.AT, j >> 5);
   }
   for (int tile = tile0; tile < tend; tile += stride, j += jstep) {
     const int64_t base = sp0 + (j & 31);
     const int w = (int)((sp1 - sp0) >> 5);
-    const int Lc = L;
+    const int Lc = L, cbc = cb;
     if (tile + stride < tend) {
       const int64_t jn = j + jstep;
       sp0 = a.AT.sp[jn >> 5];
       sp1 = a.AT.sp[(jn >> 5) + 1];
       L = a.AT.len[jn];
+      cb = slice_cbase<NW>(a.AT, jn >> 5);
     }
     double acc[R];
 #pragma unroll
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     for (int j0 = 0; j0 < w; j0 += U) {
       int c[U];
       double v[U];
-      load_chunk<U>(a.AT, base, j0, w, c, v);
+      load_chunk<U, NW>(a.AT, base, cbc, j0, w, c, v);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (!act[r]) continue;
@@ -470,10 +474,26 @@ static unsigned grid256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_
 
 template <int R>
 static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
-  if (s->observe_on)
-    k_apply<R, true><<<s->args.units_A, kTile, 0, st>>>(s->args);
+  const bool nw = s->A->a.narrow;
+  if (s->observe_on) {
+    if (nw)
+      k_apply<R, true, true><<<s->args.units_A, kTile, 0, st>>>(s->args);
+    else
+      k_apply<R, true, false><<<s->args.units_A, kTile, 0, st>>>(s->args);
+  } else {
+    if (nw)
+      k_apply<R, false, true><<<s->args.units_A, kTile, 0, st>>>(s->args);
+    else
+      k_apply<R, false, false><<<s->args.units_A, kTile, 0, st>>>(s->args);
+  }
+}
+
+template <int R>
+static void launch_transpose_r(const ck_session_s* s, cudaStream_t st) {
+  if (s->A->at.narrow)
+    k_transpose<R, true><<<s->args.units_T, kTile, 0, st>>>(s->args);
   else
-    k_apply<R, false><<<s->args.units_A, kTile, 0, st>>>(s->args);
+    k_transpose<R, false><<<s->args.units_T, kTile, 0, st>>>(s->args);
 }
 
 void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st);
@@ -505,12 +525,11 @@ void launch_transpose_only(ck_session_s* s, cudaStream_t st) {
     launch_inv_half(s, 2, st);
     return;
   }
-  const LoopArgs& a = s->args;
   switch (s->R) {
-    case 1: k_transpose<1><<<a.units_T, kTile, 0, st>>>(a); break;
-    case 2: k_transpose<2><<<a.units_T, kTile, 0, st>>>(a); break;
-    case 3: k_transpose<3><<<a.units_T, kTile, 0, st>>>(a); break;
-    default: k_transpose<4><<<a.units_T, kTile, 0, st>>>(a); break;
+    case 1: launch_transpose_r<1>(s, st); break;
+    case 2: launch_transpose_r<2>(s, st); break;
+    case 3: launch_transpose_r<3>(s, st); break;
+    default: launch_transpose_r<4>(s, st); break;
   }
 }
 

@@ -293,22 +293,30 @@ ck_status ck_matrix_free(ck_matrix a) {
     if (s) cudaStreamDestroy(s);
   });
 }
+}  // extern "C"
 
+namespace ck {
+void matrix_info(const ck_matrix_s* a, ck_matrix_info* info) {
+  info->nrows = a->nrows;
+  info->ncols = a->ncols;
+  info->nnz = a->nnz;
+  info->sell_entries_a = a->a.entries;
+  info->sell_entries_at = a->at.entries;
+  auto sb = [](const Sell& s) {
+    return s.slice_ptr.bytes() + s.len.bytes() + s.col.bytes() + s.col16.bytes() + s.cbase.bytes() +
+           s.val.bytes() + s.perm.bytes() + s.inv.bytes();
+  };
+  info->device_bytes = sb(a->a) + sb(a->at);
+  info->device = a->device;
+  info->col_format = (a->a.narrow ? 1 : 0) | (a->at.narrow ? 2 : 0);
+}
+}  // namespace ck
+
+extern "C" {
 ck_status ck_matrix_get_info(ck_matrix a, ck_matrix_info* info) {
   return guarded([&] {
-    M(a);
-    info->nrows = a->nrows;
-    info->ncols = a->ncols;
-    info->nnz = a->nnz;
-    info->sell_entries_a = a->a.entries;
-    info->sell_entries_at = a->at.entries;
-    auto sb = [](const Sell& s) {
-      return s.slice_ptr.bytes() + s.len.bytes() + s.col.bytes() + s.val.bytes() + s.perm.bytes() +
-             s.inv.bytes();
-    };
-    info->device_bytes = sb(a->a) + sb(a->at);
-    info->device = a->device;
-    info->_pad = 0;
+    if (!info) fail(CK_ERR_INVALID_ARGUMENT, "info is NULL");
+    matrix_info(M(a), info);
   });
 }
 
@@ -907,6 +915,13 @@ ck_status ck_dist_result(ck_dist d, int32_t col, int32_t part, ck_norm_result* r
   return guarded([&] {
     if (!d) fail(CK_ERR_INVALID_ARGUMENT, "dist handle is NULL");
     dist_result(d, col, part, res, witness);
+  });
+}
+
+ck_status ck_dist_part_info(ck_dist d, int32_t part, ck_matrix_info* info) {
+  return guarded([&] {
+    if (!d || !info) fail(CK_ERR_INVALID_ARGUMENT, "dist handle or info is NULL");
+    matrix_info(dist_part_matrix(d, part), info);
   });
 }
 

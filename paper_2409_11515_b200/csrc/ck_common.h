@@ -69,14 +69,27 @@ struct DBuf {
 // inside each 256-row tile by descending length (stable), so every 32-row slice
 // is nearly uniform; slice s stores entry j of its lane-th row at
 // slice_ptr[s] + 32*j + lane, which makes each warp load one contiguous
-// 256-byte run of values and a 128-byte run of column indices.
+// 256-byte run of values and a 128-byte (wide) or 64-byte (narrow) run of
+// column indices.
+//
+// Column indices come in two formats, chosen per operator at build time:
+//   wide    int32 column (12 bytes per stored entry with the value);
+//   narrow  uint16 offset from a per-slice base column, cbase[s] + col16[k]
+//           (10 bytes per stored entry). Used whenever every slice's columns
+//           span < 65536 -- any operator whose bandwidth (in the permuted
+//           spaces) is below ~32k, which covers every banded/stencil operator
+//           of the BASELINE configs. Same columns, same order: the arithmetic
+//           is unchanged.
 struct Sell {
   int64_t nrows = 0;      // logical rows
   int64_t nrows_pad = 0;  // multiple of kTile
   int64_t entries = 0;    // stored entries including slice padding
   DBuf<int64_t> slice_ptr;  // nrows_pad/32 + 1
   DBuf<uint16_t> len;       // per permuted row
-  DBuf<int32_t> col;        // column index in the permuted column space
+  DBuf<int32_t> col;        // wide: column index in the permuted column space
+  DBuf<uint16_t> col16;     // narrow: column - cbase[slice]
+  DBuf<int32_t> cbase;      // narrow: per-slice base column (nrows_pad/32)
+  bool narrow = false;
   DBuf<double> val;
   DBuf<int32_t> perm;       // perm[k] = original row at permuted position k (-1 = pad)
   DBuf<int32_t> inv;        // inv[row] = permuted position
@@ -86,10 +99,15 @@ struct SellView {
   const int64_t* __restrict__ sp;
   const uint16_t* __restrict__ len;
   const int32_t* __restrict__ col;
+  const uint16_t* __restrict__ col16;
+  const int32_t* __restrict__ cbase;
   const double* __restrict__ val;
+  int narrow;
 };
 
-inline SellView view(const Sell& s) { return {s.slice_ptr.p, s.len.p, s.col.p, s.val.p}; }
+inline SellView view(const Sell& s) {
+  return {s.slice_ptr.p, s.len.p, s.col.p, s.col16.p, s.cbase.p, s.val.p, s.narrow ? 1 : 0};
+}
 
 }  // namespace ck
 

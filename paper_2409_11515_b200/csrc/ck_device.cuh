@@ -192,20 +192,39 @@ __device__ __forceinline__ bool elect_last_block(unsigned int* counter, unsigned
 // gathered vectors keep their L2 residency.
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
+__device__ __forceinline__ int ld_stream(const uint16_t* p) {
+  return (int)__ldcs(reinterpret_cast<const unsigned short*>(p));
+}
+
+// Base column of slice s (narrow format; 0 for wide).
+template <bool NW>
+__device__ __forceinline__ int slice_cbase(const SellView& A, int64_t s) {
+  return NW ? A.cbase[s] : 0;
+}
+
+// Column of stored entry k of slice s, either format (setup kernels; the
+// sweeps use the compile-time form in load_chunk).
+__device__ __forceinline__ int sell_col(const SellView& A, int64_t s, int64_t k) {
+  return A.narrow ? A.cbase[s] + (int)A.col16[k] : A.col[k];
+}
 
 // Loads U consecutive stored entries (stored positions j0..j0+U-1) of a
 // sliced-ELL row. All loads of the chunk are issued before any use; positions at
 // or beyond the warp-uniform slice width w are predicated off and read as
-// (column 0, value 0). Padding inside [len, w) is stored as (0, 0.0), so the
-// gathers that follow never need a bounds check.
-template <int U>
-__device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int j0, int w, int* c,
-                                           double* v) {
+// (column cb, value 0). Padding inside [len, w) is stored as (cb, 0.0), so the
+// gathers that follow never need a bounds check. NW selects the narrow column
+// format (cb = the slice's base column).
+template <int U, bool NW>
+__device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int cb, int j0, int w,
+                                           int* c, double* v) {
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const bool ok = j0 + u < w;
     const int64_t k = base + (int64_t)(j0 + u) * kSlice;
-    c[u] = ok ? ld_stream(A.col + k) : 0;
+    if (NW)
+      c[u] = cb + (ok ? ld_stream(A.col16 + k) : 0);
+    else
+      c[u] = ok ? ld_stream(A.col + k) : 0;
     v[u] = ok ? ld_stream(A.val + k) : 0.0;
   }
 }

@@ -252,6 +252,11 @@ struct ck_dist_s {
 namespace ck {
 
 ck_dist_s* dist_new() { return new ck_dist_s(); }
+
+const ck_matrix_s* dist_part_matrix(const ck_dist_s* D, int part) {
+  if (part < 0 || part >= (int)D->mats.size()) fail(CK_ERR_INVALID_ARGUMENT, "part out of range");
+  return D->mats[(size_t)part];
+}
 void dist_free(ck_dist_s* D) { delete D; }
 
 void dist_nccl_id(void* out128) {

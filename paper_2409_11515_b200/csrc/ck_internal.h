@@ -10,6 +10,7 @@ namespace ck {
 
 constexpr int kNormParts = 296;  // partial blocks of the standalone norm (2 x 148 SMs)
 
+void matrix_info(const ck_matrix_s* a, ck_matrix_info* info);
 void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* rp,
                    const int32_t* ci, const double* va);
 void matrix_apply_host(ck_matrix_s* m, bool transpose, const double* x, double* y);

@@ -42,7 +42,7 @@ __global__ void k_band_bounds(SellView A, int64_t nrows_pad, const int32_t* __re
   const int L = A.len[p];
   int lo = 0, up = 0;
   for (int j = 0; j < L; ++j) {
-    const int32_t col = cperm[A.col[base + (int64_t)j * kSlice]];
+    const int32_t col = cperm[sell_col(A, p >> 5, base + (int64_t)j * kSlice)];
     lo = max(lo, row - col);
     up = max(up, col - row);
   }
@@ -60,7 +60,7 @@ __global__ void k_band_fill(SellView A, int64_t nrows_pad, const int32_t* __rest
   const int L = A.len[p];
   for (int j = 0; j < L; ++j) {
     const int64_t k = base + (int64_t)j * kSlice;
-    AB(b, row, cperm[A.col[k]]) = A.val[k];
+    AB(b, row, cperm[sell_col(A, p >> 5, k)]) = A.val[k];
   }
 }
 

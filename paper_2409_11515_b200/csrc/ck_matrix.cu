@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ck_common.h"
@@ -142,9 +143,52 @@ __global__ void k_sell_fill(int64_t nrows_pad, const int32_t* __restrict__ perm,
   }
 }
 
+// Narrow column format (ck_common.h): per-slice base = smallest stored column
+// of the slice's rows; flags bit0 when a slice's columns span >= 65536.
+__global__ void k_slice_span(int64_t nslices, const int64_t* __restrict__ sp,
+                             const uint16_t* __restrict__ len, const int32_t* __restrict__ col,
+                             int32_t* cbase, unsigned int* flags) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;  // warp-uniform
+  const int64_t base = sp[s] + lane;
+  const int L = len[s * kSlice + lane];
+  int lo = 0x7fffffff, hi = -1;
+  for (int j = 0; j < L; ++j) {
+    const int c = col[base + (int64_t)j * kSlice];
+    lo = min(lo, c);
+    hi = max(hi, c);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0) {
+    const int b = hi < 0 ? 0 : lo;
+    cbase[s] = b;
+    if (hi >= 0 && (int64_t)hi - b > 65535) atomicOr(flags, 1u);
+  }
+}
+
+__global__ void k_narrow_cols(int64_t nrows_pad, const int64_t* __restrict__ sp,
+                              const uint16_t* __restrict__ len, const int32_t* __restrict__ cbase,
+                              const int32_t* __restrict__ col, uint16_t* col16) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nrows_pad) return;
+  const int64_t slice = k >> 5, base = sp[slice] + (k & 31);
+  const int w = (int)((sp[slice + 1] - sp[slice]) >> 5), L = len[k];
+  const int b = cbase[slice];
+  for (int j = 0; j < w; ++j) {
+    const int64_t d = base + (int64_t)j * kSlice;
+    col16[d] = (uint16_t)(j < L ? col[d] - b : 0);
+  }
+}
+
 // ------------------------------------------------------ standalone kernels
 // One thread per permuted row; entries summed in stored order with unfused
 // multiply/add, i.e. exactly matvec's arithmetic (sparse.hpp:221-223).
+template <bool NW>
 __global__ void __launch_bounds__(kTile) k_sell_spmv(SellView A, int64_t nrows_pad,
                                                      const double* __restrict__ x,
                                                      double* __restrict__ y) {
@@ -155,11 +199,12 @@ __global__ void __launch_bounds__(kTile) k_sell_spmv(SellView A, int64_t nrows_p
   const int64_t base = s0 + (row & 31);
   const int w = (int)((s1 - s0) >> 5);
   const int L = A.len[row];
+  const int cb = slice_cbase<NW>(A, row >> 5);
   double acc = 0.0;
   for (int j0 = 0; j0 < w; j0 += U) {
     int c[U];
     double v[U], xg[U];
-    load_chunk<U>(A, base, j0, w, c, v);
+    load_chunk<U, NW>(A, base, cb, j0, w, c, v);
 #pragma unroll
     for (int u = 0; u < U; ++u) xg[u] = __ldg(x + c[u]);
 #pragma unroll
@@ -231,6 +276,23 @@ __global__ void __launch_bounds__(kTile) k_norm_final(int nparts, const double* 
 
 static unsigned int grid_for(int64_t n, int threads = 256) {
   return (unsigned int)std::max<int64_t>(1, ceil_div(n, threads));
+}
+
+// y = op x over a SELL operator (whole padded row range), either column format.
+static void sell_spmv(const Sell& op, const double* x, double* y, cudaStream_t st) {
+  const unsigned g = (unsigned)(op.nrows_pad / kTile);
+  if (op.narrow)
+    k_sell_spmv<true><<<g, kTile, 0, st>>>(view(op), op.nrows_pad, x, y);
+  else
+    k_sell_spmv<false><<<g, kTile, 0, st>>>(view(op), op.nrows_pad, x, y);
+  CK_CUDA(cudaGetLastError());
+}
+
+// Narrow column format unless CK_SELL_WIDE=1 (A/B switch) or a slice spans
+// >= 65536 columns.
+static bool narrow_allowed() {
+  const char* e = std::getenv("CK_SELL_WIDE");
+  return !(e && e[0] == '1');
 }
 
 double device_norm(const double* v, int64_t n, double* scratch, cudaStream_t st) {
@@ -369,6 +431,28 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
     k_sell_fill<<<grid_for(s.nrows_pad), 256, 0, st>>>(s.nrows_pad, s.perm.p, s.len.p, srp, sci,
                                                        sva, colmap, s.slice_ptr.p, s.col.p, s.val.p);
     CK_CUDA(cudaGetLastError());
+    s.narrow = false;
+    if (narrow_allowed()) {
+      s.cbase.alloc(nslices);
+      DBuf<unsigned int> wide(1);
+      CK_CUDA(cudaMemsetAsync(wide.p, 0, sizeof(unsigned int), st));
+      k_slice_span<<<grid_for(nslices * kSlice), 256, 0, st>>>(nslices, s.slice_ptr.p, s.len.p,
+                                                                s.col.p, s.cbase.p, wide.p);
+      unsigned int h_wide = 0;
+      CK_CUDA(cudaMemcpyAsync(&h_wide, wide.p, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+      CK_CUDA(cudaStreamSynchronize(st));
+      if (h_wide == 0) {
+        s.col16.alloc(std::max<int64_t>(s.entries, 1));
+        k_narrow_cols<<<grid_for(s.nrows_pad), 256, 0, st>>>(s.nrows_pad, s.slice_ptr.p, s.len.p,
+                                                             s.cbase.p, s.col.p, s.col16.p);
+        CK_CUDA(cudaGetLastError());
+        CK_CUDA(cudaStreamSynchronize(st));
+        s.col.reset();
+        s.narrow = true;
+      } else {
+        s.cbase.reset();
+      }
+    }
     CK_CUDA(cudaStreamSynchronize(st));
   };
   finish(m->a, rp.p, ci.p, va.p, m->at.inv.p);   // A's columns -> Q positions
@@ -392,7 +476,7 @@ void matrix_apply_host(ck_matrix_s* m, bool transpose, const double* x, double* 
   if (nin > 0)
     CK_CUDA(cudaMemcpyAsync(m->s_in.p, x, sizeof(double) * nin, cudaMemcpyHostToDevice, st));
   k_gather_perm<<<grid_for(dom.nrows_pad), 256, 0, st>>>(dom.nrows_pad, dom.perm.p, m->s_in.p, m->s_perm_in.p);
-  k_sell_spmv<<<(unsigned)(op.nrows_pad / kTile), kTile, 0, st>>>(view(op), op.nrows_pad, m->s_perm_in.p, m->s_perm_out.p);
+  sell_spmv(op, m->s_perm_in.p, m->s_perm_out.p, st);
   k_scatter_perm<<<grid_for(op.nrows_pad), 256, 0, st>>>(op.nrows_pad, op.perm.p, m->s_perm_out.p, m->s_out.p);
   CK_CUDA(cudaGetLastError());
   if (nout > 0)
@@ -403,8 +487,7 @@ void matrix_apply_host(ck_matrix_s* m, bool transpose, const double* x, double* 
 // Device-pointer variant in permuted spaces: x_perm (column space of A, Q
 // order, padded) -> y_perm (row space, P order, padded).
 void matrix_apply_perm(ck_matrix_s* m, const double* x_perm, double* y_perm, cudaStream_t st) {
-  k_sell_spmv<<<(unsigned)(m->a.nrows_pad / kTile), kTile, 0, st>>>(view(m->a), m->a.nrows_pad, x_perm, y_perm);
-  CK_CUDA(cudaGetLastError());
+  sell_spmv(m->a, x_perm, y_perm, st);
 }
 
 void gather_perm(const int32_t* perm, int64_t n_out, const double* in, double* out, cudaStream_t st) {
@@ -458,7 +541,7 @@ void grad_explicit_dev(ck_matrix_s* m, const double* x, double* g, bool* degener
   *degenerate = avn == 0.0;
   if (*degenerate) return;
   // atav = A^T av (Q order)
-  k_sell_spmv<<<(unsigned)(m->at.nrows_pad / kTile), kTile, 0, st>>>(view(m->at), m->at.nrows_pad, m->s_perm_out.p, m->s_out.p);
+  sell_spmv(m->at, m->s_perm_out.p, m->s_out.p, st);
   double inv_v2 = 1.0 / (vn * vn), inv_av2 = 1.0 / (avn * avn);
   k_grad_combine<<<grid_for(m->at.nrows_pad), 256, 0, st>>>(m->at.nrows_pad, m->s_perm_in.p, m->s_out.p, inv_v2, inv_av2, m->s_perm_out.p);
   scatter_perm(m->at.perm.p, m->at.nrows_pad, m->s_perm_out.p, m->s_in.p, st);

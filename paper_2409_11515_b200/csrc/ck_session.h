@@ -185,5 +185,6 @@ void dist_create(ck_dist_s* D, const ck_dist_part* parts, int np, int rank0, int
                  const void* nccl_id, const ck_adam_cfg* cfg, const uint64_t* seeds, int R);
 void dist_run(ck_dist_s* D, uint64_t max_steps, int32_t* finished);
 double dist_time(ck_dist_s* D, uint64_t steps);
+const ck_matrix_s* dist_part_matrix(const ck_dist_s* D, int part);
 void dist_result(ck_dist_s* D, int col, int part, ck_norm_result* res, double* witness);
 }  // namespace ck

@@ -274,6 +274,13 @@ class PartitionedSession:
         _lib.check(_lib.load().ck_dist_time(self.handle, steps, C.byref(ms)), "ck_dist_time")
         return ms.value
 
+    def info(self, part: int = 0) -> dict:
+        """Device layout of part `part`'s extended local operator."""
+        inf = _lib.MatrixInfo()
+        _lib.check(_lib.load().ck_dist_part_info(self.handle, part, C.byref(inf)),
+                   "ck_dist_part_info")
+        return {k: getattr(inf, k) for k, _ in _lib.MatrixInfo._fields_}
+
     def result(self, col: int = 0, part: int = 0) -> NormEstimate:
         """Estimate of restart column `col`; witness = rank `part`'s own slice."""
         r = _lib.NormResult()

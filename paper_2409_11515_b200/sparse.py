@@ -161,7 +161,7 @@ class DeviceMatrix:
     def info(self) -> dict:
         inf = _lib.MatrixInfo()
         _lib.check(_lib.load().ck_matrix_get_info(self.handle, C.byref(inf)), "ck_matrix_get_info")
-        return {k: getattr(inf, k) for k, _ in _lib.MatrixInfo._fields_ if k != "_pad"}
+        return {k: getattr(inf, k) for k, _ in _lib.MatrixInfo._fields_}
 
     def matvec(self, x) -> np.ndarray:
         x = _lib.as_f64(x, self.ncols, "matvec: vector")

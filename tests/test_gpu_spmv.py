@@ -97,3 +97,50 @@ def test_norm_overflow_safety():
     assert xn == pytest.approx(5e300, rel=1e-15)
     assert bn == pytest.approx(15e300, rel=1e-15)
     assert rn == pytest.approx(10e300, rel=1e-15)
+
+
+def _wide_span_matrix():
+    # one entry per row at column 2200 i: a 32-row slice of A spans 68200 > 65535
+    # columns (wide int32 format), while every slice of A^T stays narrow.
+    n_r, n_c = 1000, 2200 * 999 + 1
+    rows = np.arange(n_r)
+    vals = np.random.default_rng(3).standard_normal(n_r)
+    return ck.SparseMatrix.from_coo(n_r, n_c, rows, 2200 * rows, vals)
+
+
+def test_column_formats_and_bitwise(port, monkeypatch):
+    """The narrow (uint16 offset) and wide (int32) column formats give identical
+    bits; a slice spanning >= 65536 columns falls back to wide per operator."""
+    a = M.row_scaled(M.laplacian2d(40), port, 2)
+    x = port.random_unit_vectors(8, a.ncols)[0]
+    want_y, want_z = port.matvec(a, x), port.transpose_matvec(a, x)
+    assert a.device().info()["col_format"] == 3
+    assert np.array_equal(ck.matvec(a, x), want_y)
+    assert np.array_equal(ck.transpose_matvec(a, x), want_z)
+    monkeypatch.setenv("CK_SELL_WIDE", "1")
+    w = ck.SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices, a.values)
+    assert w.device().info()["col_format"] == 0
+    assert np.array_equal(ck.matvec(w, x), want_y)
+    assert np.array_equal(ck.transpose_matvec(w, x), want_z)
+    monkeypatch.delenv("CK_SELL_WIDE")
+    m = _wide_span_matrix()
+    assert m.device().info()["col_format"] == 2  # A wide, A^T narrow
+    xm = port.random_unit_vectors(9, m.ncols)[0]
+    um = port.random_unit_vectors(10, m.nrows)[0]
+    assert np.array_equal(ck.matvec(m, xm), port.matvec(m, xm))
+    assert np.array_equal(ck.transpose_matvec(m, um), port.transpose_matvec(m, um))
+
+
+def test_adam_identical_across_column_formats(port, monkeypatch):
+    """projected_adam on the narrow and wide layouts: same bits, same iterations."""
+    from paper_2409_11515_b200 import configs
+    a = configs.generate(configs.LAPLACIAN, 24, 1)
+    cfg = configs.baseline_adam(1, max_iter=150)
+    e1 = ck.norm2(a, cfg)
+    monkeypatch.setenv("CK_SELL_WIDE", "1")
+    w = ck.SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices, a.values)
+    assert w.device().info()["col_format"] == 0
+    e2 = ck.norm2(w, cfg)
+    assert e1.iterations == e2.iterations
+    assert e1.value == e2.value
+    assert np.array_equal(e1.witness, e2.witness)
