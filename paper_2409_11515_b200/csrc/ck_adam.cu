@@ -31,6 +31,7 @@
 #include <cmath>
 #include <cstring>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "ck_common.h"
@@ -644,8 +645,23 @@ void to_host(ck_session_s* s, int g, const double* src, double* host, cudaStream
     scatter_perm(s->perm + off, pad, src + off, scratch, st);
     out = scratch + off;
   }
-  CK_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * s->seg_n[g], cudaMemcpyDeviceToHost, st));
+  const int64_t n = s->seg_n[g];
+  if (s->hx.n < n) {
+    CK_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  // through the pinned staging buffer (full-rate D2H), then a threaded copy
+  CK_CUDA(cudaMemcpyAsync(s->hx.p, out, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaStreamSynchronize(st));
+  const int64_t nt = n < (int64_t(1) << 20) ? 1 : 8, chunk = ceil_div(n, nt);
+  std::vector<std::thread> pool;
+  for (int64_t t = 1; t < nt; ++t) {
+    const int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo < hi) pool.emplace_back([=] { std::memcpy(host + lo, s->hx.p + lo, sizeof(double) * (hi - lo)); });
+  }
+  std::memcpy(host, s->hx.p, sizeof(double) * std::min(n, chunk));
+  for (auto& th : pool) th.join();
 }
 
 // Upload a fresh start vector for member g, column c into buffer b: (x,
@@ -723,6 +739,7 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
                                 int64_t ywords, double bytes_per_step) {
   cudaStream_t st = s->stream;
   const int R = s->R, S = s->S;
+  Trace tr("session_init");
   s->thalf = std::max(s->npad, ywords / R);
   s->tmp.alloc(2 * s->thalf);
   CK_CUDA(cudaMemsetAsync(s->PX.p, 0, s->PX.bytes(), st));
@@ -732,15 +749,18 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
   CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_hdr), sizeof(Header) * S));
   int64_t nmax = 0;
   for (int g = 0; g < S; ++g) nmax = std::max(nmax, s->seg_n[g]);
-  s->hx.resize((size_t)nmax);
+  s->hx.resize(nmax);
   s->gens.clear();
   s->gens.reserve((size_t)S * R);
   for (int g = 0; g < S; ++g) {
     for (int c = 0; c < R; ++c) {
       s->gens.emplace_back(seeds[g * R + c]);
+      if (g == 0 && c == 0) tr.mark("buffers", st);
       draw_start(s, g * R + c, g, s->hx.data());  // x0, rng.hpp:68-77
+      if (g == 0 && c == 0) tr.mark("x0 host RNG", st);
       load_start(s, g, c, 0, s->hx.data());
       CK_CUDA(cudaStreamSynchronize(st));  // hx is reused for the next upload
+      if (g == 0 && c == 0) tr.mark("x0 upload", st);
       ColState cs{};
       cs.phase = cfg->max_iter == 0 ? PH_DONE : PH_PRO;
       cs.cur = 0;
@@ -758,11 +778,13 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
     h.ndone = cfg->max_iter == 0 ? R : 0;
     s->h_hdr[g] = h;
   }
+  tr.mark("remaining columns", st);
   push_state(s);
   // chunk length: about 4 ms of device work per host round trip, 4..256 steps
   const int steps =
       (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
   build_graph(s, steps);
+  tr.mark("graph capture", st);
 }
 
 // Explicit-operator session over S >= 1 square-or-rectangular members packed
@@ -1057,6 +1079,7 @@ void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness
   if (k < 0 || k >= s->S * s->R) fail(CK_ERR_INVALID_ARGUMENT, "column out of range");
   const int g = k / s->R, c = k % s->R;
   cudaStream_t st = s->stream;
+  Trace tr("session_result");
   pull_state(s);
   ColState& cs = s->h_st[k];
   const int64_t ncp = s->npad, off = s->seg_off[g], pad = s->seg_pad[g];
@@ -1087,7 +1110,9 @@ void session_result(ck_session_s* s, int k, ck_norm_result* res, double* witness
     res->value = 0.0;
     res->converged = 0;
   }
+  tr.mark("witness check", st);
   if (witness) to_host(s, g, xbest, witness, st);
+  tr.mark("witness D2H", st);
 }
 
 // x of buffer b / column c as a plain internal vector in `out` (npad doubles).

@@ -86,23 +86,64 @@ static void parallel_for(int64_t n, F&& f) {
 }
 
 // random_unit_vector (rng.hpp:68-77) with standard_normal (rng.hpp:61-65) and
-// uniform01 (rng.hpp:31-33): the engine draws stay sequential (they define the
-// stream); the Box-Muller transform and the final scaling are elementwise and
-// run on all host threads; the norm is sequential as in the reference.
+// uniform01 (rng.hpp:31-33). The engine draws stay sequential (they define the
+// stream) and run on the calling thread block by block, while a helper thread
+// applies the Box-Muller transform of the previous block on all host threads
+// (pipelined; no n-sized draw buffer). The norm is the reference's two_norm:
+// amax (exact in any order, folded into the transform), then the sequential
+// scaled sum of squares.
 void random_unit_vector_host(void* engine, int64_t n, double* out) {
+  if (n <= 0) return;
   auto& g = *static_cast<std::mt19937_64*>(engine);
-  std::vector<uint64_t> draws((size_t)(2 * n));
+  constexpr int64_t kBlock = int64_t(1) << 18;  // pairs per pipeline block
+  std::vector<uint64_t> buf[2];
+  buf[0].resize((size_t)(2 * std::min(n, kBlock)));
+  buf[1].resize(buf[0].size());
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nthr = std::min<int64_t>(hw, 64);
   double nrm = 0.0;
   while (nrm == 0.0) {
-    for (auto& d : draws) d = g();
-    parallel_for(n, [&](int64_t b, int64_t e) {
-      for (int64_t i = b; i < e; ++i) {
-        double u1 = 1.0 - static_cast<double>(draws[2 * i] >> 11) * 0x1.0p-53;
-        double u2 = static_cast<double>(draws[2 * i + 1] >> 11) * 0x1.0p-53;
-        out[i] = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+    std::vector<double> amax((size_t)nthr, 0.0);
+    std::thread worker;
+    for (int64_t b0 = 0; b0 < n; b0 += kBlock) {
+      const int64_t len = std::min(kBlock, n - b0);
+      std::vector<uint64_t>& d = buf[(b0 / kBlock) & 1];
+      for (int64_t k = 0; k < 2 * len; ++k) d[(size_t)k] = g();
+      if (worker.joinable()) worker.join();
+      worker = std::thread([&, b0, len, dp = d.data()] {
+        const int64_t chunk = ceil_div(len, nthr);
+        std::vector<std::thread> pool;
+        for (int64_t t = 0; t < nthr; ++t) {
+          const int64_t lo = t * chunk, hi = std::min(len, lo + chunk);
+          if (lo >= hi) break;
+          pool.emplace_back([&amax, dp, out, b0, lo, hi, t] {
+            double m = amax[(size_t)t];
+            for (int64_t i = lo; i < hi; ++i) {
+              const double u1 = 1.0 - static_cast<double>(dp[2 * i] >> 11) * 0x1.0p-53;
+              const double u2 = static_cast<double>(dp[2 * i + 1] >> 11) * 0x1.0p-53;
+              const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+              out[b0 + i] = z;
+              m = std::max(m, std::abs(z));
+            }
+            amax[(size_t)t] = m;
+          });
+        }
+        for (auto& th : pool) th.join();
+      });
+    }
+    if (worker.joinable()) worker.join();
+    double am = 0.0;
+    for (double m : amax) am = std::max(am, m);
+    if (am == 0.0 || !std::isfinite(am)) {
+      nrm = am;
+    } else {
+      double sq = 0.0;  // two_norm's scaled sum, in order (sparse.hpp:175-186)
+      for (int64_t i = 0; i < n; ++i) {
+        const double q = out[i] / am;
+        sq += q * q;
       }
-    });
-    nrm = two_norm_seq(out, n);
+      nrm = am * std::sqrt(sq);
+    }
   }
   parallel_for(n, [&](int64_t b, int64_t e) {
     for (int64_t i = b; i < e; ++i) out[i] /= nrm;

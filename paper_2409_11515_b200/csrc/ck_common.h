@@ -2,7 +2,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -28,6 +31,54 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Phase timer for the setup paths (CK_TRACE=1): synchronises the stream and
+// prints the wall time since the previous mark to stderr.
+struct Trace {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit Trace(const char* tag) : on(false) {
+    const char* e = std::getenv("CK_TRACE");
+    on = e && e[0] == '1';
+    t = std::chrono::steady_clock::now();
+    if (on) std::fprintf(stderr, "[ck_trace] %s\n", tag);
+  }
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ck_trace]   %-28s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
+// Page-locked host buffer (staging of start vectors and witnesses).
+template <class T>
+struct PinnedBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() { reset(); }
+  void resize(int64_t count) {
+    if (count <= n) return;
+    reset();
+    if (cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count)) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      fail(CK_ERR_OUT_OF_MEMORY, "cudaMallocHost failed");
+    }
+    n = count;
+  }
+  void reset() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* data() { return p; }
+};
 
 // Device buffer with RAII.
 template <class T>

@@ -323,6 +323,7 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
   m->nrows = nrows;
   m->ncols = ncols;
   m->nnz = nnz;
+  Trace tr("matrix_upload");
 
   DBuf<int64_t> rp(nrows + 1);
   DBuf<int32_t> ci(std::max<int64_t>(nnz, 1));
@@ -332,6 +333,7 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
     CK_CUDA(cudaMemcpyAsync(ci.p, h_ci, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
     CK_CUDA(cudaMemcpyAsync(va.p, h_va, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
   }
+  tr.mark("alloc + H2D", st);
   DBuf<unsigned int> flags(1);
   DBuf<int> maxlen(2);
   CK_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(unsigned int), st));
@@ -357,6 +359,7 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
   if (h_flags & 8u) fail(CK_ERR_DIMENSION, "non-finite entry");
   if (h_maxlen[0] > 65535) fail(CK_ERR_UNSUPPORTED, "row with more than 65535 entries");
 
+  tr.mark("validate + column counts", st);
   DBuf<int64_t> at_rp(std::max<int64_t>(ncols, 1) + 1);
   {
     DBuf<int64_t> cnt64(std::max<int64_t>(ncols, 1) + 1);
@@ -391,6 +394,7 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
   }
 
   // Row permutations (P for A's rows, Q for A's columns) and the two layouts.
+  tr.mark("A^T (stable radix sort)", st);
   DBuf<int32_t> lenA(std::max<int64_t>(nrows, 1));
   if (nrows > 0) k_row_len<<<grid_for(nrows), 256, 0, st>>>(nrows, rp.p, lenA.p);
   DBuf<int32_t> lenAT(std::max<int64_t>(ncols, 1));
@@ -455,8 +459,11 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
     }
     CK_CUDA(cudaStreamSynchronize(st));
   };
+  tr.mark("tile sorts", st);
   finish(m->a, rp.p, ci.p, va.p, m->at.inv.p);   // A's columns -> Q positions
+  tr.mark("SELL A", st);
   finish(m->at, at_rp.p, at_ci.p, at_va.p, m->a.inv.p);  // A^T's columns (A's rows) -> P positions
+  tr.mark("SELL A^T", st);
 
   int64_t vec = std::max(m->a.nrows_pad, m->at.nrows_pad);
   m->s_in.alloc(vec);

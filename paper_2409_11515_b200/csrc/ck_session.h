@@ -134,7 +134,7 @@ struct ck_session_s {
   Header* h_hdr = nullptr;
   cudaGraphExec_t gexec = nullptr;
   int gsteps = 0;
-  std::vector<double> hx;
+  ck::PinnedBuf<double> hx;  // start-vector staging (original order)
   bool observe_on = false;
   ck::DistPart* dist = nullptr;  // owned by the ck_dist group
 

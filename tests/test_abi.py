@@ -59,6 +59,8 @@ def test_rng_mirror_bitwise(port):
     assert np.array_equal(ck.random_unit_vectors(11, 333, 5), port.random_unit_vectors(11, 333, 5))
     # the threaded Box-Muller path (n >= 2^18)
     assert np.array_equal(ck.random_unit_vector(300_000, 4), port.random_unit_vectors(4, 300_000)[0])
+    # several pipeline blocks (2^18 pairs each) and a ragged last block
+    assert np.array_equal(ck.random_unit_vectors(9, 600_001, 2), port.random_unit_vectors(9, 600_001, 2))
 
 
 def test_bounds_match_oracle(port):
