@@ -22,7 +22,8 @@ def sources():
 
 
 def headers():
-    return sorted(glob.glob(os.path.join(PKG, "csrc", "*.h*")) +
+    return sorted(glob.glob(os.path.join(PKG, "csrc", "*.h")) +
+                  glob.glob(os.path.join(PKG, "csrc", "*.cuh")) +
                   glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
