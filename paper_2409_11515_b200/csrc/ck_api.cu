@@ -2,6 +2,7 @@
 // mapping, the host RNG mirror, the scalar error-bound formulas and the
 // estimate_norm orchestration over device sessions.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -148,6 +149,17 @@ void random_unit_vector_host(void* engine, int64_t n, double* out) {
   parallel_for(n, [&](int64_t b, int64_t e) {
     for (int64_t i = b; i < e; ++i) out[i] /= nrm;
   });
+}
+
+// Restart columns per explicit-operator sweep (estimate_norm, cond2, batches).
+// Small operators are launch/latency bound and share one sweep among up to 4
+// restarts; on large ones the R per-entry gathers bound an R-column sweep and
+// two columns per sweep is the measured optimum.
+// CK_RESTART_GROUP overrides (A/B switch).
+static int restart_group(const ck_matrix_s* m) {
+  const char* e = std::getenv("CK_RESTART_GROUP");
+  if (e && e[0] >= '1' && e[0] <= '4') return e[0] - '0';
+  return m->nnz >= (int64_t(1) << 24) ? 2 : kMaxCols;
 }
 
 static void check_cfg(const ck_adam_cfg* cfg) {
@@ -470,8 +482,9 @@ ck_status ck_estimate_norm(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restart
     if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
     M(a);
     bool have = false;
-    for (uint64_t r0 = 0; r0 < restarts; r0 += kMaxCols) {
-      int R = (int)std::min<uint64_t>(kMaxCols, restarts - r0);
+    const int group = restart_group(a);
+    for (uint64_t r0 = 0; r0 < restarts; r0 += group) {
+      int R = (int)std::min<uint64_t>(group, restarts - r0);
       std::vector<uint64_t> seeds(R);
       for (int c = 0; c < R; ++c) {
         uint64_t r = r0 + c;
@@ -523,11 +536,11 @@ static void lu_solve_host(ck_lu_s* f, const double* b, double* x, bool transpose
 // estimate_norm over an already created session kind (restart groups of <= 4).
 template <class MakeSession>
 static void estimate_norm_groups(const ck_adam_cfg* cfg, uint64_t restarts, ck_norm_result* res,
-                                 double* witness, MakeSession&& make) {
+                                 double* witness, int group, MakeSession&& make) {
   if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
   bool have = false;
-  for (uint64_t r0 = 0; r0 < restarts; r0 += kMaxCols) {
-    const int R = (int)std::min<uint64_t>(kMaxCols, restarts - r0);
+  for (uint64_t r0 = 0; r0 < restarts; r0 += group) {
+    const int R = (int)std::min<uint64_t>(group, restarts - r0);
     std::vector<uint64_t> seeds(R);
     for (int c = 0; c < R; ++c) {
       const uint64_t r = r0 + c;
@@ -638,7 +651,7 @@ ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restart
   return guarded([&] {
     check_cfg(cfg);
     LU(f);
-    estimate_norm_groups(cfg, restarts, res, witness, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+    estimate_norm_groups(cfg, restarts, res, witness, kMaxCols, [&](ck_session_s* s, const uint64_t* seeds, int R) {
       session_create_inverse(s, f, cfg, seeds, R);
     });
   });
@@ -653,7 +666,7 @@ ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, doubl
     check_cfg(cfg);
     ck_matrix_s* m = M(a);
     if (m->nrows != m->ncols) fail(CK_ERR_DIMENSION, "cond2: matrix must be square");
-    estimate_norm_groups(cfg, restarts, fwd, nullptr, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+    estimate_norm_groups(cfg, restarts, fwd, nullptr, restart_group(m), [&](ck_session_s* s, const uint64_t* seeds, int R) {
       session_create(s, m, cfg, seeds, R);
     });
     *inv = ck_norm_result{};
@@ -671,7 +684,7 @@ ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, doubl
     }
     ck_adam_cfg ci = *cfg;
     ci.seed = ck_mix_seed(cfg->seed, 0x1234);
-    estimate_norm_groups(&ci, restarts, inv, nullptr, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+    estimate_norm_groups(&ci, restarts, inv, nullptr, kMaxCols, [&](ck_session_s* s, const uint64_t* seeds, int R) {
       session_create_inverse(s, &f, &ci, seeds, R);
     });
     *kappa = fwd->value * inv->value;
@@ -764,8 +777,9 @@ ck_status ck_estimate_norm_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg
     if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
     ck_matrix_s* m = M(a);
     std::vector<char> have((size_t)nseg, 0);
-    for (uint64_t r0 = 0; r0 < restarts; r0 += kMaxCols) {
-      const int R = (int)std::min<uint64_t>(kMaxCols, restarts - r0);
+    const int group = restart_group(m);
+    for (uint64_t r0 = 0; r0 < restarts; r0 += group) {
+      const int R = (int)std::min<uint64_t>(group, restarts - r0);
       std::vector<uint64_t> seeds((size_t)nseg * R);
       for (int g = 0; g < nseg; ++g)
         for (int c = 0; c < R; ++c) {
