@@ -48,6 +48,7 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc")]
     if prof:
         flags.insert(0, "-DCK_SWEEP_PROF")
+    flags = os.environ.get("CK_NVCC_FLAGS", "").split() + flags  # A/B builds
     if verbose:
         flags.insert(0, "-Xptxas=-v")
     objdir = os.path.join(ROOT, "build", "prof" if prof else "lib")

@@ -13,9 +13,10 @@
 // for own rows gathers x~ at halo columns, z = A^T y' for own columns gathers
 // y' at halo rows, and every row keeps the reference's summation order, so the
 // sparse products are bit-identical to one device. Per half step:
-//   k_apply (own tiles)  -> allgather partials -> combine + control (every rank)
-//   -> halo exchange of y' -> k_transpose (own tiles) -> allgather partials
-//   -> combine + radial step -> halo exchange of (x, delta) of the live buffer.
+//   k_apply (own tiles) -> one exchange {partials to every rank, y' halo}
+//   -> combine + control (every rank) -> k_transpose (own tiles)
+//   -> one exchange {partials, (x, delta) halo of the buffers the radial step
+//   makes live} -> combine + radial step.
 // Only the reductions change association (per-rank partials merged in rank
 // order, the same on every rank), so results match one device to rounding.
 //
@@ -98,15 +99,8 @@ __global__ void k_unpack_y(int64_t n, int R, const int32_t* __restrict__ pos, co
   y[(int64_t)pos[k / R] * R + k % R] = buf[k];
 }
 
-// (x, delta) of every column's live buffer (ColState::cur)
-__global__ void k_pack_x(int64_t n, int R, const int32_t* __restrict__ pos, const double2* __restrict__ px,
-                         int64_t nc_pad, const ColState* __restrict__ st, double2* buf) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n * R) return;
-  const int r = (int)(k % R);
-  buf[k] = px[((int64_t)st[r].cur * nc_pad + pos[k / R]) * R + r];
-}
-
+// (x, delta) of every column's live buffer (ColState::cur) -- after the
+// transpose control step (unpack side).
 __global__ void k_unpack_x(int64_t n, int R, const int32_t* __restrict__ pos, const double2* __restrict__ buf,
                            int64_t nc_pad, const ColState* __restrict__ st, double2* px) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -115,69 +109,46 @@ __global__ void k_unpack_x(int64_t n, int R, const int32_t* __restrict__ pos, co
   px[((int64_t)st[r].cur * nc_pad + pos[k / R]) * R + r] = buf[k];
 }
 
+// Pack side, before the transpose control step runs: the buffer that step
+// makes live (control_tail_transpose: a gradient column whose x was
+// materialised moves on to nxt; every other column keeps cur).
+__global__ void k_pack_x_next(int64_t n, int R, const int32_t* __restrict__ pos,
+                              const double2* __restrict__ px, int64_t nc_pad,
+                              const ColState* __restrict__ st, double2* buf) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n * R) return;
+  const int r = (int)(k % R);
+  const ColState& c = st[r];
+  const int b = (c.phase == PH_GRAD && c.mat) ? c.nxt : c.cur;
+  buf[k] = px[((int64_t)b * nc_pad + pos[k / R]) * R + r];
+}
+
 static unsigned blocks_for(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + 255) / 256); }
 
 // ------------------------------------------------------------ communication
-// ss: the sessions this process drives (NCCL: exactly one).
-static void comm_allgather(ck_session_s* const* ss, int np, cudaStream_t st) {
-  const DistPart& d0 = *ss[0]->dist;
-  const size_t w = (size_t)partial_words(ss[0]->R);
-  if (d0.nccl) {
-    CK_NCCL(nccl().AllGather(d0.part.p, d0.gather.p, w, ncclDouble, (ncclComm_t)d0.comm, st));
-    return;
-  }
-  for (int q = 0; q < np; ++q)
-    for (int p = 0; p < np; ++p)
-      CK_CUDA(cudaMemcpyAsync(ss[q]->dist->gather.p + (size_t)p * w, ss[p]->dist->part.p,
-                              w * sizeof(double), cudaMemcpyDeviceToDevice, st));
-}
-
-// Halo exchange of y' (x_side = false) or of the live (x, delta) pairs.
-static void comm_exchange(ck_session_s* const* ss, int np, bool x_side, cudaStream_t st) {
+// ss: the sessions this process drives (NCCL: exactly one). One exchange per
+// half step carries both the per-rank reduction partials (an allgather, as
+// point-to-point messages) and the halo of y' (x_side = false) or of the
+// (x, delta) pairs (x_side = true): a single NCCL group, so every half step
+// pays one communication latency.
+static void pack_halo(ck_session_s* const* ss, int np, bool x_side, cudaStream_t st) {
   const int R = ss[0]->R;
-  const size_t esz = x_side ? sizeof(double2) : sizeof(double);  // per entry and column
-  for (int p = 0; p < np; ++p) {  // pack
+  for (int p = 0; p < np; ++p) {
     ck_session_s* s = ss[p];
     DistPart& d = *s->dist;
     const int64_t n = x_side ? d.xs_off.back() : d.ys_off.back();
     if (n == 0) continue;
     if (x_side)
-      k_pack_x<<<blocks_for(n * R), 256, 0, st>>>(n, R, d.xs_pos.p, s->PX.p, s->npad, s->st.p, d.xs_buf.p);
+      k_pack_x_next<<<blocks_for(n * R), 256, 0, st>>>(n, R, d.xs_pos.p, s->PX.p, s->npad, s->st.p,
+                                                      d.xs_buf.p);
     else
       k_pack_y<<<blocks_for(n * R), 256, 0, st>>>(n, R, d.ys_pos.p, s->y.p, d.ys_buf.p);
   }
-  const DistPart& d0 = *ss[0]->dist;
-  if (d0.nccl) {
-    const DistPart& d = d0;
-    const char* sb = x_side ? (const char*)d.xs_buf.p : (const char*)d.ys_buf.p;
-    char* rb = x_side ? (char*)d.xr_buf.p : (char*)d.yr_buf.p;
-    const auto& so = x_side ? d.xs_off : d.ys_off;
-    const auto& ro = x_side ? d.xr_off : d.yr_off;
-    const size_t words = esz / sizeof(double) * R;  // doubles per entry
-    CK_NCCL(nccl().GroupStart());
-    for (int q = 0; q < d.nranks; ++q) {
-      if (q == d.rank) continue;
-      const int64_t ns = so[q + 1] - so[q], nr = ro[q + 1] - ro[q];
-      if (ns) CK_NCCL(nccl().Send(sb + so[q] * esz * R, ns * words, ncclDouble, q, (ncclComm_t)d.comm, st));
-      if (nr) CK_NCCL(nccl().Recv(rb + ro[q] * esz * R, nr * words, ncclDouble, q, (ncclComm_t)d.comm, st));
-    }
-    CK_NCCL(nccl().GroupEnd());
-  } else {
-    for (int p = 0; p < np; ++p)
-      for (int q = 0; q < np; ++q) {
-        const DistPart& a = *ss[p]->dist;  // sender
-        DistPart& b = *ss[q]->dist;        // receiver
-        const auto& so = x_side ? a.xs_off : a.ys_off;
-        const auto& ro = x_side ? b.xr_off : b.yr_off;
-        const int64_t ns = so[q + 1] - so[q];
-        if (ns == 0) continue;
-        if (ro[p + 1] - ro[p] != ns) fail(CK_ERR_LOGIC, "halo lists of two ranks disagree");
-        const char* src = (x_side ? (const char*)a.xs_buf.p : (const char*)a.ys_buf.p) + so[q] * esz * R;
-        char* dst = (x_side ? (char*)b.xr_buf.p : (char*)b.yr_buf.p) + ro[p] * esz * R;
-        CK_CUDA(cudaMemcpyAsync(dst, src, ns * esz * R, cudaMemcpyDeviceToDevice, st));
-      }
-  }
-  for (int q = 0; q < np; ++q) {  // unpack
+}
+
+static void unpack_halo(ck_session_s* const* ss, int np, bool x_side, cudaStream_t st) {
+  const int R = ss[0]->R;
+  for (int q = 0; q < np; ++q) {
     ck_session_s* s = ss[q];
     DistPart& d = *s->dist;
     const int64_t n = x_side ? d.xr_off.back() : d.yr_off.back();
@@ -189,18 +160,65 @@ static void comm_exchange(ck_session_s* const* ss, int np, bool x_side, cudaStre
   }
 }
 
+static void transfer(ck_session_s* const* ss, int np, bool x_side, cudaStream_t st) {
+  const int R = ss[0]->R;
+  const size_t w = (size_t)partial_words(R);
+  const size_t esz = x_side ? sizeof(double2) : sizeof(double);  // per entry and column
+  const DistPart& d0 = *ss[0]->dist;
+  if (d0.nccl) {
+    const DistPart& d = d0;
+    CK_CUDA(cudaMemcpyAsync(d.gather.p + (size_t)d.rank * w, d.part.p, w * sizeof(double),
+                            cudaMemcpyDeviceToDevice, st));
+    const char* sb = x_side ? (const char*)d.xs_buf.p : (const char*)d.ys_buf.p;
+    char* rb = x_side ? (char*)d.xr_buf.p : (char*)d.yr_buf.p;
+    const auto& so = x_side ? d.xs_off : d.ys_off;
+    const auto& ro = x_side ? d.xr_off : d.yr_off;
+    const size_t words = esz / sizeof(double) * R;  // doubles per entry
+    CK_NCCL(nccl().GroupStart());
+    for (int q = 0; q < d.nranks; ++q) {
+      if (q == d.rank) continue;
+      CK_NCCL(nccl().Send(d.part.p, w, ncclDouble, q, (ncclComm_t)d.comm, st));
+      CK_NCCL(nccl().Recv(d.gather.p + (size_t)q * w, w, ncclDouble, q, (ncclComm_t)d.comm, st));
+      const int64_t ns = so[q + 1] - so[q], nr = ro[q + 1] - ro[q];
+      if (ns) CK_NCCL(nccl().Send(sb + so[q] * esz * R, ns * words, ncclDouble, q, (ncclComm_t)d.comm, st));
+      if (nr) CK_NCCL(nccl().Recv(rb + ro[q] * esz * R, nr * words, ncclDouble, q, (ncclComm_t)d.comm, st));
+    }
+    CK_NCCL(nccl().GroupEnd());
+    return;
+  }
+  for (int q = 0; q < np; ++q)  // partials
+    for (int p = 0; p < np; ++p)
+      CK_CUDA(cudaMemcpyAsync(ss[q]->dist->gather.p + (size_t)p * w, ss[p]->dist->part.p,
+                              w * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  for (int p = 0; p < np; ++p)  // halos
+    for (int q = 0; q < np; ++q) {
+      const DistPart& a = *ss[p]->dist;  // sender
+      DistPart& b = *ss[q]->dist;        // receiver
+      const auto& so = x_side ? a.xs_off : a.ys_off;
+      const auto& ro = x_side ? b.xr_off : b.yr_off;
+      const int64_t ns = so[q + 1] - so[q];
+      if (ns == 0) continue;
+      if (ro[p + 1] - ro[p] != ns) fail(CK_ERR_LOGIC, "halo lists of two ranks disagree");
+      const char* src = (x_side ? (const char*)a.xs_buf.p : (const char*)a.ys_buf.p) + so[q] * esz * R;
+      char* dst = (x_side ? (char*)b.xr_buf.p : (char*)b.yr_buf.p) + ro[p] * esz * R;
+      CK_CUDA(cudaMemcpyAsync(dst, src, ns * esz * R, cudaMemcpyDeviceToDevice, st));
+    }
+}
+
 // One Projected-Adam iteration of every rank in ss.
 static void run_step(ck_session_s* const* ss, int np, cudaStream_t st) {
   for (int p = 0; p < np; ++p) launch_apply_only(ss[p], st);
-  comm_allgather(ss, np, st);
+  pack_halo(ss, np, false, st);
+  transfer(ss, np, false, st);  // apply partials + y' halo
   for (int p = 0; p < np; ++p)
     launch_dist_control(ss[p], true, ss[p]->dist->gather.p, ss[p]->dist->nranks, st);
-  comm_exchange(ss, np, false, st);
+  unpack_halo(ss, np, false, st);
   for (int p = 0; p < np; ++p) launch_transpose_only(ss[p], st);
-  comm_allgather(ss, np, st);
+  pack_halo(ss, np, true, st);  // the buffers the control step below makes live
+  transfer(ss, np, true, st);   // transpose partials + (x, delta) halo
   for (int p = 0; p < np; ++p)
     launch_dist_control(ss[p], false, ss[p]->dist->gather.p, ss[p]->dist->nranks, st);
-  comm_exchange(ss, np, true, st);
+  unpack_halo(ss, np, true, st);
   CK_CUDA(cudaGetLastError());
 }
 
