@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
     cb = slice_cbase<NW>(a.A, i >> 5);
   }
   for (int tile = tile0; tile < tend; tile += stride, i += istep) {
-    const int64_t base = sp0 + (i & 31);
+    const int64_t base = sell_rowbase(sp0, i);
     const int w = (int)((sp1 - sp0) >> 5);  // slice width: uniform across the warp
     const int Lc = L, cbc = cb;
     const int64_t inext = i + istep;
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     cb = slice_cbase<NW>(a.AT, j >> 5);
   }
   for (int tile = tile0; tile < tend; tile += stride, j += jstep) {
-    const int64_t base = sp0 + (j & 31);
+    const int64_t base = sell_rowbase(sp0, j);
     const int w = (int)((sp1 - sp0) >> 5);
     const int Lc = L, cbc = cb;
     if (tile + stride < tend) {

@@ -118,10 +118,12 @@ struct DBuf {
 
 // Sliced-ELL (SELL-32-256) layout of a sparse operator. Rows are permuted
 // inside each 256-row tile by descending length (stable), so every 32-row slice
-// is nearly uniform; slice s stores entry j of its lane-th row at
-// slice_ptr[s] + 32*j + lane, which makes each warp load one contiguous
-// 256-byte run of values and a 128-byte (wide) or 64-byte (narrow) run of
-// column indices.
+// is nearly uniform. Slice widths are even and entries are interleaved in
+// pairs: entry j of the slice's lane-th row sits at
+//   slice_ptr[s] + 2*lane + 64*(j/2) + (j%2)          (sell_at below),
+// so a lane's entries 2m, 2m+1 are adjacent -- one 16-byte value load and one
+// 4-byte (narrow) or 8-byte (wide) column load -- and a warp's pair of entry
+// rows is one contiguous 512-byte run of values.
 //
 // Column indices come in two formats, chosen per operator at build time:
 //   wide    int32 column (12 bytes per stored entry with the value);
@@ -145,6 +147,14 @@ struct Sell {
   DBuf<int32_t> perm;       // perm[k] = original row at permuted position k (-1 = pad)
   DBuf<int32_t> inv;        // inv[row] = permuted position
 };
+
+// Position of stored entry j of a row whose row base is slice_ptr[s] + 2*lane.
+__host__ __device__ __forceinline__ int64_t sell_at(int64_t rowbase, int64_t j) {
+  return rowbase + ((j >> 1) << 6) + (j & 1);
+}
+__host__ __device__ __forceinline__ int64_t sell_rowbase(int64_t slice_start, int64_t row) {
+  return slice_start + 2 * (row & 31);
+}
 
 struct SellView {
   const int64_t* __restrict__ sp;

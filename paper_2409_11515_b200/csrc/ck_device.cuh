@@ -208,24 +208,37 @@ __device__ __forceinline__ int sell_col(const SellView& A, int64_t s, int64_t k)
   return A.narrow ? A.cbase[s] + (int)A.col16[k] : A.col[k];
 }
 
-// Loads U consecutive stored entries (stored positions j0..j0+U-1) of a
-// sliced-ELL row. All loads of the chunk are issued before any use; positions at
-// or beyond the warp-uniform slice width w are predicated off and read as
-// (column cb, value 0). Padding inside [len, w) is stored as (cb, 0.0), so the
-// gathers that follow never need a bounds check. NW selects the narrow column
-// format (cb = the slice's base column).
+// Loads U consecutive stored entries (stored positions j0..j0+U-1, j0 and U
+// even) of a sliced-ELL row with row base `base` (sell_rowbase): U/2 16-byte
+// value loads and U/2 column-pair loads, all issued before any use. Positions
+// at or beyond the warp-uniform (even) slice width w are predicated off and
+// read as (column cb, value 0). Padding inside [len, w) is stored as (cb, 0.0),
+// so the gathers that follow never need a bounds check. NW selects the narrow
+// column format (cb = the slice's base column; 0 for wide).
 template <int U, bool NW>
 __device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int cb, int j0, int w,
                                            int* c, double* v) {
+  static_assert(U % 2 == 0, "chunks cover whole entry pairs");
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const bool ok = j0 + u < w;
-    const int64_t k = base + (int64_t)(j0 + u) * kSlice;
-    if (NW)
-      c[u] = cb + (ok ? ld_stream(A.col16 + k) : 0);
-    else
-      c[u] = ok ? ld_stream(A.col + k) : 0;
-    v[u] = ok ? ld_stream(A.val + k) : 0.0;
+  for (int m = 0; m < U / 2; ++m) {
+    const int j = j0 + 2 * m;
+    const bool ok = j < w;
+    const int64_t k = sell_at(base, j);
+    double2 vv = make_double2(0.0, 0.0);
+    if (ok) vv = __ldcs(reinterpret_cast<const double2*>(A.val + k));
+    v[2 * m] = vv.x;
+    v[2 * m + 1] = vv.y;
+    if (NW) {
+      ushort2 cc = make_ushort2(0, 0);
+      if (ok) cc = __ldcs(reinterpret_cast<const ushort2*>(A.col16 + k));
+      c[2 * m] = cb + (int)cc.x;
+      c[2 * m + 1] = cb + (int)cc.y;
+    } else {
+      int2 cc = make_int2(0, 0);
+      if (ok) cc = __ldcs(reinterpret_cast<const int2*>(A.col + k));
+      c[2 * m] = cc.x;
+      c[2 * m + 1] = cc.y;
+    }
   }
 }
 

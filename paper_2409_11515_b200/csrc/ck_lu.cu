@@ -38,11 +38,11 @@ __global__ void k_band_bounds(SellView A, int64_t nrows_pad, const int32_t* __re
   if (p >= nrows_pad) return;
   const int32_t row = rperm[p];
   if (row < 0) return;
-  const int64_t base = A.sp[p >> 5] + (p & 31);
+  const int64_t base = sell_rowbase(A.sp[p >> 5], p);
   const int L = A.len[p];
   int lo = 0, up = 0;
   for (int j = 0; j < L; ++j) {
-    const int32_t col = cperm[sell_col(A, p >> 5, base + (int64_t)j * kSlice)];
+    const int32_t col = cperm[sell_col(A, p >> 5, sell_at(base, j))];
     lo = max(lo, row - col);
     up = max(up, col - row);
   }
@@ -56,10 +56,10 @@ __global__ void k_band_fill(SellView A, int64_t nrows_pad, const int32_t* __rest
   if (p >= nrows_pad) return;
   const int32_t row = rperm[p];
   if (row < 0) return;
-  const int64_t base = A.sp[p >> 5] + (p & 31);
+  const int64_t base = sell_rowbase(A.sp[p >> 5], p);
   const int L = A.len[p];
   for (int j = 0; j < L; ++j) {
-    const int64_t k = base + (int64_t)j * kSlice;
+    const int64_t k = sell_at(base, j);
     AB(b, row, cperm[sell_col(A, p >> 5, k)]) = A.val[k];
   }
 }

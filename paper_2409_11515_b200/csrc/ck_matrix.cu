@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kTile) k_tile_sort(int64_t n, const int32_t* _
 // widest. The last element (index nslices) is left for the exclusive scan total.
 __global__ void k_slice_entries(int64_t nslices, const uint16_t* __restrict__ len, int64_t* cnt) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s < nslices) cnt[s] = (int64_t)len[s * kSlice] * kSlice;
+  if (s < nslices) cnt[s] = (((int64_t)len[s * kSlice] + 1) & ~int64_t(1)) * kSlice;  // even widths
   if (s == nslices) cnt[s] = 0;
 }
 
@@ -132,7 +132,7 @@ __global__ void k_sell_fill(int64_t nrows_pad, const int32_t* __restrict__ perm,
   int32_t row = perm[k];
   int64_t src = row >= 0 ? rp[row] : 0;
   for (int j = 0; j < w; ++j) {
-    int64_t d = base + (int64_t)j * kSlice + lane;
+    int64_t d = sell_at(base + 2 * lane, j);
     if (j < L) {
       scol[d] = colmap[ci[src + j]];
       sval[d] = va[src + j];
@@ -151,11 +151,11 @@ __global__ void k_slice_span(int64_t nslices, const int64_t* __restrict__ sp,
   const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= nslices) return;  // warp-uniform
-  const int64_t base = sp[s] + lane;
+  const int64_t base = sp[s] + 2 * lane;
   const int L = len[s * kSlice + lane];
   int lo = 0x7fffffff, hi = -1;
   for (int j = 0; j < L; ++j) {
-    const int c = col[base + (int64_t)j * kSlice];
+    const int c = col[sell_at(base, j)];
     lo = min(lo, c);
     hi = max(hi, c);
   }
@@ -176,11 +176,11 @@ __global__ void k_narrow_cols(int64_t nrows_pad, const int64_t* __restrict__ sp,
                               const int32_t* __restrict__ col, uint16_t* col16) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nrows_pad) return;
-  const int64_t slice = k >> 5, base = sp[slice] + (k & 31);
+  const int64_t slice = k >> 5, base = sell_rowbase(sp[slice], k);
   const int w = (int)((sp[slice + 1] - sp[slice]) >> 5), L = len[k];
   const int b = cbase[slice];
   for (int j = 0; j < w; ++j) {
-    const int64_t d = base + (int64_t)j * kSlice;
+    const int64_t d = sell_at(base, j);
     col16[d] = (uint16_t)(j < L ? col[d] - b : 0);
   }
 }
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kTile) k_sell_spmv(SellView A, int64_t nrows_p
   int64_t row = blockIdx.x * (int64_t)kTile + threadIdx.x;
   if (row >= nrows_pad) return;
   const int64_t s0 = A.sp[row >> 5], s1 = A.sp[(row >> 5) + 1];
-  const int64_t base = s0 + (row & 31);
+  const int64_t base = sell_rowbase(s0, row);
   const int w = (int)((s1 - s0) >> 5);
   const int L = A.len[row];
   const int cb = slice_cbase<NW>(A, row >> 5);

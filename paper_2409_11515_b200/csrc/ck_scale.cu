@@ -20,11 +20,11 @@ template <bool kColumn>
 __global__ void __launch_bounds__(256) k_sell_norms(int64_t nrows_pad, SellView s, double* out) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= nrows_pad) return;
-  const int64_t base = s.sp[r / kSlice] + (r % kSlice);
+  const int64_t base = sell_rowbase(s.sp[r / kSlice], r);
   const int len = s.len[r];
   double amax = 0.0;
   for (int j = 0; j < len; ++j) {
-    const double a = fabs(s.val[base + (int64_t)kSlice * j]);
+    const double a = fabs(s.val[sell_at(base, j)]);
     amax = amax < a ? a : amax;  // std::max(amax, |x|)
   }
   if (amax == 0.0) {
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) k_sell_norms(int64_t nrows_pad, SellView 
   }
   double sum = 0.0;
   for (int j = 0; j < len; ++j) {
-    const double q = __ddiv_rn(s.val[base + (int64_t)kSlice * j], amax);
+    const double q = __ddiv_rn(s.val[sell_at(base, j)], amax);
     sum = __dadd_rn(sum, __dmul_rn(q, q));
   }
   out[r] = __dmul_rn(amax, __dsqrt_rn(sum));
