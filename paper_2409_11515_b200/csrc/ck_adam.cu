@@ -781,8 +781,11 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
   tr.mark("remaining columns", st);
   push_state(s);
   // chunk length: about 4 ms of device work per host round trip, 4..256 steps
-  const int steps =
-      (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
+  // bytes_per_step < 0: a fixed chunk of -bytes_per_step steps (latency-bound
+  // loops, where streamed bytes say nothing about the step time)
+  const int steps = bytes_per_step < 0
+                        ? (int)-bytes_per_step
+                        : (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
   build_graph(s, steps);
   tr.mark("graph capture", st);
 }
@@ -928,7 +931,6 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
   s->seg_pad.assign(S, 0);
   int64_t off = 0;
   size_t smem = 0;
-  double bytes_per_step = 0.0;
   for (int g = 0; g < S; ++g) {
     const int64_t n = lus[g]->n;
     s->seg_n[g] = n;
@@ -936,7 +938,6 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
     s->seg_pad[g] = S == 1 ? n : ceil_div(n, 32) * 32;
     off += s->seg_pad[g];
     smem = std::max(smem, inv_step_smem(lus[g]->view(), R));
-    bytes_per_step += 8.0 * 4.0 * (double)(2 * lus[g]->kl + lus[g]->ku + 1) * (double)n;
   }
   s->npad = off;
   s->n = S == 1 ? s->seg_n[0] : off;
@@ -970,7 +971,9 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
   }
   s->dargs.alloc(S);
   CK_CUDA(cudaMemcpy(s->dargs.p, h.data(), sizeof(InvArgs) * S, cudaMemcpyHostToDevice));
-  session_init_common(s, cfg, seeds, yw, bytes_per_step * 50.0);
+  // the sweeps are a latency chain (~0.1-0.5 ms per step): 32 steps per graph
+  // chunk keep the host round trips (restart service, termination) negligible
+  session_init_common(s, cfg, seeds, yw, -32.0);
 }
 
 void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg,

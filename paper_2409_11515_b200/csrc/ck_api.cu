@@ -533,6 +533,19 @@ static void lu_solve_host(ck_lu_s* f, const double* b, double* x, bool transpose
   CK_CUDA(cudaStreamSynchronize(st));
 }
 
+// InverseOracle restarts run as separate members of one batch session -- one
+// CTA each, sharing the factors -- rather than as columns of one sweep: the
+// sweeps are a latency chain, so R columns on one CTA cost ~1.5x a single one
+// while R CTAs run side by side. Column k of the session is restart k.
+constexpr int kInvRestartGroup = 64;
+void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S, const ck_adam_cfg* cfg,
+                                  const uint64_t* seeds, int R);
+static void inverse_restarts_session(ck_session_s* s, ck_lu_s* f, const ck_adam_cfg* cfg,
+                                     const uint64_t* seeds, int restarts) {
+  std::vector<ck_lu_s*> lus((size_t)restarts, f);
+  session_create_inverse_batch(s, lus.data(), restarts, cfg, seeds, 1);
+}
+
 // estimate_norm over an already created session kind (restart groups of <= 4).
 template <class MakeSession>
 static void estimate_norm_groups(const ck_adam_cfg* cfg, uint64_t restarts, ck_norm_result* res,
@@ -651,8 +664,8 @@ ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restart
   return guarded([&] {
     check_cfg(cfg);
     LU(f);
-    estimate_norm_groups(cfg, restarts, res, witness, kMaxCols, [&](ck_session_s* s, const uint64_t* seeds, int R) {
-      session_create_inverse(s, f, cfg, seeds, R);
+    estimate_norm_groups(cfg, restarts, res, witness, kInvRestartGroup, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+      inverse_restarts_session(s, f, cfg, seeds, R);
     });
   });
 }
@@ -684,8 +697,8 @@ ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, doubl
     }
     ck_adam_cfg ci = *cfg;
     ci.seed = ck_mix_seed(cfg->seed, 0x1234);
-    estimate_norm_groups(&ci, restarts, inv, nullptr, kMaxCols, [&](ck_session_s* s, const uint64_t* seeds, int R) {
-      session_create_inverse(s, &f, &ci, seeds, R);
+    estimate_norm_groups(&ci, restarts, inv, nullptr, kInvRestartGroup, [&](ck_session_s* s, const uint64_t* seeds, int R) {
+      inverse_restarts_session(s, &f, &ci, seeds, R);
     });
     *kappa = fwd->value * inv->value;
     *has_factors = 1;

@@ -13,4 +13,4 @@ for name, a in [("c1", configs.config(1)), ("c5m0", configs.ensemble_member(0, 1
     steps = 40 if name != "c2" else 10
     ms, _, _ = s.time(steps, 1)
     print(f"{name}: n={f.n} kl={f.kl} ku={f.ku} factor {tf:.3f}s  inverse iteration {ms/steps:.3f} ms"
-          f"  (2000 its: {2*ms:.1f} s)", flush=True)
+          f"  (2000 its: {2 * ms / steps:.1f} s)", flush=True)
