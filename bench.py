@@ -345,31 +345,49 @@ def run_ours(args):
     t_up = time.perf_counter() - t_up
     info = dev.info()
     if ensemble:
+        # the restarts in groups of restart columns per sweep, as estimate_norm_batch
+        # runs them (restart_group, ck_api.cu: 2 per sweep above 2^24 nonzeros)
         ms = batch.member_seeds(configs.CONFIGS[5]["count"])
-        seeds = [ms[i] if r == 0 else ck.mix_seed(ms[i], r) for i in member_idx for r in range(R)]
-        sess = batch.BatchSession(packed, cfg, seeds)
+        rg = 2 if a.nnz >= (1 << 24) else R
+        groups = [list(range(r0, min(R, r0 + rg))) for r0 in range(0, R, rg)]
+        sessions = [batch.BatchSession(packed, cfg, [ms[i] if r == 0 else ck.mix_seed(ms[i], r)
+                                                     for i in member_idx for r in g])
+                    for g in groups]
     else:
-        sess = ck.Session(ck.ExplicitOracle(a), cfg, [seed])
-    sess.run(args.warmup)
+        groups = [[0]]
+        sessions = [ck.Session(ck.ExplicitOracle(a), cfg, [seed])]
+    for sess in sessions:
+        sess.run(args.warmup)
     barrier()
     sampler = ClockSampler(local) if rank == 0 else None
-    # value: the product loop as it runs (CUDA-graph chunks of whole steps)
-    ms_total, _, _ = sess.time(args.steps, mode=1)
+    # value: the product loop as it runs (CUDA-graph chunks of whole steps); a step
+    # of the ensemble advances every restart group once
+    ms_total = sum(sess.time(args.steps, mode=1)[0] for sess in sessions)
     barrier()
     clocks = sampler.stop() if sampler else None
     ms_max = allmax(ms_total)
     # kernel split (events between the two kernels, no graph) for the roofline
-    _, ms_apply, ms_tr = sess.time(args.steps, mode=0)
+    ms_apply = ms_tr = 0.0
+    for sess in sessions:
+        _, ma, mt = sess.time(args.steps, mode=0)
+        ms_apply += ma
+        ms_tr += mt
     runs_per_step = (len(member_idx) * R) if ensemble else 1
     total_runs = allsum(runs_per_step) if ensemble else world
     value = total_runs * args.steps / (ms_max / 1000.0)
-    sess.close()
+    for sess in sessions:
+        sess.close()
 
     n, nnz = a.nrows, a.nnz
-    b_apply, b_tr = bytes_per_iteration(nnz, n, R, info["col_format"])
+    b_apply = b_tr = 0
+    for g in groups:
+        ba, bt = bytes_per_iteration(nnz, n, len(g), info["col_format"])
+        b_apply += ba
+        b_tr += bt
     peak, peak_kind = measured_peaks()
-    k_apply = {"name": f"k_apply<{R}>", "ms_avg": ms_apply / args.steps, "bytes": b_apply}
-    k_tr = {"name": f"k_transpose<{R}>", "ms_avg": ms_tr / args.steps, "bytes": b_tr}
+    rg_name = len(groups[0])
+    k_apply = {"name": f"k_apply<{rg_name}>", "ms_avg": ms_apply / args.steps, "bytes": b_apply}
+    k_tr = {"name": f"k_transpose<{rg_name}>", "ms_avg": ms_tr / args.steps, "bytes": b_tr}
     for k in (k_apply, k_tr):
         k["gbs"] = k["bytes"] / (k["ms_avg"] / 1000.0) / 1e9
         k["frac"] = k["gbs"] / peak
@@ -438,6 +456,7 @@ def run_ours(args):
             "config": {"workload": name, "n": n, "nnz": nnz, "path": "sigma_max",
                        "adam": "alpha=1e-2,beta1=.9,beta2=.999,eps=1e-8",
                        "runs_per_step": runs_per_step,
+                       "restart_groups": [len(g) for g in groups],
                        "parallelism": (f"members sharded over {world} ranks" if ensemble else
                                        f"replicas{world} (independent restart streams)"),
                        "col_format": {0: "int32", 1: "A uint16", 2: "A^T uint16",
@@ -452,7 +471,7 @@ def run_ours(args):
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 2 * args.steps * len(groups),
             "setup_s": {"generate": t_gen, "upload_and_build": t_up},
         }
         print(json.dumps(line), flush=True)

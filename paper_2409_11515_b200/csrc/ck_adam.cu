@@ -50,8 +50,11 @@ constexpr int kPT = 1;  // per-column partials of k_transpose
 // every result bit -- is the same on every device.
 template <int R>
 struct Occ {
-  static constexpr int apply = R == 1 ? 4 : 2;
-  static constexpr int transpose = R <= 2 ? 4 : 3;  // R >= 3: latency-bound, 3 CTAs beat the spill-free 2
+  // measured optima (config 4 and config 5, scripts/ab_restarts.py): R = 1 and
+  // R = 3 want the full 4 CTAs; R = 2 apply 3; R = 4 apply is latency-bound at
+  // 2 (more CTAs spill); every transpose runs 4 CTAs
+  static constexpr int apply = R == 1 || R == 3 ? 4 : R == 2 ? 3 : 2;
+  static constexpr int transpose = 4;
 };
 
 // Work assignment of CTA `unit`. One operator (S == 1): the tiles are dealt
