@@ -166,3 +166,16 @@ def test_rectangular(port):
     r, cidx = np.nonzero(d)
     a = ck.SparseMatrix.from_coo(30, 50, r, cidx, d[r, cidx])
     _cmp(port, a, M.cfg(seed=3), tol=1e-9)
+
+
+def test_restart_grouping_is_invisible(port, monkeypatch):
+    """Restart columns per sweep (CK_RESTART_GROUP) change nothing on a
+    one-tile operator: every restart is the same run."""
+    a = M.random_sparse(port, 40, 0.15, 21)
+    c = M.cfg(seed=5)
+    ref = ck.estimate_norm(ck.ExplicitOracle(a), c, 4)
+    for g in ("1", "2", "3"):
+        monkeypatch.setenv("CK_RESTART_GROUP", g)
+        e = ck.estimate_norm(ck.ExplicitOracle(a), c, 4)
+        assert e.value == ref.value and e.iterations == ref.iterations
+        assert np.array_equal(e.witness, ref.witness)

@@ -228,3 +228,21 @@ def test_verify_solution_vs_oracle(port):
         ck.verify_solution(a, np.zeros(40), b)
     with pytest.raises(ck.ZeroRHS):
         ck.verify_solution(a, xh, np.zeros(40))
+
+
+def test_inverse_restarts_are_separate_runs(port):
+    """estimate_norm on the InverseOracle runs every restart on its own CTA
+    (batch members sharing the factors): the best restart is bit-identical to
+    the separately seeded run (condest.hpp:301-312)."""
+    a = M.row_scaled(M.laplacian2d(12), port, 3)
+    f = ck.lu_factorize(a, 1e-14)
+    c = M.cfg(alpha=1e-2, max_iter=300, patience=300, seed=11)
+    comb = ck.estimate_norm(ck.InverseOracle(f), c, 4)
+    best = None
+    for r in range(4):
+        cr = M.cfg(alpha=1e-2, max_iter=300, patience=300, seed=11 if r == 0 else ck.mix_seed(11, r))
+        e = ck.projected_adam(ck.InverseOracle(f), cr)
+        if best is None or e.value > best.value:
+            best = e
+    assert comb.value == best.value and comb.iterations == best.iterations
+    assert np.array_equal(comb.witness, best.witness)
