@@ -964,6 +964,7 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
     a.ring_size = lu_ring_size(b);
     a.b.stage_cap = (int64_t)(smem / sizeof(double)) - stage_offset(R, a.ring_size);
     if (a.b.stage_cap < 0) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+    a.b.stage_min = lu_stage_min();
     a.PX = s->PX.p + o * R;
     a.pstride = s->npad * R;
     a.MV = s->MV.p + o * R;

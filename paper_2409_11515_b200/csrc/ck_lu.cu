@@ -292,6 +292,17 @@ size_t lu_solve_smem(const BandView& b, int R) {
   return std::min(kSolveDynMax, sizeof(double) * (size_t)(base + full));
 }
 
+// Coefficient runs shorter than this are read straight from L2/HBM: for narrow
+// bands the TMA stage's issue and completion latency outweighs the traffic it
+// saves (config 1, runs of 64 and 128 rows: 1.78 vs 2.10 ms per inverse
+// iteration unstaged); wide bands need it (config-5 member, runs of 255 and 510
+// rows: 72.7 ms staged vs 83.0 with the 255-row runs unstaged, 103 with none
+// staged; config 2 339 vs 465 ms). CK_LU_STAGE_MIN overrides (A/B).
+int64_t lu_stage_min() {
+  if (const char* e = std::getenv("CK_LU_STAGE_MIN")) return std::atoll(e);
+  return kLUStageMinRows;
+}
+
 int64_t lu_stage_cap(const BandView& b, int R) {
   return (int64_t)(lu_solve_smem(b, R) / sizeof(double)) - stage_offset(R, lu_ring_size(b));
 }
@@ -303,6 +314,7 @@ void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaSt
   const int ring = lu_ring_size(b);
   const size_t smem = lu_solve_smem(b, R);
   b.stage_cap = lu_stage_cap(b, R);
+  b.stage_min = lu_stage_min();
   if (b.stage_cap < 0) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
   double* xs[4] = {x[0], R > 1 ? x[1] : nullptr, R > 2 ? x[2] : nullptr, R > 3 ? x[3] : nullptr};
   switch (R) {

@@ -31,6 +31,8 @@ struct BandView {
   // doubles of dynamic shared memory the solve CTA has for its TMA stage
   // (set by the launcher, see lu_solve_smem)
   int64_t stage_cap;
+  // runs shorter than this many rows are read directly instead of staged
+  int64_t stage_min;
 };
 
 struct LUStatus {
@@ -43,6 +45,8 @@ struct LUStatus {
 };
 
 constexpr int kLUBlock = 32;  // panel width / solve block
+constexpr int64_t kLUStageMinRows = 129;  // runs of <= 128 rows unstaged; lu_stage_min (ck_lu.cu)
+int64_t lu_stage_min();
 
 // Raise a kernel's dynamic shared-memory ceiling to everything the SM has
 // left beside its static shared memory. Always the same value, so concurrent

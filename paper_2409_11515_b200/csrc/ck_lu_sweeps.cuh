@@ -70,9 +70,9 @@ struct Stage {
   int64_t srows = 0, sld = 2;
   uint32_t parity = 0;
 
-  __device__ void layout(int64_t cap, int64_t len) {
+  __device__ void layout(int64_t cap, int64_t len, int64_t min_len) {
     const int64_t rows_fit = ((cap / kLUBlock) & ~(int64_t)1) - 2;
-    srows = lmax(0, lmin(len, rows_fit));
+    srows = len < min_len ? 0 : lmax(0, lmin(len, rows_fit));
     sld = (srows + 3) & ~(int64_t)1;
   }
   __device__ __forceinline__ uint32_t copy_bytes(int64_t first) const {
@@ -650,14 +650,14 @@ __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, d
   S.st = smem + stage_offset(R, ring_size);
   S.bar = &mbar;
   if (!transpose) {
-    S.layout(b.stage_cap, b.kl);
+    S.layout(b.stage_cap, b.kl, b.stage_min);
     sweep_l_forward<R>(b, x, ring, H, S);
-    S.layout(b.stage_cap, b.kv);
+    S.layout(b.stage_cap, b.kv, b.stage_min);
     sweep_u_backward<R>(b, x, ring, H, S);
   } else {
-    S.layout(b.stage_cap, b.kv);
+    S.layout(b.stage_cap, b.kv, b.stage_min);
     sweep_ut_forward<R>(b, x, ring, s_dot, H, S);
-    S.layout(b.stage_cap, b.kl);
+    S.layout(b.stage_cap, b.kl, b.stage_min);
     sweep_l_backward<R>(b, x, ring, s_dot, H, S);
   }
 }
