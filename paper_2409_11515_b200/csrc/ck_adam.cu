@@ -500,7 +500,8 @@ static void launch_transpose_r(const ck_session_s* s, cudaStream_t st) {
     k_transpose<R, false><<<s->args.units_T, kTile, 0, st>>>(s->args);
 }
 
-void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st);
+void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st, int cl);
+int inv_cluster_size(const BandView& b, int S, int R, size_t smem);
 void prepare_inv_step(size_t smem, int R);
 size_t inv_step_smem(const BandView& b, int R);
 int lu_ring_size(const BandView& b);
@@ -508,7 +509,7 @@ int64_t lu_stage_cap(const BandView& b, int R);
 void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st);
 
 static void launch_inv_half(ck_session_s* s, int half, cudaStream_t st) {
-  launch_inv_step(s->dargs.p, s->S, s->R, s->inv_smem, half, st);
+  launch_inv_step(s->dargs.p, s->S, s->R, s->inv_smem, half, st, s->inv_cl);
 }
 
 void launch_apply_only(ck_session_s* s, cudaStream_t st) {
@@ -948,6 +949,16 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
                   cfg->patience};
   s->inv_smem = smem;
   prepare_inv_step(smem, R);
+  // widest band of the batch decides the cluster split of the sweeps
+  BandView wide = lus[0]->view();
+  for (int g = 1; g < S; ++g)
+    if (lus[g]->kl + lus[g]->ku > wide.kv) wide = lus[g]->view();
+  const int cl = inv_cluster_size(wide, S, R, smem);
+  s->inv_cl = cl;
+  const int64_t dyn = (int64_t)(smem / sizeof(double));
+  const int64_t ts = (std::max(wide.kl, wide.kv) + 2) & ~(int64_t)1;
+  const int64_t dpart_off = cl > 1 ? dyn - (int64_t)cl * R * kLUBlock : dyn;
+  const int64_t tsum_off = cl > 1 ? dpart_off - (int64_t)R * ts : dyn;
   const int64_t yw = s->npad * R;
   s->PX.alloc(3 * R * s->npad);
   s->MV.alloc(s->npad * R);
@@ -962,8 +973,12 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
     a.b = b;
     a.n = s->seg_n[g];
     a.ring_size = lu_ring_size(b);
-    a.b.stage_cap = (int64_t)(smem / sizeof(double)) - stage_offset(R, a.ring_size);
+    a.b.stage_cap = tsum_off - stage_offset(R, a.ring_size);
     if (a.b.stage_cap < 0) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip solve window");
+    a.cl = cl;
+    a.cl_tsum_off = tsum_off;
+    a.cl_ts = ts;
+    a.cl_dpart_off = dpart_off;
     a.b.stage_min = lu_stage_min();
     a.PX = s->PX.p + o * R;
     a.pstride = s->npad * R;

@@ -10,6 +10,9 @@
 // State layout and control are those of the explicit path (ck_adam.cu), so the
 // host session, restarts, best tracking and observer mode are shared.
 #include <cmath>
+#include <cooperative_groups.h>
+#include <cstdlib>
+#include <algorithm>
 
 #include "ck_common.h"
 #include "ck_device.cuh"
@@ -27,10 +30,29 @@ __device__ __forceinline__ double xtilde_inv(double2 p, double rad) {
 
 // One CTA per member: blockIdx.x selects the member's arguments. half: 0 the
 // whole step, 1 the apply half only, 2 the transpose half only (observer).
-template <int R>
+// CLU: one cluster per member (launched with cluster dims a.cl); rank 0 runs the
+// step, the other ranks only help with the sweeps (helper_solve).
+template <int R, bool CLU>
 __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ args, int half) {
-  const InvArgs& a = args[blockIdx.x];
+  const unsigned crank = CLU ? cooperative_groups::this_cluster().block_rank() : 0u;
+  const unsigned csize = CLU ? cooperative_groups::this_cluster().num_blocks() : 1u;
+  const InvArgs& a = args[blockIdx.x / csize];
   extern __shared__ double smem[];
+  Clu C{(int)csize, (int)crank, smem + a.cl_tsum_off, a.cl_ts, smem + a.cl_dpart_off};
+  if (CLU && crank > 0) {
+    bool any = false;
+    for (int r = 0; r < R; ++r) {
+      const int ph = a.st[r].phase;
+      any |= ph == PH_PRO || ph == PH_APPLY;
+    }
+    if (any && half != 2) helper_solve<R>(a.b, smem, a.ring_size, false, C);
+    clu_sync();  // the leader's control step is done
+    bool anyg = false;
+    for (int r = 0; r < R; ++r) anyg |= __ldcg(&a.st[r].phase) == PH_GRAD;
+    if (anyg && half != 1) helper_solve<R>(a.b, smem, a.ring_size, true, C);
+    clu_sync();
+    return;
+  }
   __shared__ double s_h[32], s_l[32];
   __shared__ int s_e[32], s_f[32];
   __shared__ double s_res[R][4];
@@ -92,7 +114,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
       }
     }
     __syncthreads();
-    inv_solve<R>(a.b, ys, smem, a.ring_size, false);
+    inv_solve<R, CLU>(a.b, ys, smem, a.ring_size, false, C);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -116,6 +138,10 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
     }
     __syncthreads();
   }
+  if (CLU) {
+    __threadfence();
+    clu_sync();  // the helpers read the control state next
+  }
 
   // ---------------- transpose half: z = A^{-T} y', Adam, r = x.delta
   bool grad[R], mat[R];
@@ -138,7 +164,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
     anyg |= grad[r];
   }
   if (anyg && half != 1) {
-    inv_solve<R>(a.b, ys, smem, a.ring_size, true);
+    inv_solve<R, CLU>(a.b, ys, smem, a.ring_size, true, C);
     __syncthreads();
     const Params& p = a.prm;
     const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
@@ -194,23 +220,64 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
     a.hdr->ndone = ndone;
     a.hdr->needA = 1;
   }
+  if (CLU) clu_sync();  // no rank leaves while another may still touch its shared memory
 }
 
 void prepare_inv_step(size_t smem, int R) {
   switch (R) {
-    case 1: CK_CUDA(allow_max_dynamic_smem(k_inv_step<1>)); break;
-    case 2: CK_CUDA(allow_max_dynamic_smem(k_inv_step<2>)); break;
-    case 3: CK_CUDA(allow_max_dynamic_smem(k_inv_step<3>)); break;
-    default: CK_CUDA(allow_max_dynamic_smem(k_inv_step<4>)); break;
+    case 1:
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<1, false>));
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<1, true>));
+      break;
+    case 2:
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<2, false>));
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<2, true>));
+      break;
+    case 3:
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<3, false>));
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<3, true>));
+      break;
+    default:
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<4, false>));
+      CK_CUDA(allow_max_dynamic_smem(k_inv_step<4, true>));
+      break;
   }
 }
 
-// S members, one CTA each, smem bytes of dynamic shared memory per CTA.
-void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st) {
+template <int R>
+static void launch_cluster(const InvArgs* args, int S, int cl, size_t smem, int half, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(S * cl));
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK_CUDA(cudaLaunchKernelEx(&cfg, k_inv_step<R, true>, args, half));
+}
+
+// S members, one CTA (cl == 1) or one cluster of cl CTAs each, smem bytes of
+// dynamic shared memory per CTA.
+void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st, int cl) {
+  if (cl > 1) {
+    switch (R) {
+      case 1: launch_cluster<1>(args, S, cl, smem, half, st); break;
+      case 2: launch_cluster<2>(args, S, cl, smem, half, st); break;
+      case 3: launch_cluster<3>(args, S, cl, smem, half, st); break;
+      case 4: launch_cluster<4>(args, S, cl, smem, half, st); break;
+      default: fail(CK_ERR_INVALID_ARGUMENT, "1..4 columns");
+    }
+    return;
+  }
   switch (R) {
 #define CK_INV_CASE(RR)                                                                        \
   case RR:                                                                                     \
-    k_inv_step<RR><<<S, 1024, smem, st>>>(args, half);                                         \
+    k_inv_step<RR, false><<<S, 1024, smem, st>>>(args, half);                                  \
     break;
     CK_INV_CASE(1)
     CK_INV_CASE(2)
@@ -221,4 +288,52 @@ void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, c
   }
 }
 
+// Cluster size for the sweeps of S systems of band b: 8 CTAs per system for
+// wide bands when the clusters fit the chip, else 1 (CK_LU_CLUSTER=1 disables,
+// =2..8 forces a size).
+int inv_cluster_size(const BandView& b, int S, int R, size_t smem) {
+  int cl = (b.kv >= kLUClusterMinRows && S * 8 <= 148) ? 8 : 1;
+  if (const char* e = std::getenv("CK_LU_CLUSTER")) cl = std::max(1, std::min(8, std::atoi(e)));
+  if (cl <= 1) return 1;
+  // the occupancy calculator must accept a cluster of this size
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(S * cl));
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (R) {
+    case 1: e = cudaOccupancyMaxActiveClusters(&nclusters, k_inv_step<1, true>, &cfg); break;
+    case 2: e = cudaOccupancyMaxActiveClusters(&nclusters, k_inv_step<2, true>, &cfg); break;
+    case 3: e = cudaOccupancyMaxActiveClusters(&nclusters, k_inv_step<3, true>, &cfg); break;
+    default: e = cudaOccupancyMaxActiveClusters(&nclusters, k_inv_step<4, true>, &cfg); break;
+  }
+  if (e != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    return 1;
+  }
+  return cl;
+}
+
 }  // namespace ck
+
+#ifdef CK_SWEEP_PROF
+// Profiling build only: phase cycles of the sweeps inside the inverse step
+// (this translation unit's copy of the counters; the leader CTA's thread 0).
+extern "C" int ck_debug_sweep_prof_inv(unsigned long long* out32, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out32, ck::g_sweep_prof, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(ck::g_sweep_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

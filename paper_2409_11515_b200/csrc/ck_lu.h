@@ -47,6 +47,9 @@ struct LUStatus {
 constexpr int kLUBlock = 32;  // panel width / solve block
 constexpr int64_t kLUStageMinRows = 129;  // runs of <= 128 rows unstaged; lu_stage_min (ck_lu.cu)
 int64_t lu_stage_min();
+// bands at least this wide (kl + ku rows above the diagonal of U) sweep on a
+// cluster of CTAs per system (ck_lu_sweeps.cuh, Clu)
+constexpr int64_t kLUClusterMinRows = 256;
 
 // Raise a kernel's dynamic shared-memory ceiling to everything the SM has
 // left beside its static shared memory. Always the same value, so concurrent

@@ -15,6 +15,8 @@
 // interchange pairs and incoming rows into registers at the same time. Rows
 // beyond the stage capacity (very wide bands) are read directly.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "ck_device.cuh"
 #include "ck_lu.h"
 
@@ -298,15 +300,150 @@ __device__ __forceinline__ void warp_dot(int64_t base, int64_t m0, int64_t m1, c
   }
 }
 
+// ------------------------------------------------------ cluster split
+// Wide bands on few systems: the sweep of one system runs on a cluster of
+// CTAs. Rank 0 (the leader) keeps everything the single-CTA sweep has -- the
+// solution ring, interchanges, head solves, prefetch and TMA stage -- and works
+// on the first share of every block's tail rows / dot rows; ranks 1.. (helpers)
+// stream the remaining shares of the block's coefficients from HBM, read the
+// head values / final rows they need from the leader's ring through DSMEM, and
+// write their tail sums / dot partials back into the leader's shared memory.
+// Two cluster barriers per block. Tail rows keep the single-CTA arithmetic
+// (same per-row sum order for a given lanes-per-row); dot rows are summed per
+// rank and combined in rank order.
+struct Clu {
+  int size, rank;
+  double* tsum;   // leader smem: [R][ts] helper tail sums, by tail-relative row
+  int64_t ts;
+  double* dpart;  // leader smem: [size][R][32] dot partials per rank
+};
+
+__device__ __forceinline__ void clu_sync() { cooperative_groups::this_cluster().sync(); }
+
+template <class T>
+__device__ __forceinline__ T* clu_leader(T* p) {
+  return cooperative_groups::this_cluster().map_shared_rank(p, 0);
+}
+
+// Rows [lo, hi) of share k out of `size` of the row range [m0, m1).
+__device__ __forceinline__ int64_t clu_cut(int64_t m0, int64_t m1, int k, int size) {
+  return m0 + ((m1 - m0) * k) / size;
+}
+
+// Helper: the coefficients of a share, cf[c * (hi - lo) + (m - lo)] = coef(m, c)
+// for m in [lo, hi), c < jb -- loaded before the cluster barrier that releases
+// the head values, so their latency hides behind the leader's head solve. Warp
+// c loads column c, 32 consecutive rows per step, 8 steps in flight (TMA bulk
+// copies of the 32 runs, one thread issuing, measured slower: 164 vs 134 ms per
+// config-2 iteration).
+template <class Coef>
+__device__ __forceinline__ void helper_fetch(int64_t lo, int64_t hi, int jb, double* cf, Coef coef) {
+  constexpr int U = 8;
+  const int sh = (int)(hi - lo);
+  const int c = (int)threadIdx.x >> 5, l = (int)threadIdx.x & 31;
+  if (c >= jb) return;
+  for (int m0 = l; m0 < sh; m0 += 32 * U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int mm = m0 + 32 * u;
+      v[u] = mm < sh ? coef(lo + mm, c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int mm = m0 + 32 * u;
+      if (mm < sh) cf[c * sh + mm] = v[u];
+    }
+  }
+}
+
+// Helper: sums of rows m in [lo, hi) of a block tail, sum_c cf(m, c) * y_c,
+// written to the leader's tsum (same lane split and order as tail_update).
+template <int R>
+__device__ __forceinline__ void helper_tail(int64_t lo, int64_t hi, int jb, const double* hy,
+                                            const double* cf, const Clu& C) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lg = tail_log_lanes(hi - lo);
+  const int rs_bits = 5 - lg, G = 1 << lg;
+  const int g = lane >> rs_bits, rs = lane & ((1 << rs_bits) - 1);
+  const int64_t per_pass = (int64_t)kSweepThreads >> lg;
+  double* ts = clu_leader(C.tsum);
+  for (int64_t mb = lo; mb < hi; mb += per_pass) {
+    if (mb + ((int64_t)warp << rs_bits) >= hi) continue;  // warp-uniform
+    const int64_t m = mb + ((int64_t)warp << rs_bits) + rs;
+    const bool act = m < hi;
+    double sm[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[r] = 0.0;
+    if (act) {
+#pragma unroll 8
+      for (int c = g; c < jb; c += G) {
+        const double l = cf[(int64_t)c * (hi - lo) + (m - lo)];
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[r] = __fma_rn(l, hy[r * kLUBlock + c], sm[r]);
+      }
+    }
+    for (int o = 16; o >= (1 << rs_bits); o >>= 1)
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[r] = __dadd_rn(sm[r], __shfl_xor_sync(0xffffffffu, sm[r], o));
+    if (act && g == 0)
+#pragma unroll
+      for (int r = 0; r < R; ++r) ts[r * C.ts + m] = sm[r];
+  }
+}
+
+// Helper: copy the head values y_c = ring[J + c] (c < 32) of the leader into hy.
+template <int R>
+__device__ __forceinline__ void helper_head(const Ring* lring, int64_t J, double* hy) {
+  if (threadIdx.x < 32 * R) {
+    const int r = threadIdx.x >> 5, c = threadIdx.x & 31;
+    hy[r * kLUBlock + c] = lring[r][J + c];
+  }
+  __syncthreads();
+}
+
+// Helper: dot partials of rows m in [lo, hi) (ring rows base + m, copied from
+// the leader into hl) for every head column c < jb, into the leader's dpart.
+template <int R>
+__device__ __forceinline__ void helper_dots(const Ring* lring, int64_t base, int64_t lo, int64_t hi, int jb,
+                                            int64_t cmin_off, double* hl, const double* cf, const Clu& C) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t m = lo + tid; m < hi; m += kSweepThreads)
+#pragma unroll
+    for (int r = 0; r < R; ++r) hl[r * (hi - lo) + (m - lo)] = lring[r][base + m];
+  __syncthreads();
+  double* dp = clu_leader(C.dpart) + (int64_t)C.rank * R * kLUBlock;
+  const int c = warp;
+  double sm[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) sm[r] = 0.0;
+  if (c < jb) {
+    const int64_t s0 = lmax(lo, cmin_off >= 0 ? (int64_t)c + cmin_off : lo);
+#pragma unroll 4
+    for (int64_t m = s0 + lane; m < hi; m += 32) {
+      const double u = cf[(int64_t)c * (hi - lo) + (m - lo)];
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[r] = __fma_rn(u, hl[r * (hi - lo) + (m - lo)], sm[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double t = warp_sum(sm[r]);
+    if (lane == 0) dp[r * kLUBlock + c] = t;
+  }
+  __syncthreads();  // hl is reused by the next block
+}
+
 // ------------------------------------------------------------ L forward
 // x := (L-part)^{-1} x, i.e. LAPACK gbtrs 'N' first half: for every step j
 // interchange rows j, ipiv[j], then eliminate below j.
-template <int R>
-__device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S) {
+template <int R, bool CLU = false>
+__device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S,
+                                const Clu& C) {
   const int64_t n = b.n;
   const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
   if (n == 0) return;
-  const int lg = tail_log_lanes(b.kl);
+  const int lg = tail_log_lanes(CLU ? (b.kl + C.size - 1) / C.size : b.kl);
   Perm pq;
   HeadPrefetch ph;
   RowPrefetch<R> px;
@@ -354,12 +491,22 @@ __device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring,
     CK_PROF(0);
     __syncthreads();
     CK_PROF(1);
+    if (CLU) clu_sync();  // head values in the ring for the helpers
+    const int64_t M = wend - J - kLUBlock;  // tail rows
+    const int64_t mh = CLU ? 0 : M;  // the leader's own tail rows (none with helpers)
     if (tail) {
       S.wait();
       const double* lbk = b.lb + blk * kLUBlock * b.lb_ld;
-      tail_update<R>(J + kLUBlock, 0, wend - J - kLUBlock, J, jb, lg, ring, [&](int64_t m, int c) {
+      tail_update<R>(J + kLUBlock, 0, mh, J, jb, lg, ring, [&](int64_t m, int c) {
         return m < S.srows ? S.at(c, (int)((c * b.lb_ld) & 1), m) : lbk[c * b.lb_ld + kLUBlock + m];
       });
+    }
+    if (CLU) {
+      clu_sync();  // helper sums in tsum
+      for (int64_t m = mh + tid; m < M; m += nt)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          ring[r][J + kLUBlock + m] = __dsub_rn(ring[r][J + kLUBlock + m], C.tsum[r * C.ts + m]);
     }
     if (more) {
       ph.commit(H);
@@ -375,13 +522,14 @@ __device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring,
 // ----------------------------------------------------------- U backward
 // x := U^{-1} x (backward), U of bandwidth kv above the diagonal; blocks in
 // reverse, same two phases as sweep_l_forward.
-template <int R>
-__device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S) {
+template <int R, bool CLU = false>
+__device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S,
+                                 const Clu& C) {
   const int64_t n = b.n;
   const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = (n + kLUBlock - 1) / kLUBlock;
   if (nblk == 0) return;
-  const int lg = tail_log_lanes(b.kv);
+  const int lg = tail_log_lanes(CLU ? (b.kv + C.size - 1) / C.size : b.kv);
   HeadPrefetch ph;
   RowPrefetch<R> px;
   int64_t lo;  // rows [lo, n) are in the ring
@@ -435,14 +583,24 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
     CK_PROF(8);
     __syncthreads();
     CK_PROF(9);
+    if (CLU) clu_sync();  // head values in the ring for the helpers
+    const int64_t m0 = wbeg - (J - b.kv);  // first tail row (relative)
+    const int64_t mh = CLU ? m0 : b.kv;  // the leader's own tail rows (none with helpers)
     if (tail) {
       S.wait();
       // tail row i = J - kv + m; U(i, J+c) lies in the band for m >= c
-      tail_update<R>(J - b.kv, wbeg - (J - b.kv), b.kv, J, jb, lg, ring, [&](int64_t m, int c) {
+      tail_update<R>(J - b.kv, m0, mh, J, jb, lg, ring, [&](int64_t m, int c) {
         if (m < c) return 0.0;
         const int64_t f = u_run_first(b, J, c);
         return m < S.srows ? S.at(c, (int)(f & 1), m) : b.ab[f + m];
       });
+    }
+    if (CLU) {
+      clu_sync();  // helper sums in tsum
+      for (int64_t m = mh + tid; m < b.kv; m += nt)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          ring[r][J - b.kv + m] = __dsub_rn(ring[r][J - b.kv + m], C.tsum[r * C.ts + m]);
     }
     if (more) {
       ph.commit(H, true);
@@ -460,9 +618,9 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
 // Phase 1: warp c forms head row c's dot over the final rows below J (from
 // the stage). Phase 2: warp 0 solves the head triangle while the stage and
 // the idle warps fetch the next block.
-template <int R>
+template <int R, bool CLU = false>
 __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring, double* s_dot,
-                                 Head& H, Stage& S) {
+                                 Head& H, Stage& S, const Clu& C) {
   const int64_t n = b.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (n == 0) return;
@@ -480,18 +638,27 @@ __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring
     const int jb = (int)lmin(kLUBlock, n - J);
     const int64_t J1 = J + kLUBlock;
     const bool dots = J > 0;
+    const int64_t mh = CLU ? 0 : b.kv;  // the leader's own dot rows (none with helpers)
     if (dots) {
       S.wait();
       if (warp < jb) {
         const int c = warp;
         // rows i = J - kv + m of column J+c: in the band for m >= c, i >= 0
         const int64_t f = u_run_first(b, J, c);
-        warp_dot<R>(J - b.kv, lmax(c, b.kv - J), b.kv, ring, s_dot, c, [&](int64_t m) {
+        warp_dot<R>(J - b.kv, lmax(c, b.kv - J), mh, ring, CLU ? C.dpart : s_dot, c, [&](int64_t m) {
           return m < S.srows ? S.at(c, (int)(f & 1), m) : b.ab[f + m];
         });
       }
     }
     CK_PROF(16);
+    if (CLU) {
+      clu_sync();  // every rank's partials in dpart
+      if (dots && tid < R * kLUBlock) {
+        double t = 0.0;
+        for (int k = 0; k < C.size; ++k) t = __dadd_rn(t, C.dpart[(int64_t)k * R * kLUBlock + tid]);
+        s_dot[tid] = t;
+      }
+    }
     __syncthreads();
     CK_PROF(17);
     if (warp == 0) {
@@ -529,6 +696,7 @@ __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring
     CK_PROF(20);
     __syncthreads();
     CK_PROF(21);
+    if (CLU) clu_sync();  // the block's rows are final for the helpers
     if (J1 < n) {
       ph.commit(H, true);
       px.commit(ring, J1, lmin(n, J1 + kLUBlock));
@@ -543,9 +711,9 @@ __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring
 // stage) and the rows the previous block finalised go out. Phase 2: warp 0
 // solves the head and applies the block's inverse interchange while the
 // stage and the idle warps fetch the next block.
-template <int R>
+template <int R, bool CLU = false>
 __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring, double* s_dot,
-                                 Head& H, Stage& S) {
+                                 Head& H, Stage& S, const Clu& C) {
   const int64_t n = b.n;
   const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = (n + kLUBlock - 1) / kLUBlock;
@@ -574,17 +742,27 @@ __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring
 #pragma unroll
         for (int r = 0; r < R; ++r) x[r][i] = ring[r][i];
     }
+    const int64_t M = wend - J - kLUBlock;
+    const int64_t mh = CLU ? 0 : M;  // the leader's own dot rows (none with helpers)
     if (dots) {
       S.wait();
       if (warp < jb) {
         const int c = warp;
         const double* col = b.lb + l_run_first(b, blk, c);
         const int off = (int)((c * b.lb_ld) & 1);
-        warp_dot<R>(J + kLUBlock, 0, wend - J - kLUBlock, ring, s_dot, c,
+        warp_dot<R>(J + kLUBlock, 0, mh, ring, CLU ? C.dpart : s_dot, c,
                     [&](int64_t m) { return m < S.srows ? S.at(c, off, m) : col[m]; });
       }
     }
     CK_PROF(24);
+    if (CLU) {
+      clu_sync();  // every rank's partials in dpart
+      if (dots && tid < R * kLUBlock) {
+        double t = 0.0;
+        for (int k = 0; k < C.size; ++k) t = __dadd_rn(t, C.dpart[(int64_t)k * R * kLUBlock + tid]);
+        s_dot[tid] = t;
+      }
+    }
     __syncthreads();
     CK_PROF(25);
     if (warp == 0) {
@@ -617,6 +795,7 @@ __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring
     CK_PROF(28);
     __syncthreads();
     CK_PROF(29);
+    if (CLU) clu_sync();  // the block's rows are final for the helpers
     if (blk > 0) {
       ph.commit(H);
       px.commit(ring, J - kLUBlock, J);
@@ -630,10 +809,10 @@ __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring
 }
 
 // x := A^{-1} x (transpose = false) or A^{-T} x, for R right-hand sides, by the
-// calling CTA of kSweepThreads threads.
-template <int R>
+// calling CTA of kSweepThreads threads (CLU: the cluster's leader, see Clu).
+template <int R, bool CLU = false>
 __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, double* smem,
-                                          int ring_size, bool transpose) {
+                                          int ring_size, bool transpose, const Clu& C = Clu{1, 0, nullptr, 0, nullptr}) {
   __shared__ Head H;
   __shared__ alignas(8) uint64_t mbar;
   Ring ring[R];
@@ -649,16 +828,129 @@ __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, d
   Stage S;
   S.st = smem + stage_offset(R, ring_size);
   S.bar = &mbar;
+  // the leader works on no tail / dot rows itself in cluster mode: no stage
+  const int64_t kl = CLU ? 0 : b.kl;
+  const int64_t kv = CLU ? 0 : b.kv;
   if (!transpose) {
-    S.layout(b.stage_cap, b.kl, b.stage_min);
-    sweep_l_forward<R>(b, x, ring, H, S);
-    S.layout(b.stage_cap, b.kv, b.stage_min);
-    sweep_u_backward<R>(b, x, ring, H, S);
+    S.layout(b.stage_cap, kl, b.stage_min);
+    sweep_l_forward<R, CLU>(b, x, ring, H, S, C);
+    S.layout(b.stage_cap, kv, b.stage_min);
+    sweep_u_backward<R, CLU>(b, x, ring, H, S, C);
   } else {
-    S.layout(b.stage_cap, b.kv, b.stage_min);
-    sweep_ut_forward<R>(b, x, ring, s_dot, H, S);
-    S.layout(b.stage_cap, b.kl, b.stage_min);
-    sweep_l_backward<R>(b, x, ring, s_dot, H, S);
+    S.layout(b.stage_cap, kv, b.stage_min);
+    sweep_ut_forward<R, CLU>(b, x, ring, s_dot, H, S, C);
+    S.layout(b.stage_cap, kl, b.stage_min);
+    sweep_l_backward<R, CLU>(b, x, ring, s_dot, H, S, C);
+  }
+}
+
+// The helper side of inv_solve (cluster rank > 0): the same block sequence and
+// cluster barriers as the leader's four sweeps; `local` is this CTA's dynamic
+// shared memory (head copy, then copied ring rows).
+template <int R>
+__device__ void helper_solve(const BandView& b, double* local, int ring_size, bool transpose, const Clu& C) {
+  const int64_t n = b.n;
+  const int64_t nblk = (n + kLUBlock - 1) / kLUBlock;
+  const Clu& c = C;
+  Ring lring[R];  // the leader's rings (DSMEM)
+#pragma unroll
+  for (int r = 0; r < R; ++r) lring[r] = Ring{clu_leader(local + (int64_t)r * ring_size), ring_size - 1};
+  const int64_t shmax = (lmax(b.kl, b.kv) + c.size - 2) / (c.size - 1) + 2;
+  double* hy = local;                         // [R][32] head values
+  double* hl = hy + (int64_t)R * kLUBlock;      // [R][share] ring rows of a dot share
+  double* cf = hl + (int64_t)R * shmax;         // [32][share] coefficients of a share
+  auto share = [&](int64_t m0, int64_t m1, int64_t& lo, int64_t& hi) {  // helpers only
+    lo = clu_cut(m0, m1, c.rank - 1, c.size - 1);
+    hi = clu_cut(m0, m1, c.rank, c.size - 1);
+  };
+  if (n == 0) return;
+  if (!transpose) {
+    for (int64_t J = 0; J < n; J += kLUBlock) {  // L forward
+      const int64_t blk = J / kLUBlock;
+      const int jb = (int)lmin(kLUBlock, n - J);
+      const int64_t wend = lmin(n, J + kLUBlock + b.kl);
+      const bool tail = wend > J + jb;
+      int64_t lo = 0, hi = 0;
+      if (tail) {
+        share(0, wend - J - kLUBlock, lo, hi);
+        const double* lbk = b.lb + blk * kLUBlock * b.lb_ld;
+        helper_fetch(lo, hi, jb, cf, [&](int64_t m, int cc) { return lbk[cc * b.lb_ld + kLUBlock + m]; });
+      }
+      clu_sync();
+      if (tail) {
+        helper_head<R>(lring, J, hy);  // (its barrier also publishes cf)
+        helper_tail<R>(lo, hi, jb, hy, cf, c);
+      }
+      clu_sync();
+    }
+    for (int64_t blk = nblk - 1; blk >= 0; --blk) {  // U backward
+      const int64_t J = blk * kLUBlock;
+      const int jb = (int)lmin(kLUBlock, n - J);
+      const int64_t wbeg = lmax(0, J - b.kv);
+      const bool tail = J > wbeg;
+      int64_t lo = 0, hi = 0;
+      if (tail) {
+        share(wbeg - (J - b.kv), b.kv, lo, hi);
+        helper_fetch(lo, hi, jb, cf, [&](int64_t m, int cc) {
+          return m < cc ? 0.0 : b.ab[u_run_first(b, J, cc) + m];
+        });
+      }
+      clu_sync();
+      if (tail) {
+        helper_head<R>(lring, J, hy);
+        helper_tail<R>(lo, hi, jb, hy, cf, c);
+      }
+      clu_sync();
+    }
+  } else {
+    // dots of block J: coefficients fetched while the leader combines and
+    // solves the previous head (between its two barriers)
+    auto ut_fetch = [&](int64_t J) {
+      if (J <= 0 || J >= n) return;
+      int64_t lo, hi;
+      share(lmax(0, b.kv - J), b.kv, lo, hi);
+      helper_fetch(lo, hi, (int)lmin(kLUBlock, n - J), cf,
+                   [&](int64_t m, int cc) { return m < cc ? 0.0 : b.ab[u_run_first(b, J, cc) + m]; });
+    };
+    for (int64_t J = 0; J < n; J += kLUBlock) {  // U^T forward (block 0 has no dots)
+      const int jb = (int)lmin(kLUBlock, n - J);
+      if (J > 0) {
+        int64_t lo, hi;
+        share(lmax(0, b.kv - J), b.kv, lo, hi);
+        __syncthreads();  // cf complete
+        helper_dots<R>(lring, J - b.kv, lo, hi, jb, 0, hl, cf, c);
+      }
+      clu_sync();
+      ut_fetch(J + kLUBlock);
+      clu_sync();
+    }
+    auto lt_dots = [&](int64_t blk, int64_t& lo, int64_t& hi) {
+      const int64_t J = blk * kLUBlock;
+      const int jb = (int)lmin(kLUBlock, n - J);
+      const int64_t wend = lmin(n, J + kLUBlock + b.kl);
+      if (!(wend > J + jb)) return false;
+      share(0, wend - J - kLUBlock, lo, hi);
+      return true;
+    };
+    auto lt_fetch = [&](int64_t blk) {
+      int64_t lo, hi;
+      if (blk < 0 || !lt_dots(blk, lo, hi)) return;
+      helper_fetch(lo, hi, (int)lmin(kLUBlock, n - blk * kLUBlock), cf,
+                   [&](int64_t m, int cc) { return b.lb[l_run_first(b, blk, cc) + m]; });
+    };
+    lt_fetch(nblk - 1);
+    for (int64_t blk = nblk - 1; blk >= 0; --blk) {  // L^T backward
+      const int64_t J = blk * kLUBlock;
+      const int jb = (int)lmin(kLUBlock, n - J);
+      int64_t lo, hi;
+      if (lt_dots(blk, lo, hi)) {
+        __syncthreads();  // cf complete
+        helper_dots<R>(lring, J + kLUBlock, lo, hi, jb, -1, hl, cf, c);
+      }
+      clu_sync();
+      lt_fetch(blk - 1);
+      clu_sync();
+    }
   }
 }
 

@@ -77,6 +77,11 @@ struct InvArgs {
   ColState* st;     // R columns
   Header* hdr;
   Params prm;
+  // cluster split of the sweeps (cl > 1, ck_lu_sweeps.cuh Clu): offsets in
+  // doubles into the dynamic shared memory of the leader's tail sums [R][cl_ts]
+  // and dot partials [cl][R][32]
+  int cl;
+  int64_t cl_tsum_off, cl_ts, cl_dpart_off;
 };
 
 // Row-block partition rank (ck_dist.cu): this rank owns global rows/columns
@@ -116,6 +121,7 @@ struct ck_session_s {
   std::vector<ck_lu_s*> lus;  // kind 1: factors per member
   DBuf<ck::InvArgs> dargs;    // kind 1: per-member step arguments
   size_t inv_smem = 0;        // kind 1: dynamic shared memory of the step CTA
+  int inv_cl = 1;             // kind 1: CTAs per system (cluster split of the sweeps)
   cudaStream_t stream = nullptr;
   int device = 0;
   int64_t n = 0;            // operator dimension (columns of A)

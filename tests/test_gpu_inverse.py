@@ -246,3 +246,22 @@ def test_inverse_restarts_are_separate_runs(port):
             best = e
     assert comb.value == best.value and comb.iterations == best.iterations
     assert np.array_equal(comb.witness, best.witness)
+
+
+@pytest.mark.parametrize("cl", ["2", "8"])
+def test_cluster_sweeps_match_single_cta_and_oracle(port, monkeypatch, cl):
+    """The cluster split of the band sweeps (helpers stream the tail / dot
+    coefficients, the leader keeps heads and the ring) agrees with the
+    single-CTA sweeps and with the oracle."""
+    a = M.row_scaled(M.laplacian2d(24), port, 5)
+    f, rf = ck.lu_factorize(a, 1e-14), port.lu_factorize(a, 1e-14)
+    c = M.cfg(alpha=1e-2, max_iter=400, patience=400, seed=9)
+    monkeypatch.setenv("CK_LU_CLUSTER", "1")
+    one = ck.projected_adam(ck.InverseOracle(f), c)
+    monkeypatch.setenv("CK_LU_CLUSTER", cl)
+    clu = ck.projected_adam(ck.InverseOracle(f), c)
+    o = port.projected_adam_inverse(rf, c)
+    assert clu.iterations == one.iterations == o.iterations
+    assert clu.value == pytest.approx(one.value, rel=1e-12)
+    assert clu.value == pytest.approx(o.value, rel=1e-9)
+    assert np.linalg.norm(port.lu_solve(rf, clu.witness)) == pytest.approx(clu.value, rel=1e-11)
