@@ -288,14 +288,20 @@ void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, c
   }
 }
 
-// Cluster size for the sweeps of S systems of band b: 8 CTAs per system for
-// wide bands when the clusters fit the chip, else 1 (CK_LU_CLUSTER=1 disables,
-// =2..8 forces a size).
-int inv_cluster_size(const BandView& b, int S, int R, size_t smem) {
-  int cl = (b.kv >= kLUClusterMinRows && S * 8 <= 148) ? 8 : 1;
-  if (const char* e = std::getenv("CK_LU_CLUSTER")) cl = std::max(1, std::min(8, std::atoi(e)));
-  if (cl <= 1) return 1;
-  // the occupancy calculator must accept a cluster of this size
+// Cluster size for the sweeps of S systems of band b (measured,
+// scripts/check_cluster.py): 8 CTAs per system from kl + ku >= 256 (config-5
+// member 74 -> 54 ms per inverse iteration), 12 from kl + ku >= 1024 (config 2
+// 358 -> 124 ms; 134 with 8, 125 with 16), when the clusters fit the chip;
+// else 1. CK_LU_CLUSTER=1 disables, =2..16 forces a size.
+static bool cluster_fits(int cl, int S, int R, size_t smem) {
+  if (cl > 8) {  // non-portable cluster sizes need the opt-in
+    switch (R) {
+      case 1: cudaFuncSetAttribute(k_inv_step<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); break;
+      case 2: cudaFuncSetAttribute(k_inv_step<2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); break;
+      case 3: cudaFuncSetAttribute(k_inv_step<3, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); break;
+      default: cudaFuncSetAttribute(k_inv_step<4, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); break;
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(S * cl));
   cfg.blockDim = dim3(1024);
@@ -315,11 +321,21 @@ int inv_cluster_size(const BandView& b, int S, int R, size_t smem) {
     case 3: e = cudaOccupancyMaxActiveClusters(&nclusters, k_inv_step<3, true>, &cfg); break;
     default: e = cudaOccupancyMaxActiveClusters(&nclusters, k_inv_step<4, true>, &cfg); break;
   }
-  if (e != cudaSuccess || nclusters < 1) {
+  if (e != cudaSuccess) {
     cudaGetLastError();
-    return 1;
+    return false;
   }
-  return cl;
+  return nclusters >= 1;
+}
+
+int inv_cluster_size(const BandView& b, int S, int R, size_t smem) {
+  if (const char* e = std::getenv("CK_LU_CLUSTER")) {
+    const int cl = std::max(1, std::min(16, std::atoi(e)));
+    return cl > 1 && cluster_fits(cl, S, R, smem) ? cl : 1;
+  }
+  if (b.kv >= 4 * kLUClusterMinRows && S * 12 <= 148 && cluster_fits(12, S, R, smem)) return 12;
+  if (b.kv >= kLUClusterMinRows && S * 8 <= 148 && cluster_fits(8, S, R, smem)) return 8;
+  return 1;
 }
 
 }  // namespace ck

@@ -27,15 +27,18 @@ print(json.dumps({"value": e.value, "its": e.iterations, "ms_per_it": (t1 - t0) 
 '''
 for name, its in [("c1", 200), ("c5m0", 40), ("c2", 20)]:
     out = {}
-    for cl in ("1", "8"):
+    for cl in os.environ.get("CK_CL_LIST", "1 8").split():
         env = dict(os.environ, CK_LU_CLUSTER=cl)
+        if cl == "auto":
+            env.pop("CK_LU_CLUSTER")
         r = subprocess.run([sys.executable, "-c", code, name, str(its)], capture_output=True, text=True,
                            env=env, timeout=900)
         if r.returncode:
             print(name, cl, "FAILED", r.stderr[-500:], flush=True)
             continue
         out[cl] = json.loads(r.stdout.strip().splitlines()[-1])
-    if len(out) == 2:
-        rel = abs(out["8"]["value"] - out["1"]["value"]) / out["1"]["value"]
-        print(f"{name}: single {out['1']['ms_per_it']:.3f} ms/it, cluster {out['8']['ms_per_it']:.3f} ms/it, "
-              f"value rel diff {rel:.2e}, its {out['1']['its']}/{out['8']['its']}", flush=True)
+    if "1" in out:
+        for k, v in out.items():
+            rel = abs(v["value"] - out["1"]["value"]) / out["1"]["value"]
+            print(f"{name}: cluster {k}: {v['ms_per_it']:.3f} ms/it, value rel diff vs one CTA {rel:.2e}, "
+                  f"its {v['its']}", flush=True)
