@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
   const unsigned csize = CLU ? cooperative_groups::this_cluster().num_blocks() : 1u;
   const InvArgs& a = args[blockIdx.x / csize];
   extern __shared__ double smem[];
-  Clu C{(int)csize, (int)crank, smem + a.cl_tsum_off, a.cl_ts, smem + a.cl_dpart_off};
+  Clu C{(int)csize, (int)crank, smem + a.cl_tsum_off, a.cl_ts, smem + a.cl_dpart_off, smem};
   if (CLU && crank > 0) {
     bool any = false;
     for (int r = 0; r < R; ++r) {

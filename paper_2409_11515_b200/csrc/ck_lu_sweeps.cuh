@@ -316,7 +316,22 @@ struct Clu {
   double* tsum;   // leader smem: [R][ts] helper tail sums, by tail-relative row
   int64_t ts;
   double* dpart;  // leader smem: [size][R][32] dot partials per rank
+  double* hy;     // helpers' smem (same offset in every CTA): [R][32] head values, pushed by the leader
 };
+
+// Leader, warp 0 after a head solve: lane c's solved values of the block go
+// straight into every helper's head buffer (remote stores; the next cluster
+// barrier publishes them), so the helpers need no DSMEM round trip.
+template <int R>
+__device__ __forceinline__ void clu_push_head(const Clu& C, int lane, int jb, const double* v) {
+  if (lane >= jb) return;
+  auto cl = cooperative_groups::this_cluster();
+  for (int k = 1; k < C.size; ++k) {
+    double* d = cl.map_shared_rank(C.hy, k);
+#pragma unroll
+    for (int r = 0; r < R; ++r) d[r * kLUBlock + lane] = v[r];
+  }
+}
 
 __device__ __forceinline__ void clu_sync() { cooperative_groups::this_cluster().sync(); }
 
@@ -481,6 +496,7 @@ __device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring,
           ring[r][J + lane] = hv[r];
           x[r][J + lane] = hv[r];  // head rows are final
         }
+      if (CLU && tail) clu_push_head<R>(C, lane, jb, hv);
     } else {
       if (tid == kIssuer && tail) S.issue(b.lb, jb, [&](int c) { return l_run_first(b, blk, c); });
       if (more) {
@@ -572,6 +588,7 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
           ring[r][J + lane] = h[r];
           x[r][J + lane] = h[r];
         }
+      if (CLU && tail) clu_push_head<R>(C, lane, jb, h);
     } else {
       if (tid == kIssuer && tail) S.issue(b.ab, jb, [&](int c) { return u_run_first(b, J, c); });
       if (more) {
@@ -812,7 +829,7 @@ __device__ void sweep_l_backward(const BandView& b, double* const* x, Ring* ring
 // calling CTA of kSweepThreads threads (CLU: the cluster's leader, see Clu).
 template <int R, bool CLU = false>
 __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, double* smem,
-                                          int ring_size, bool transpose, const Clu& C = Clu{1, 0, nullptr, 0, nullptr}) {
+                                          int ring_size, bool transpose, const Clu& C = Clu{1, 0, nullptr, 0, nullptr, nullptr}) {
   __shared__ Head H;
   __shared__ alignas(8) uint64_t mbar;
   Ring ring[R];
@@ -876,11 +893,8 @@ __device__ void helper_solve(const BandView& b, double* local, int ring_size, bo
         const double* lbk = b.lb + blk * kLUBlock * b.lb_ld;
         helper_fetch(lo, hi, jb, cf, [&](int64_t m, int cc) { return lbk[cc * b.lb_ld + kLUBlock + m]; });
       }
-      clu_sync();
-      if (tail) {
-        helper_head<R>(lring, J, hy);  // (its barrier also publishes cf)
-        helper_tail<R>(lo, hi, jb, hy, cf, c);
-      }
+      clu_sync();  // head values pushed by the leader, cf complete
+      if (tail) helper_tail<R>(lo, hi, jb, hy, cf, c);
       clu_sync();
     }
     for (int64_t blk = nblk - 1; blk >= 0; --blk) {  // U backward
@@ -895,11 +909,8 @@ __device__ void helper_solve(const BandView& b, double* local, int ring_size, bo
           return m < cc ? 0.0 : b.ab[u_run_first(b, J, cc) + m];
         });
       }
-      clu_sync();
-      if (tail) {
-        helper_head<R>(lring, J, hy);
-        helper_tail<R>(lo, hi, jb, hy, cf, c);
-      }
+      clu_sync();  // head values pushed by the leader, cf complete
+      if (tail) helper_tail<R>(lo, hi, jb, hy, cf, c);
       clu_sync();
     }
   } else {
