@@ -953,9 +953,13 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
   BandView wide = lus[0]->view();
   for (int g = 1; g < S; ++g)
     if (lus[g]->kl + lus[g]->ku > wide.kv) wide = lus[g]->view();
-  const int cl = inv_cluster_size(wide, S, R, smem);
-  s->inv_cl = cl;
+  int cl = inv_cluster_size(wide, S, R, smem);
   const int64_t dyn = (int64_t)(smem / sizeof(double));
+  if (cl > 1) {  // the helpers' layout (helper_solve): head values, dot rows, coefficient share
+    const int64_t sh = (std::max(wide.kl, wide.kv) + cl - 2) / (cl - 1) + 2;
+    if ((int64_t)R * kLUBlock + (int64_t)(R + kLUBlock) * sh > dyn) cl = 1;
+  }
+  s->inv_cl = cl;
   const int64_t ts = (std::max(wide.kl, wide.kv) + 2) & ~(int64_t)1;
   const int64_t dpart_off = cl > 1 ? dyn - (int64_t)cl * R * kLUBlock : dyn;
   const int64_t tsum_off = cl > 1 ? dpart_off - (int64_t)R * ts : dyn;
