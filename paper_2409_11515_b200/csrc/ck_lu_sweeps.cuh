@@ -303,14 +303,14 @@ __device__ __forceinline__ void warp_dot(int64_t base, int64_t m0, int64_t m1, c
 // ------------------------------------------------------ cluster split
 // Wide bands on few systems: the sweep of one system runs on a cluster of
 // CTAs. Rank 0 (the leader) keeps everything the single-CTA sweep has -- the
-// solution ring, interchanges, head solves, prefetch and TMA stage -- and works
-// on the first share of every block's tail rows / dot rows; ranks 1.. (helpers)
-// stream the remaining shares of the block's coefficients from HBM, read the
-// head values / final rows they need from the leader's ring through DSMEM, and
-// write their tail sums / dot partials back into the leader's shared memory.
-// Two cluster barriers per block. Tail rows keep the single-CTA arithmetic
-// (same per-row sum order for a given lanes-per-row); dot rows are summed per
-// rank and combined in rank order.
+// solution ring, interchanges, head solves and prefetch -- and hands every
+// block's tail rows / dot rows to ranks 1.. (helpers), split evenly. A helper
+// loads its share of the block's coefficients before the barrier that releases
+// the block, gets the head values pushed by the leader (tails) or reads the
+// final ring rows it needs through DSMEM (dots), and writes its tail sums / dot
+// partials back into the leader's shared memory. Two cluster barriers per
+// block. Tail rows keep the single-CTA arithmetic (same per-row sum order for a
+// given lanes-per-row); dot rows are summed per rank and combined in rank order.
 struct Clu {
   int size, rank;
   double* tsum;   // leader smem: [R][ts] helper tail sums, by tail-relative row
@@ -405,16 +405,6 @@ __device__ __forceinline__ void helper_tail(int64_t lo, int64_t hi, int jb, cons
 #pragma unroll
       for (int r = 0; r < R; ++r) ts[r * C.ts + m] = sm[r];
   }
-}
-
-// Helper: copy the head values y_c = ring[J + c] (c < 32) of the leader into hy.
-template <int R>
-__device__ __forceinline__ void helper_head(const Ring* lring, int64_t J, double* hy) {
-  if (threadIdx.x < 32 * R) {
-    const int r = threadIdx.x >> 5, c = threadIdx.x & 31;
-    hy[r * kLUBlock + c] = lring[r][J + c];
-  }
-  __syncthreads();
 }
 
 // Helper: dot partials of rows m in [lo, hi) (ring rows base + m, copied from
