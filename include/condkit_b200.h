@@ -91,6 +91,8 @@ typedef struct ck_lu_s* ck_lu;
 const char* ck_last_error(void);
 int32_t ck_abi_version(void);
 ck_status ck_device_count(int32_t* count);
+/* Free / total memory and SM count of the current device (sizing of ensemble waves). */
+ck_status ck_device_memory(uint64_t* free_bytes, uint64_t* total_bytes, int32_t* sm_count);
 /* Select the device for handles created by this thread (cudaSetDevice). */
 ck_status ck_set_device(int32_t device);
 ck_status ck_device_synchronize(void);

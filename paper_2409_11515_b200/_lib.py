@@ -51,6 +51,7 @@ _SIGS = {
     "ck_last_error": (C.c_char_p, []),
     "ck_abi_version": (C.c_int32, []),
     "ck_device_count": (C.c_int, [i32p]),
+    "ck_device_memory": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), i32p]),
     "ck_set_device": (C.c_int, [C.c_int32]),
     "ck_device_synchronize": (C.c_int, []),
     "ck_host_register": (C.c_int, [C.c_void_p, C.c_uint64]),

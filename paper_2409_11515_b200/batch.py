@@ -168,17 +168,44 @@ class InverseBatchSession(Session):
         return NormEstimate(r.value, w, int(r.iterations), bool(r.converged))
 
 
+def _band_bytes(a: SparseMatrix) -> int:
+    """Device bytes of a's band LU (lu.hpp layout, ldab = 2 kl + ku + 1) plus the
+    solve working vectors, from the CSR's band."""
+    rp, ci = a.row_offsets, a.col_indices
+    rows = np.repeat(np.arange(a.nrows, dtype=np.int64), np.diff(rp))
+    d = rows - ci.astype(np.int64)
+    kl = int(d.max(initial=0))
+    ku = int((-d).max(initial=0))
+    return 8 * a.nrows * (2 * kl + ku + 1 + 64) + (1 << 20)
+
+
+def auto_wave(members: Sequence[SparseMatrix], fraction: float = 0.7) -> int:
+    """Members factorised and iterated at once: one CTA each, so up to the SM
+    count (config 5: 64 -> 148 members lifts sigma_min throughput 1917 -> 4433
+    run-iterations/s, scripts/time_inverse_batch.py), bounded by `fraction` of
+    the free device memory for the band LUs."""
+    free, total, sms = C.c_uint64(0), C.c_uint64(0), C.c_int32(0)
+    _lib.check(_lib.load().ck_device_memory(C.byref(free), C.byref(total), C.byref(sms)),
+               "ck_device_memory")
+    per = max(_band_bytes(m) for m in members) if members else 1
+    return max(1, min(int(sms.value), int(fraction * free.value) // per))
+
+
 def cond2_batch(members: Sequence[SparseMatrix], cfg: Optional[AdamConfig] = None,
                 restarts: int = 4, pivot_tol: float = 1e-14,
-                seeds: Optional[Sequence[int]] = None, wave: int = 32, threads: int = 8):
+                seeds: Optional[Sequence[int]] = None, wave: Optional[int] = None,
+                threads: int = 8):
     """cond2 (condest.hpp:341-365) of every member, as run_bench computes it per
     matrix with seed seeds[g] (default: member_seeds): ||A_g|| for the whole
     ensemble in one packed device sweep, then the factorisations and ||A_g^-1||
-    in waves of `wave` members (bounded device memory), one CTA per member."""
+    in waves of `wave` members (default auto_wave: as many as SMs, within the
+    device memory), one CTA per member."""
     from .inverse import Cond2Result  # noqa: PLC0415
     cfg = cfg or AdamConfig()
     seeds = list(seeds) if seeds is not None else member_seeds(len(members), cfg.seed)
     fwd = estimate_norm_batch(members, cfg, restarts, seeds)
+    if wave is None:
+        wave = auto_wave(members)
     out = [Cond2Result(operator_norm=e) for e in fwd]
     for w0 in range(0, len(members), wave):
         idx = list(range(w0, min(len(members), w0 + wave)))

@@ -202,6 +202,19 @@ ck_status ck_device_count(int32_t* count) {
   });
 }
 
+ck_status ck_device_memory(uint64_t* free_bytes, uint64_t* total_bytes, int32_t* sm_count) {
+  return guarded([&] {
+    size_t f = 0, t = 0;
+    CK_CUDA(cudaMemGetInfo(&f, &t));
+    int dev = 0, sms = 0;
+    CK_CUDA(cudaGetDevice(&dev));
+    CK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (free_bytes) *free_bytes = f;
+    if (total_bytes) *total_bytes = t;
+    if (sm_count) *sm_count = sms;
+  });
+}
+
 ck_status ck_set_device(int32_t device) {
   return guarded([&] {
     int n = 0;

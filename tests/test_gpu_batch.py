@@ -126,3 +126,14 @@ def test_cond2_batch_matches_cond2(port):
         o = port.cond2(m, c, restarts=2)
         assert r.kappa == pytest.approx(o["kappa"], rel=1e-9)
     assert got[4].kappa == float("inf")
+
+
+def test_auto_wave_fills_the_device(port):
+    """Default ensemble waves: one member per SM, within device memory."""
+    mem = _inv_members(port)[:3]
+    w = batch.auto_wave(mem)
+    assert 3 <= w <= 1024
+    got = batch.cond2_batch(mem, M.cfg(alpha=1e-2, max_iter=100, patience=100), restarts=2)
+    want = batch.cond2_batch(mem, M.cfg(alpha=1e-2, max_iter=100, patience=100), restarts=2, wave=1)
+    for g, h in zip(got, want):
+        assert g.kappa == h.kappa
