@@ -501,7 +501,7 @@ static void launch_transpose_r(const ck_session_s* s, cudaStream_t st) {
 }
 
 void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st, int cl);
-int inv_cluster_size(const BandView& b, int S, int R, size_t smem);
+bool inv_cluster_fits(int cl, int S, int R, size_t smem);
 void prepare_inv_step(size_t smem, int R);
 size_t inv_step_smem(const BandView& b, int R);
 int lu_ring_size(const BandView& b);
@@ -953,16 +953,39 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
   BandView wide = lus[0]->view();
   for (int g = 1; g < S; ++g)
     if (lus[g]->kl + lus[g]->ku > wide.kv) wide = lus[g]->view();
-  int cl = inv_cluster_size(wide, S, R, smem);
-  const int64_t dyn = (int64_t)(smem / sizeof(double));
-  if (cl > 1) {  // the helpers' layout (helper_solve): head values, dot rows, coefficient share
-    const int64_t sh = (std::max(wide.kl, wide.kv) + cl - 2) / (cl - 1) + 2;
-    if ((int64_t)R * kLUBlock + (int64_t)(R + kLUBlock) * sh > dyn) cl = 1;
-  }
-  s->inv_cl = cl;
   const int64_t ts = (std::max(wide.kl, wide.kv) + 2) & ~(int64_t)1;
-  const int64_t dpart_off = cl > 1 ? dyn - (int64_t)cl * R * kLUBlock : dyn;
-  const int64_t tsum_off = cl > 1 ? dpart_off - (int64_t)R * ts : dyn;
+  // dynamic shared memory of a cluster CTA (doubles): the leader's rings, dot
+  // scratch, two tail-sum slots and the dot partials (no stage); a helper's
+  // two head slots, dot rows and coefficient share
+  auto clu_smem = [&](int cl) {
+    int64_t ring_max = 0;
+    for (int g = 0; g < S; ++g) ring_max = std::max<int64_t>(ring_max, lu_ring_size(lus[g]->view()));
+    const int64_t leader = stage_offset(R, (int)ring_max) + 2 * (int64_t)R * ts + (int64_t)cl * R * kLUBlock;
+    const int64_t sh = (std::max(wide.kl, wide.kv) + cl - 2) / (cl - 1) + 2;
+    const int64_t helper = (int64_t)2 * R * kLUBlock + (int64_t)(R + kLUBlock) * sh;
+    return (size_t)(8 * std::max(leader, helper) + 256);
+  };
+  // cluster size (scripts/check_cluster.py): 12 CTAs from kl + ku >= 1024 (config 2),
+  // 8 from >= 256 (config-5 member), when the clusters fit; CK_LU_CLUSTER forces
+  int cl = 1;
+  auto try_cl = [&](int c) {
+    if (cl == 1 && c > 1 && inv_cluster_fits(c, S, R, clu_smem(c))) cl = c;
+  };
+  if (const char* e = std::getenv("CK_LU_CLUSTER")) {
+    try_cl(std::max(1, std::min(16, std::atoi(e))));
+  } else {
+    if (wide.kv >= 4 * kLUClusterMinRows && S * 12 <= 148) try_cl(12);
+    if (wide.kv >= kLUClusterMinRows && S * 8 <= 148) try_cl(8);
+  }
+  if (cl > 1) {
+    smem = clu_smem(cl);
+    s->inv_smem = smem;
+    prepare_inv_step(smem, R);
+  }
+  const int64_t dyn = (int64_t)(smem / sizeof(double));
+  const int64_t dpart_off = cl > 1 ? dyn - 32 - (int64_t)cl * R * kLUBlock : dyn;
+  const int64_t tsum_off = cl > 1 ? dpart_off - (int64_t)2 * R * ts : dyn;  // two slots (block parity)
+  s->inv_cl = cl;
   const int64_t yw = s->npad * R;
   s->PX.alloc(3 * R * s->npad);
   s->MV.alloc(s->npad * R);

@@ -294,6 +294,7 @@ void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, c
 // 358 -> 124 ms; 134 with 8, 125 with 16), when the clusters fit the chip;
 // else 1. CK_LU_CLUSTER=1 disables, =2..16 forces a size.
 static bool cluster_fits(int cl, int S, int R, size_t smem) {
+  prepare_inv_step(smem, R);
   if (cl > 8) {  // non-portable cluster sizes need the opt-in
     switch (R) {
       case 1: cudaFuncSetAttribute(k_inv_step<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); break;
@@ -328,15 +329,7 @@ static bool cluster_fits(int cl, int S, int R, size_t smem) {
   return nclusters >= 1;
 }
 
-int inv_cluster_size(const BandView& b, int S, int R, size_t smem) {
-  if (const char* e = std::getenv("CK_LU_CLUSTER")) {
-    const int cl = std::max(1, std::min(16, std::atoi(e)));
-    return cl > 1 && cluster_fits(cl, S, R, smem) ? cl : 1;
-  }
-  if (b.kv >= 4 * kLUClusterMinRows && S * 12 <= 148 && cluster_fits(12, S, R, smem)) return 12;
-  if (b.kv >= kLUClusterMinRows && S * 8 <= 148 && cluster_fits(8, S, R, smem)) return 8;
-  return 1;
-}
+bool inv_cluster_fits(int cl, int S, int R, size_t smem) { return cluster_fits(cl, S, R, smem); }
 
 }  // namespace ck
 

@@ -323,11 +323,11 @@ struct Clu {
 // straight into every helper's head buffer (remote stores; the next cluster
 // barrier publishes them), so the helpers need no DSMEM round trip.
 template <int R>
-__device__ __forceinline__ void clu_push_head(const Clu& C, int lane, int jb, const double* v) {
+__device__ __forceinline__ void clu_push_head(const Clu& C, int lane, int jb, const double* v, int slot = 0) {
   if (lane >= jb) return;
   auto cl = cooperative_groups::this_cluster();
   for (int k = 1; k < C.size; ++k) {
-    double* d = cl.map_shared_rank(C.hy, k);
+    double* d = cl.map_shared_rank(C.hy + slot * R * kLUBlock, k);
 #pragma unroll
     for (int r = 0; r < R; ++r) d[r * kLUBlock + lane] = v[r];
   }
@@ -338,6 +338,19 @@ __device__ __forceinline__ void clu_sync() { cooperative_groups::this_cluster().
 template <class T>
 __device__ __forceinline__ T* clu_leader(T* p) {
   return cooperative_groups::this_cluster().map_shared_rank(p, 0);
+}
+
+// Leader, after the CTA barrier that follows a head solve: warp k (1..size-1)
+// copies the block's head values from the ring into helper k's head slot
+// (remote stores, published by the next cluster barrier) -- all helpers at once.
+template <int R>
+__device__ __forceinline__ void clu_push_ring_head(const Clu& C, const Ring* ring, int64_t J, int jb,
+                                                   int slot) {
+  const int warp = (int)threadIdx.x >> 5, lane = (int)threadIdx.x & 31;
+  if (warp < 1 || warp >= C.size || lane >= jb) return;
+  double* d = cooperative_groups::this_cluster().map_shared_rank(C.hy + slot * R * kLUBlock, warp);
+#pragma unroll
+  for (int r = 0; r < R; ++r) d[r * kLUBlock + lane] = ring[r][J + lane];
 }
 
 // Rows [lo, hi) of share k out of `size` of the row range [m0, m1).
@@ -486,7 +499,7 @@ __device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring,
           ring[r][J + lane] = hv[r];
           x[r][J + lane] = hv[r];  // head rows are final
         }
-      if (CLU && tail) clu_push_head<R>(C, lane, jb, hv);
+
     } else {
       if (tid == kIssuer && tail) S.issue(b.lb, jb, [&](int c) { return l_run_first(b, blk, c); });
       if (more) {
@@ -497,7 +510,8 @@ __device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring,
     CK_PROF(0);
     __syncthreads();
     CK_PROF(1);
-    if (CLU) clu_sync();  // head values in the ring for the helpers
+    if (CLU && tail) clu_push_ring_head<R>(C, ring, J, jb, 0);
+    if (CLU) clu_sync();  // head values pushed to the helpers
     const int64_t M = wend - J - kLUBlock;  // tail rows
     const int64_t mh = CLU ? 0 : M;  // the leader's own tail rows (none with helpers)
     if (tail) {
@@ -609,6 +623,135 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
         for (int r = 0; r < R; ++r)
           ring[r][J - b.kv + m] = __dsub_rn(ring[r][J - b.kv + m], C.tsum[r * C.ts + m]);
     }
+    if (more) {
+      ph.commit(H, true);
+      px.commit(ring, nlo, lo);
+      lo = nlo;
+    }
+    CK_PROF(12);
+    __syncthreads();
+    CK_PROF(13);
+  }
+}
+
+// U backward on a cluster: one cluster barrier per block. The helpers' share of
+// block J's tail -- every row above the next head block ("far" rows) -- is
+// computed while the leader solves the next head, and folded in by the leader
+// one block later; the next head block's rows ("near": J-32 .. J-1) the leader
+// does itself right after the barrier, after the pending far rows of block J+32
+// (per-row order: blocks in sweep order, as in the single-CTA sweep). Tail sums
+// and head values are double-buffered by block parity.
+template <int R>
+__device__ void sweep_u_backward_clu(const BandView& b, double* const* x, Ring* ring, Head& H,
+                                     const Clu& C) {
+  __shared__ double s_un[kLUBlock][kLUBlock + 1];  // near coefficients [m - (kv-32)][c]
+  const int64_t n = b.n;
+  const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
+  const int64_t nblk = (n + kLUBlock - 1) / kLUBlock;
+  if (nblk == 0) return;
+  HeadPrefetch ph;
+  RowPrefetch<R> px;
+  int64_t lo;  // rows [lo, n) are in the ring
+  {
+    const int64_t J = (nblk - 1) * kLUBlock;
+    lo = lmax(0, J - b.kv);
+    for (int64_t i = lo + tid; i < n; i += nt)
+#pragma unroll
+      for (int r = 0; r < R; ++r) ring[r][i] = x[r][i];
+    H.v[tid >> 5][tid & 31] = u_head_elem(b, J, (int)(n - J), tid);
+    if (tid < kLUBlock) H.rd[tid] = u_head_rd(b, J, (int)(n - J), tid);
+  }
+  __syncthreads();
+  int64_t pend_J = -1, pend_m0 = 0, pend_m1 = 0;  // far rows of the previous block, in flight
+  double un[2] = {0.0, 0.0};                      // near coefficients loaded during the head
+  CK_PROF_INIT;
+  for (int64_t blk = nblk - 1; blk >= 0; --blk) {
+    const int64_t J = blk * kLUBlock;
+    const int jb = (int)lmin(kLUBlock, n - J);
+    const int64_t wbeg = lmax(0, J - b.kv);
+    const int64_t nlo = lmax(0, J - kLUBlock - b.kv);
+    const bool more = blk > 0;
+    const bool tail = J > wbeg;
+    const int64_t m0 = wbeg - (J - b.kv);        // first tail row (relative)
+    const int64_t mn = lmax(m0, b.kv - kLUBlock);  // first near row
+    if (warp == 0) {
+      double h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) h[r] = lane < jb ? ring[r][J + lane] : 0.0;
+#pragma unroll
+      for (int c = kLUBlock - 1; c >= 0; --c) {
+        const double d = H.v[c][c], rd = H.rd[c];
+        const double u = lane < c ? H.v[c][lane] : 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double y = div_rcp(__shfl_sync(0xffffffffu, h[r], c), d, rd);
+          const double t = __dsub_rn(h[r], __dmul_rn(u, y));
+          h[r] = lane == c ? y : t;
+        }
+      }
+      if (lane < jb)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          ring[r][J + lane] = h[r];
+          x[r][J + lane] = h[r];
+        }
+
+    } else {
+      // near coefficients U(J - kv + m, J + c), m in [mn, kv): thread q -> (row, column)
+      if (tail) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int q = tid - 32 + k * (kSweepThreads - 32);
+          if (q < kLUBlock * kLUBlock) {
+            const int rr = q >> 5, c = q & 31;
+            const int64_t m = b.kv - kLUBlock + rr;
+            un[k] = (m >= mn && m >= c && c < jb) ? b.ab[u_run_first(b, J, c) + m] : 0.0;
+          }
+        }
+      }
+      if (more) {
+        ph.load([&](int q) { return u_head_elem(b, J - kLUBlock, kLUBlock, q); },
+                [&](int c) { return u_head_rd(b, J - kLUBlock, kLUBlock, c); });
+        px.load(x, nlo, lo);
+      }
+    }
+    if (warp != 0 && tail) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int q = tid - 32 + k * (kSweepThreads - 32);
+        if (q < kLUBlock * kLUBlock) s_un[q >> 5][q & 31] = un[k];
+      }
+    }
+    CK_PROF(8);
+    __syncthreads();
+    CK_PROF(9);
+    if (tail) clu_push_ring_head<R>(C, ring, J, jb, (int)(blk & 1));
+    clu_sync();  // head values pushed; the far sums of block J+32 are in their slot
+    if (pend_J >= 0) {  // far rows of block J+32: rows pend_J - kv + m, m in [pend_m0, pend_m1)
+      const double* ts = C.tsum + (int64_t)(((pend_J / kLUBlock) & 1) * R) * C.ts;
+      for (int64_t m = pend_m0 + tid; m < pend_m1; m += nt)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          ring[r][pend_J - b.kv + m] = __dsub_rn(ring[r][pend_J - b.kv + m], ts[r * C.ts + m]);
+      __syncthreads();
+    }
+    if (tail && tid < b.kv - mn) {  // near rows, one thread each, columns in order
+      const int rr = (int)(mn - (b.kv - kLUBlock)) + tid;
+      const int64_t i = J - kLUBlock + rr;
+      double sm[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[r] = 0.0;
+      for (int c = 0; c < jb; ++c) {
+        const double u = s_un[rr][c];
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[r] = __fma_rn(u, ring[r][J + c], sm[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) ring[r][i] = __dsub_rn(ring[r][i], sm[r]);
+    }
+    pend_J = tail ? J : -1;
+    pend_m0 = m0;
+    pend_m1 = b.kv - kLUBlock;
     if (more) {
       ph.commit(H, true);
       px.commit(ring, nlo, lo);
@@ -841,8 +984,12 @@ __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, d
   if (!transpose) {
     S.layout(b.stage_cap, kl, b.stage_min);
     sweep_l_forward<R, CLU>(b, x, ring, H, S, C);
-    S.layout(b.stage_cap, kv, b.stage_min);
-    sweep_u_backward<R, CLU>(b, x, ring, H, S, C);
+    if (CLU) {
+      sweep_u_backward_clu<R>(b, x, ring, H, C);
+    } else {
+      S.layout(b.stage_cap, kv, b.stage_min);
+      sweep_u_backward<R, CLU>(b, x, ring, H, S, C);
+    }
   } else {
     S.layout(b.stage_cap, kv, b.stage_min);
     sweep_ut_forward<R, CLU>(b, x, ring, s_dot, H, S, C);
@@ -863,8 +1010,8 @@ __device__ void helper_solve(const BandView& b, double* local, int ring_size, bo
 #pragma unroll
   for (int r = 0; r < R; ++r) lring[r] = Ring{clu_leader(local + (int64_t)r * ring_size), ring_size - 1};
   const int64_t shmax = (lmax(b.kl, b.kv) + c.size - 2) / (c.size - 1) + 2;
-  double* hy = local;                         // [R][32] head values
-  double* hl = hy + (int64_t)R * kLUBlock;      // [R][share] ring rows of a dot share
+  double* hy = local;                            // [2][R][32] head values (block parity)
+  double* hl = hy + (int64_t)2 * R * kLUBlock;   // [R][share] ring rows of a dot share
   double* cf = hl + (int64_t)R * shmax;         // [32][share] coefficients of a share
   auto share = [&](int64_t m0, int64_t m1, int64_t& lo, int64_t& hi) {  // helpers only
     lo = clu_cut(m0, m1, c.rank - 1, c.size - 1);
@@ -887,21 +1034,36 @@ __device__ void helper_solve(const BandView& b, double* local, int ring_size, bo
       if (tail) helper_tail<R>(lo, hi, jb, hy, cf, c);
       clu_sync();
     }
-    for (int64_t blk = nblk - 1; blk >= 0; --blk) {  // U backward
+    // U backward (sweep_u_backward_clu): one barrier per block; far rows of
+    // block J (above J - 32) while the leader solves the next head
+    auto u_share = [&](int64_t blk, int64_t& lo, int64_t& hi) {
+      const int64_t J = blk * kLUBlock;
+      const int64_t wbeg = lmax(0, J - b.kv);
+      if (!(J > wbeg)) return false;
+      share(wbeg - (J - b.kv), lmax(wbeg - (J - b.kv), b.kv - kLUBlock), lo, hi);
+      return true;
+    };
+    auto u_fetch = [&](int64_t blk) {
+      int64_t lo, hi;
+      if (blk < 0 || !u_share(blk, lo, hi)) return;
+      const int64_t J = blk * kLUBlock;
+      helper_fetch(lo, hi, (int)lmin(kLUBlock, n - J), cf, [&](int64_t m, int cc) {
+        return m < cc ? 0.0 : b.ab[u_run_first(b, J, cc) + m];
+      });
+    };
+    u_fetch(nblk - 1);
+    for (int64_t blk = nblk - 1; blk >= 0; --blk) {
       const int64_t J = blk * kLUBlock;
       const int jb = (int)lmin(kLUBlock, n - J);
-      const int64_t wbeg = lmax(0, J - b.kv);
-      const bool tail = J > wbeg;
-      int64_t lo = 0, hi = 0;
-      if (tail) {
-        share(wbeg - (J - b.kv), b.kv, lo, hi);
-        helper_fetch(lo, hi, jb, cf, [&](int64_t m, int cc) {
-          return m < cc ? 0.0 : b.ab[u_run_first(b, J, cc) + m];
-        });
+      clu_sync();  // head values of block J pushed, cf complete
+      int64_t lo, hi;
+      if (u_share(blk, lo, hi)) {
+        Clu cs = c;
+        cs.tsum = c.tsum + (int64_t)((blk & 1) * R) * c.ts;
+        helper_tail<R>(lo, hi, jb, hy + (blk & 1) * R * kLUBlock, cf, cs);
       }
-      clu_sync();  // head values pushed by the leader, cf complete
-      if (tail) helper_tail<R>(lo, hi, jb, hy, cf, c);
-      clu_sync();
+      __syncthreads();  // cf consumed
+      u_fetch(blk - 1);
     }
   } else {
     // dots of block J: coefficients fetched while the leader combines and
