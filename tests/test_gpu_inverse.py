@@ -265,3 +265,21 @@ def test_cluster_sweeps_match_single_cta_and_oracle(port, monkeypatch, cl):
     assert clu.value == pytest.approx(one.value, rel=1e-12)
     assert clu.value == pytest.approx(o.value, rel=1e-9)
     assert np.linalg.norm(port.lu_solve(rf, clu.witness)) == pytest.approx(clu.value, rel=1e-11)
+
+
+def test_cluster_sweeps_several_columns(port, monkeypatch):
+    """Restart columns (R = 3) through the cluster split: every column agrees
+    with the single-CTA sweep."""
+    from paper_2409_11515_b200 import inverse
+    a = M.row_scaled(M.laplacian2d(20), port, 7)
+    f = ck.lu_factorize(a, 1e-14)
+    c = M.cfg(alpha=1e-2, max_iter=200, patience=200, seed=4)
+    res = {}
+    for cl in ("1", "8"):
+        monkeypatch.setenv("CK_LU_CLUSTER", cl)
+        s = inverse.InverseSession(ck.InverseOracle(f), c, [4, 5, 6])
+        assert s.run()
+        res[cl] = [s.result(k) for k in range(3)]
+    for e1, e8 in zip(res["1"], res["8"]):
+        assert e8.iterations == e1.iterations
+        assert e8.value == pytest.approx(e1.value, rel=1e-12)
