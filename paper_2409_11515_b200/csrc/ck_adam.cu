@@ -960,9 +960,9 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
   auto clu_smem = [&](int cl) {
     int64_t ring_max = 0;
     for (int g = 0; g < S; ++g) ring_max = std::max<int64_t>(ring_max, lu_ring_size(lus[g]->view()));
-    const int64_t leader = stage_offset(R, (int)ring_max) + 2 * (int64_t)R * ts + (int64_t)cl * R * kLUBlock;
+    const int64_t leader = stage_offset(R, (int)ring_max) + 2 * (int64_t)R * ts + 2 * (int64_t)cl * R * kLUBlock;
     const int64_t sh = (std::max(wide.kl, wide.kv) + cl - 2) / (cl - 1) + 2;
-    const int64_t helper = (int64_t)2 * R * kLUBlock + (int64_t)(R + kLUBlock) * sh;
+    const int64_t helper = (int64_t)2 * R * kLUBlock + (int64_t)(R + 2 * kLUBlock) * sh;  // two cf slots
     return (size_t)(8 * std::max(leader, helper) + 256);
   };
   // cluster size (scripts/check_cluster.py): 12 CTAs from kl + ku >= 1024 (config 2),
@@ -983,7 +983,7 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
     prepare_inv_step(smem, R);
   }
   const int64_t dyn = (int64_t)(smem / sizeof(double));
-  const int64_t dpart_off = cl > 1 ? dyn - 32 - (int64_t)cl * R * kLUBlock : dyn;
+  const int64_t dpart_off = cl > 1 ? dyn - 32 - 2 * (int64_t)cl * R * kLUBlock : dyn;  // two slots
   const int64_t tsum_off = cl > 1 ? dpart_off - (int64_t)2 * R * ts : dyn;  // two slots (block parity)
   s->inv_cl = cl;
   const int64_t yw = s->npad * R;

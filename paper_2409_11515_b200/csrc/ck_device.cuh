@@ -242,4 +242,16 @@ __device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int 
   }
 }
 
+// Asynchronous global -> shared copies (cp.async, 8 bytes), grouped per thread.
+__device__ __forceinline__ void cp_async_elem(double* smem, const double* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 }  // namespace ck

@@ -385,6 +385,22 @@ __device__ __forceinline__ void helper_fetch(int64_t lo, int64_t hi, int jb, dou
   }
 }
 
+// Helper: the same share copied asynchronously (cp.async, 8 bytes per element,
+// warp c -> column c, 32 consecutive rows per step): the copies proceed while
+// the helper works on the previous block; cp_async_wait<0>() + a CTA barrier
+// before use. Element (m, c) of the share is src[first(c) + (m - lo)].
+template <class First>
+__device__ __forceinline__ void helper_fetch_async(int64_t lo, int64_t hi, int jb, double* cf,
+                                                   const double* src, First first) {
+  const int sh = (int)(hi - lo);
+  const int c = (int)threadIdx.x >> 5, l = (int)threadIdx.x & 31;
+  if (c < jb) {
+    const double* s0 = src + first(c);
+    for (int mm = l; mm < sh; mm += 32) cp_async_elem(cf + c * sh + mm, s0 + mm);
+  }
+  cp_async_commit();
+}
+
 // Helper: sums of rows m in [lo, hi) of a block tail, sum_c cf(m, c) * y_c,
 // written to the leader's tsum (same lane split and order as tail_update).
 template <int R>
@@ -855,6 +871,96 @@ __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring
   __syncthreads();
 }
 
+// U^T forward on a cluster: one cluster barrier per block. The dots of block J
+// over rows below J - 32 ("far") are the helpers', computed one block ahead
+// (those rows are final once head J - 64 is done) into a slot by block parity;
+// the rows of the previous head block ("near", J - 32 .. J - 1) the leader
+// folds in itself, with coefficients loaded during that head.
+template <int R>
+__device__ void sweep_ut_forward_clu(const BandView& b, double* const* x, Ring* ring, double* s_dot,
+                                     Head& H, const Clu& C) {
+  __shared__ double s_un[kLUBlock][kLUBlock + 1];  // U(J - 32 + k, J + c) for the next block
+  const int64_t n = b.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (n == 0) return;
+  HeadPrefetch ph;
+  RowPrefetch<R> px;
+  H.v[tid >> 5][tid & 31] = u_head_elem(b, 0, (int)lmin(kLUBlock, n), tid);
+  if (tid < kLUBlock) H.rd[tid] = u_head_rd(b, 0, (int)lmin(kLUBlock, n), tid);
+  if (tid < lmin(kLUBlock, n))
+#pragma unroll
+    for (int r = 0; r < R; ++r) ring[r][tid] = x[r][tid];
+  __syncthreads();
+  CK_PROF_INIT;
+  for (int64_t J = 0; J < n; J += kLUBlock) {
+    const int jb = (int)lmin(kLUBlock, n - J);
+    const int64_t J1 = J + kLUBlock;
+    const bool dots = J > 0;
+    if (dots && tid < R * kLUBlock) {  // thread (r, c): far partials, then the near rows
+      const int r = tid >> 5, c = tid & 31;
+      double t = 0.0;
+      if (J > kLUBlock) {
+        const double* dp = C.dpart + (int64_t)((J / kLUBlock) & 1) * C.size * R * kLUBlock;
+        for (int k = 1; k < C.size; ++k) t = __dadd_rn(t, dp[((int64_t)k * R + r) * kLUBlock + c]);
+      }
+      double sn = 0.0;
+      for (int k = 0; k < kLUBlock; ++k) sn = __fma_rn(s_un[k][c], ring[r][J - kLUBlock + k], sn);
+      s_dot[tid] = __dadd_rn(t, sn);
+    }
+    CK_PROF(16);
+    __syncthreads();
+    CK_PROF(17);
+    if (warp == 0) {
+      double h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        h[r] = lane < jb ? (dots ? __dsub_rn(ring[r][J + lane], s_dot[r * kLUBlock + lane])
+                                 : ring[r][J + lane])
+                         : 0.0;
+#pragma unroll
+      for (int c = 0; c < kLUBlock; ++c) {
+        const double d = H.v[c][c], rd = H.rd[c];
+        const double u = lane > c ? H.v[lane][c] : 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double w = div_rcp(__shfl_sync(0xffffffffu, h[r], c), d, rd);
+          const double t = __dsub_rn(h[r], __dmul_rn(u, w));
+          h[r] = lane == c ? w : t;
+        }
+      }
+      if (lane < jb)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          ring[r][J + lane] = h[r];
+          x[r][J + lane] = h[r];
+        }
+    } else if (J1 < n) {
+      const int jb1 = (int)lmin(kLUBlock, n - J1);
+      ph.load([&](int q) { return u_head_elem(b, J1, jb1, q); },
+              [&](int c) { return u_head_rd(b, J1, jb1, c); });
+      px.load(x, J1, J1 + jb1);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {  // near coefficients of block J1: rows J + k
+        const int q = tid - 32 + kk * (kSweepThreads - 32);
+        if (q < kLUBlock * kLUBlock) {
+          const int k = q >> 5, c = q & 31;
+          const bool in = c < jb1 && c + kLUBlock - k <= b.kv;
+          s_un[k][c] = in ? b.ab[u_run_first(b, J1, c) + (b.kv - kLUBlock + k)] : 0.0;
+        }
+      }
+    }
+    CK_PROF(20);
+    __syncthreads();
+    CK_PROF(21);
+    clu_sync();  // block J final: the helpers go on with the far dots of block J + 64
+    if (J1 < n) {
+      ph.commit(H, true);
+      px.commit(ring, J1, lmin(n, J1 + kLUBlock));
+    }
+  }
+  __syncthreads();
+}
+
 // --------------------------------------------------------- L^T backward
 // x := (L-part)^{-T} x: LAPACK gbtrs 'T' second half, blocks in reverse.
 // Phase 1: warp c forms head column c's dot over the block's tail (from the
@@ -991,8 +1097,12 @@ __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, d
       sweep_u_backward<R, CLU>(b, x, ring, H, S, C);
     }
   } else {
-    S.layout(b.stage_cap, kv, b.stage_min);
-    sweep_ut_forward<R, CLU>(b, x, ring, s_dot, H, S, C);
+    if (CLU) {
+      sweep_ut_forward_clu<R>(b, x, ring, s_dot, H, C);
+    } else {
+      S.layout(b.stage_cap, kv, b.stage_min);
+      sweep_ut_forward<R, CLU>(b, x, ring, s_dot, H, S, C);
+    }
     S.layout(b.stage_cap, kl, b.stage_min);
     sweep_l_backward<R, CLU>(b, x, ring, s_dot, H, S, C);
   }
@@ -1066,27 +1176,42 @@ __device__ void helper_solve(const BandView& b, double* local, int ring_size, bo
       u_fetch(blk - 1);
     }
   } else {
-    // dots of block J: coefficients fetched while the leader combines and
-    // solves the previous head (between its two barriers)
-    auto ut_fetch = [&](int64_t J) {
-      if (J <= 0 || J >= n) return;
-      int64_t lo, hi;
-      share(lmax(0, b.kv - J), b.kv, lo, hi);
-      helper_fetch(lo, hi, (int)lmin(kLUBlock, n - J), cf,
-                   [&](int64_t m, int cc) { return m < cc ? 0.0 : b.ab[u_run_first(b, J, cc) + m]; });
+    // U^T forward (sweep_ut_forward_clu): after barrier B(J) the rows below
+    // J + 32 are final; the far dots of block J + 64 (rows below J + 32) go
+    // into the partial slot of that block's parity. The coefficient shares are
+    // double-buffered and copied asynchronously one block ahead.
+    auto ut_share = [&](int64_t Jd, int64_t& lo, int64_t& hi) {
+      share(lmax(0, b.kv - Jd), lmax(lmax(0, b.kv - Jd), b.kv - kLUBlock), lo, hi);
     };
-    for (int64_t J = 0; J < n; J += kLUBlock) {  // U^T forward (block 0 has no dots)
-      const int jb = (int)lmin(kLUBlock, n - J);
-      if (J > 0) {
-        int64_t lo, hi;
-        share(lmax(0, b.kv - J), b.kv, lo, hi);
-        __syncthreads();  // cf complete
-        helper_dots<R>(lring, J - b.kv, lo, hi, jb, 0, hl, cf, c);
+    double* cfs[2] = {cf, cf + (int64_t)kLUBlock * shmax};
+    auto ut_fetch = [&](int64_t Jd) {
+      if (Jd >= n) {
+        cp_async_commit();
+        return;
       }
-      clu_sync();
-      ut_fetch(J + kLUBlock);
-      clu_sync();
+      int64_t lo, hi;
+      ut_share(Jd, lo, hi);
+      helper_fetch_async(lo, hi, (int)lmin(kLUBlock, n - Jd), cfs[(Jd / kLUBlock) & 1], b.ab,
+                         [&](int cc) { return u_run_first(b, Jd, cc) + lo; });
+    };
+    ut_fetch(2 * kLUBlock);
+    for (int64_t J = 0; J < n; J += kLUBlock) {
+      clu_sync();  // B(J)
+      const int64_t Jd = J + 2 * kLUBlock;
+      if (Jd < n) {
+        int64_t lo, hi;
+        ut_share(Jd, lo, hi);
+        cp_async_wait<0>();
+        __syncthreads();  // the share of block Jd is in
+        ut_fetch(Jd + kLUBlock);  // next block's share streams in meanwhile
+        Clu cs = c;
+        cs.dpart = c.dpart + (int64_t)((Jd / kLUBlock) & 1) * c.size * R * kLUBlock;
+        helper_dots<R>(lring, Jd - b.kv, lo, hi, (int)lmin(kLUBlock, n - Jd), 0, hl,
+                       cfs[(Jd / kLUBlock) & 1], cs);
+      }
     }
+    cp_async_wait<0>();
+    __syncthreads();
     auto lt_dots = [&](int64_t blk, int64_t& lo, int64_t& hi) {
       const int64_t J = blk * kLUBlock;
       const int jb = (int)lmin(kLUBlock, n - J);
