@@ -405,7 +405,7 @@ __device__ __forceinline__ void helper_fetch_async(int64_t lo, int64_t hi, int j
 // written to the leader's tsum (same lane split and order as tail_update).
 template <int R>
 __device__ __forceinline__ void helper_tail(int64_t lo, int64_t hi, int jb, const double* hy,
-                                            const double* cf, const Clu& C) {
+                                            const double* cf, const Clu& C, bool umask = false) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lg = tail_log_lanes(hi - lo);
   const int rs_bits = 5 - lg, G = 1 << lg;
@@ -422,7 +422,7 @@ __device__ __forceinline__ void helper_tail(int64_t lo, int64_t hi, int jb, cons
     if (act) {
 #pragma unroll 8
       for (int c = g; c < jb; c += G) {
-        const double l = cf[(int64_t)c * (hi - lo) + (m - lo)];
+        const double l = (umask && m < c) ? 0.0 : cf[(int64_t)c * (hi - lo) + (m - lo)];
 #pragma unroll
         for (int r = 0; r < R; ++r) sm[r] = __fma_rn(l, hy[r * kLUBlock + c], sm[r]);
       }
@@ -1145,7 +1145,9 @@ __device__ void helper_solve(const BandView& b, double* local, int ring_size, bo
       clu_sync();
     }
     // U backward (sweep_u_backward_clu): one barrier per block; far rows of
-    // block J (above J - 32) while the leader solves the next head
+    // block J (above J - 32) while the leader solves the next head. Coefficient
+    // shares double-buffered, copied asynchronously one block ahead (U runs are
+    // masked above the band, m < c, at use).
     auto u_share = [&](int64_t blk, int64_t& lo, int64_t& hi) {
       const int64_t J = blk * kLUBlock;
       const int64_t wbeg = lmax(0, J - b.kv);
@@ -1153,28 +1155,34 @@ __device__ void helper_solve(const BandView& b, double* local, int ring_size, bo
       share(wbeg - (J - b.kv), lmax(wbeg - (J - b.kv), b.kv - kLUBlock), lo, hi);
       return true;
     };
+    double* cfs[2] = {cf, cf + (int64_t)kLUBlock * shmax};
     auto u_fetch = [&](int64_t blk) {
       int64_t lo, hi;
-      if (blk < 0 || !u_share(blk, lo, hi)) return;
+      if (blk < 0 || !u_share(blk, lo, hi)) {
+        cp_async_commit();
+        return;
+      }
       const int64_t J = blk * kLUBlock;
-      helper_fetch(lo, hi, (int)lmin(kLUBlock, n - J), cf, [&](int64_t m, int cc) {
-        return m < cc ? 0.0 : b.ab[u_run_first(b, J, cc) + m];
-      });
+      helper_fetch_async(lo, hi, (int)lmin(kLUBlock, n - J), cfs[blk & 1], b.ab,
+                         [&](int cc) { return u_run_first(b, J, cc) + lo; });
     };
     u_fetch(nblk - 1);
     for (int64_t blk = nblk - 1; blk >= 0; --blk) {
       const int64_t J = blk * kLUBlock;
       const int jb = (int)lmin(kLUBlock, n - J);
-      clu_sync();  // head values of block J pushed, cf complete
+      clu_sync();  // head values of block J pushed
+      cp_async_wait<0>();
+      __syncthreads();  // the share of block J is in
+      u_fetch(blk - 1);  // the next block's share streams in meanwhile
       int64_t lo, hi;
       if (u_share(blk, lo, hi)) {
         Clu cs = c;
         cs.tsum = c.tsum + (int64_t)((blk & 1) * R) * c.ts;
-        helper_tail<R>(lo, hi, jb, hy + (blk & 1) * R * kLUBlock, cf, cs);
+        helper_tail<R>(lo, hi, jb, hy + (blk & 1) * R * kLUBlock, cfs[blk & 1], cs, true);
       }
-      __syncthreads();  // cf consumed
-      u_fetch(blk - 1);
     }
+    cp_async_wait<0>();
+    __syncthreads();
   } else {
     // U^T forward (sweep_ut_forward_clu): after barrier B(J) the rows below
     // J + 32 are final; the far dots of block J + 64 (rows below J + 32) go
