@@ -558,14 +558,13 @@ __device__ void sweep_l_forward(const BandView& b, double* const* x, Ring* ring,
 // ----------------------------------------------------------- U backward
 // x := U^{-1} x (backward), U of bandwidth kv above the diagonal; blocks in
 // reverse, same two phases as sweep_l_forward.
-template <int R, bool CLU = false>
-__device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S,
-                                 const Clu& C) {
+template <int R>
+__device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring, Head& H, Stage& S) {
   const int64_t n = b.n;
   const int tid = threadIdx.x, nt = kSweepThreads, lane = tid & 31, warp = tid >> 5;
   const int64_t nblk = (n + kLUBlock - 1) / kLUBlock;
   if (nblk == 0) return;
-  const int lg = tail_log_lanes(CLU ? (b.kv + C.size - 1) / C.size : b.kv);
+  const int lg = tail_log_lanes(b.kv);
   HeadPrefetch ph;
   RowPrefetch<R> px;
   int64_t lo;  // rows [lo, n) are in the ring
@@ -608,7 +607,6 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
           ring[r][J + lane] = h[r];
           x[r][J + lane] = h[r];
         }
-      if (CLU && tail) clu_push_head<R>(C, lane, jb, h);
     } else {
       if (tid == kIssuer && tail) S.issue(b.ab, jb, [&](int c) { return u_run_first(b, J, c); });
       if (more) {
@@ -620,24 +618,15 @@ __device__ void sweep_u_backward(const BandView& b, double* const* x, Ring* ring
     CK_PROF(8);
     __syncthreads();
     CK_PROF(9);
-    if (CLU) clu_sync();  // head values in the ring for the helpers
     const int64_t m0 = wbeg - (J - b.kv);  // first tail row (relative)
-    const int64_t mh = CLU ? m0 : b.kv;  // the leader's own tail rows (none with helpers)
     if (tail) {
       S.wait();
       // tail row i = J - kv + m; U(i, J+c) lies in the band for m >= c
-      tail_update<R>(J - b.kv, m0, mh, J, jb, lg, ring, [&](int64_t m, int c) {
+      tail_update<R>(J - b.kv, m0, b.kv, J, jb, lg, ring, [&](int64_t m, int c) {
         if (m < c) return 0.0;
         const int64_t f = u_run_first(b, J, c);
         return m < S.srows ? S.at(c, (int)(f & 1), m) : b.ab[f + m];
       });
-    }
-    if (CLU) {
-      clu_sync();  // helper sums in tsum
-      for (int64_t m = mh + tid; m < b.kv; m += nt)
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          ring[r][J - b.kv + m] = __dsub_rn(ring[r][J - b.kv + m], C.tsum[r * C.ts + m]);
     }
     if (more) {
       ph.commit(H, true);
@@ -784,9 +773,9 @@ __device__ void sweep_u_backward_clu(const BandView& b, double* const* x, Ring* 
 // Phase 1: warp c forms head row c's dot over the final rows below J (from
 // the stage). Phase 2: warp 0 solves the head triangle while the stage and
 // the idle warps fetch the next block.
-template <int R, bool CLU = false>
+template <int R>
 __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring, double* s_dot,
-                                 Head& H, Stage& S, const Clu& C) {
+                                 Head& H, Stage& S) {
   const int64_t n = b.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (n == 0) return;
@@ -804,27 +793,18 @@ __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring
     const int jb = (int)lmin(kLUBlock, n - J);
     const int64_t J1 = J + kLUBlock;
     const bool dots = J > 0;
-    const int64_t mh = CLU ? 0 : b.kv;  // the leader's own dot rows (none with helpers)
     if (dots) {
       S.wait();
       if (warp < jb) {
         const int c = warp;
         // rows i = J - kv + m of column J+c: in the band for m >= c, i >= 0
         const int64_t f = u_run_first(b, J, c);
-        warp_dot<R>(J - b.kv, lmax(c, b.kv - J), mh, ring, CLU ? C.dpart : s_dot, c, [&](int64_t m) {
+        warp_dot<R>(J - b.kv, lmax(c, b.kv - J), b.kv, ring, s_dot, c, [&](int64_t m) {
           return m < S.srows ? S.at(c, (int)(f & 1), m) : b.ab[f + m];
         });
       }
     }
     CK_PROF(16);
-    if (CLU) {
-      clu_sync();  // every rank's partials in dpart
-      if (dots && tid < R * kLUBlock) {
-        double t = 0.0;
-        for (int k = 0; k < C.size; ++k) t = __dadd_rn(t, C.dpart[(int64_t)k * R * kLUBlock + tid]);
-        s_dot[tid] = t;
-      }
-    }
     __syncthreads();
     CK_PROF(17);
     if (warp == 0) {
@@ -862,7 +842,6 @@ __device__ void sweep_ut_forward(const BandView& b, double* const* x, Ring* ring
     CK_PROF(20);
     __syncthreads();
     CK_PROF(21);
-    if (CLU) clu_sync();  // the block's rows are final for the helpers
     if (J1 < n) {
       ph.commit(H, true);
       px.commit(ring, J1, lmin(n, J1 + kLUBlock));
@@ -1094,14 +1073,14 @@ __device__ __forceinline__ void inv_solve(const BandView& b, double* const* x, d
       sweep_u_backward_clu<R>(b, x, ring, H, C);
     } else {
       S.layout(b.stage_cap, kv, b.stage_min);
-      sweep_u_backward<R, CLU>(b, x, ring, H, S, C);
+      sweep_u_backward<R>(b, x, ring, H, S);
     }
   } else {
     if (CLU) {
       sweep_ut_forward_clu<R>(b, x, ring, s_dot, H, C);
     } else {
       S.layout(b.stage_cap, kv, b.stage_min);
-      sweep_ut_forward<R, CLU>(b, x, ring, s_dot, H, S, C);
+      sweep_ut_forward<R>(b, x, ring, s_dot, H, S);
     }
     S.layout(b.stage_cap, kl, b.stage_min);
     sweep_l_backward<R, CLU>(b, x, ring, s_dot, H, S, C);
