@@ -190,6 +190,12 @@ ck_status ck_session_free(ck_session s);
  * structure). On failure *fail_col / *fail_pivot (may be NULL) are set. */
 ck_status ck_lu_factorize(ck_matrix a, double pivot_tol, ck_lu* out, int64_t* fail_col,
                           double* fail_pivot);
+/* lu_factorize of nmem matrices at once (run_bench's per-matrix cond2 over an
+ * ensemble, bench.hpp:430-442): one panel loop for the whole batch. status[g] is
+ * CK_OK with out[g] the factors, or the member's error (out[g] = NULL) with
+ * fail_col / fail_pivot (optional arrays) as for ck_lu_factorize. */
+ck_status ck_lu_factorize_batch(const ck_matrix* a, int32_t nmem, double pivot_tol, ck_lu* out,
+                                int32_t* status, int64_t* fail_col, double* fail_pivot);
 ck_status ck_lu_free(ck_lu f);
 /* n, band widths, LUFactors::pivot_min (lu.hpp:46), device bytes. */
 ck_status ck_lu_get_info(ck_lu f, int64_t* n, int64_t* kl, int64_t* ku, double* pivot_min,

@@ -101,22 +101,38 @@ class BatchSession(Session):
 # ------------------------------------------------------------ sigma_min side
 def lu_factorize_many(members: Sequence[SparseMatrix], pivot_tol: float = 1e-14,
                       threads: int = 8) -> list:
-    """lu_factorize for every member, several factorisations in flight on the
-    device at once (each runs on its own stream; the C calls release the GIL).
-    Singular members give the exception instance instead of factors."""
-    from concurrent.futures import ThreadPoolExecutor  # noqa: PLC0415
-    from .inverse import lu_factorize  # noqa: PLC0415
-
-    def one(m):
-        try:
-            return lu_factorize(m, pivot_tol)
-        except (StructurallySingular, NumericallySingular) as e:
-            return e
-
-    if threads <= 1 or len(members) <= 1:
-        return [one(m) for m in members]
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        return list(ex.map(one, members))
+    """lu_factorize for every member in one batched device factorisation
+    (ck_lu_factorize_batch: one panel loop for all members). Singular members
+    give the exception instance instead of factors. `threads` is kept for
+    compatibility (the device batch needs none)."""
+    from .errors import from_status  # noqa: PLC0415
+    from .inverse import LUFactors  # noqa: PLC0415
+    del threads
+    if not members:
+        return []
+    lib = _lib.load()
+    S = len(members)
+    hs = (C.c_void_p * S)()
+    for g, m in enumerate(members):
+        hs[g] = m.device().handle
+    out = (C.c_void_p * S)()
+    status = np.zeros(S, np.int32)
+    fcol = np.zeros(S, np.int64)
+    fpiv = np.zeros(S)
+    _lib.check(lib.ck_lu_factorize_batch(C.cast(hs, C.c_void_p), S, pivot_tol, C.cast(out, C.c_void_p),
+                                         _lib.i32ptr(status), fcol.ctypes.data_as(_lib.i64p),
+                                         _lib.dptr(fpiv)), "ck_lu_factorize_batch")
+    res = []
+    for g, m in enumerate(members):
+        if status[g] == 0:
+            res.append(LUFactors(C.c_void_p(out[g]), m.nrows))
+        else:
+            e = from_status(int(status[g]), f"lu_factorize: member {g}: column {int(fcol[g])}, "
+                                            f"pivot {float(fpiv[g]):.3e}")
+            if not isinstance(e, (StructurallySingular, NumericallySingular)):
+                raise e
+            res.append(e)
+    return res
 
 
 def _lu_handles(factors):

@@ -973,7 +973,7 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
   };
   if (const char* e = std::getenv("CK_LU_CLUSTER")) {
     try_cl(std::max(1, std::min(16, std::atoi(e))));
-  } else {
+  } else if (R == 1) {  // measured with one column per system; 4 columns ran slower split (214 vs 134 ms)
     if (wide.kv >= 4 * kLUClusterMinRows && S * 12 <= 148) try_cl(12);
     if (wide.kv >= kLUClusterMinRows && S * 8 <= 148) try_cl(8);
   }

@@ -606,6 +606,31 @@ ck_status ck_lu_factorize(ck_matrix a, double pivot_tol, ck_lu* out, int64_t* fa
   });
 }
 
+ck_status ck_lu_factorize_batch(const ck_matrix* a, int32_t nmem, double pivot_tol, ck_lu* out,
+                                int32_t* status, int64_t* fail_col, double* fail_pivot) {
+  return guarded([&] {
+    if (nmem < 1 || !a || !out || !status) fail(CK_ERR_INVALID_ARGUMENT, "lu_factorize_batch: bad arguments");
+    std::vector<ck_matrix_s*> ms((size_t)nmem);
+    for (int g = 0; g < nmem; ++g) ms[g] = M(a[g]);
+    std::vector<ck_lu_s*> fs((size_t)nmem, nullptr);
+    try {
+      for (int g = 0; g < nmem; ++g) fs[g] = new ck_lu_s();
+      ck::lu_factorize_batch(fs.data(), ms.data(), nmem, pivot_tol, status, fail_col, fail_pivot);
+    } catch (...) {
+      for (auto* f : fs) delete f;
+      throw;
+    }
+    for (int g = 0; g < nmem; ++g) {
+      if (status[g] == CK_OK) {
+        out[g] = fs[g];
+      } else {
+        delete fs[g];
+        out[g] = nullptr;
+      }
+    }
+  });
+}
+
 ck_status ck_lu_free(ck_lu f) {
   return guarded([&] {
     if (!f) return;

@@ -6,11 +6,16 @@
 
 #include "ck_common.h"
 
+struct ck_lu_s;
+
 namespace ck {
 
 constexpr int kNormParts = 296;  // partial blocks of the standalone norm (2 x 148 SMs)
 
 void matrix_info(const ck_matrix_s* a, ck_matrix_info* info);
+// Batched band LU (ck_lu.cu): codes[g] = CK_OK or the member's error status.
+void lu_factorize_batch(ck_lu_s* const* fs, ck_matrix_s* const* ms, int S, double pivot_tol,
+                        int32_t* codes, int64_t* fail_cols, double* fail_pivots);
 void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* rp,
                    const int32_t* ci, const double* va);
 void matrix_apply_host(ck_matrix_s* m, bool transpose, const double* x, double* y);

@@ -65,13 +65,18 @@ __global__ void k_band_fill(SellView A, int64_t nrows_pad, const int32_t* __rest
 }
 
 // ----------------------------------------------------------- factorisation
-// Panel: columns j0 .. j0+jb-1 by one CTA.
-__global__ void __launch_bounds__(256) k_gbtrf_panel(BandView b, int64_t j0, int jb,
-                                                     double pivot_tol, LUStatus* st) {
+// Panel: columns j0 .. j0+jb-1 by one CTA per factorisation (blockIdx.y
+// selects the member of a batch; members shorter than j0 are done).
+__global__ void __launch_bounds__(256) k_gbtrf_panel(const BandView* __restrict__ bs, int64_t j0,
+                                                     double pivot_tol, LUStatus* const* sts) {
   __shared__ double s_mag[256], s_cmax[256];
   __shared__ int64_t s_idx[256];
   __shared__ int64_t s_p;
   __shared__ double s_piv;
+  const BandView b = bs[blockIdx.y];
+  LUStatus* st = sts[blockIdx.y];
+  if (j0 >= b.n) return;
+  const int jb = (int)lmin(kLUBlock, b.n - j0);
   if (st->code != 0) return;
   const int tid = threadIdx.x;
   // running maximum over every step so far (dgbtf2's ju): rows of this panel may
@@ -157,9 +162,14 @@ __global__ void __launch_bounds__(256) k_gbtrf_panel(BandView b, int64_t j0, int
 // Trailing columns j0+jb .. ju: per column, the panel's interchanges and
 // updates in pivot order. One warp per column; multipliers of the panel in
 // shared memory: s_l[c * (kl+1) + r] = l(j0+c+1+r, j0+c).
-__global__ void __launch_bounds__(512) k_gbtrf_update(BandView b, int64_t j0, int jb,
-                                                      const LUStatus* st) {
+__global__ void __launch_bounds__(512) k_gbtrf_update(const BandView* __restrict__ bs, int64_t j0,
+                                                      LUStatus* const* sts) {
   extern __shared__ double s_l[];
+  const BandView b = bs[blockIdx.y];
+  const LUStatus* st = sts[blockIdx.y];
+  if (j0 >= b.n) return;
+  const int jb = (int)lmin(kLUBlock, b.n - j0);
+  if (j0 + jb >= b.n) return;
   if (st->code != 0) return;
   const int64_t ju = st->ju;
   const int64_t kfirst = j0 + jb;
@@ -333,8 +343,8 @@ void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaSt
   CK_CUDA(cudaGetLastError());
 }
 
-void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_col,
-                  double* fail_pivot) {
+// Band bounds, storage, fill and status of one factorisation (lu.hpp:55-100).
+static void lu_prepare(ck_lu_s* f, ck_matrix_s* m) {
   if (m->nrows != m->ncols) fail(CK_ERR_DIMENSION, "lu_factorize: matrix must be square");
   f->device = m->device;
   // the factors outlive the matrix handle (LUFactors is a value in lu.hpp:42-47):
@@ -371,15 +381,43 @@ void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_co
   CK_CUDA(cudaGetLastError());
   const size_t usmem = sizeof(double) * kLUBlock * (size_t)(f->kl + 1);
   if (usmem > 227 * 1024) fail(CK_ERR_UNSUPPORTED, "band too wide for the on-chip panel update");
+  CK_CUDA(cudaStreamSynchronize(st));
+}
+
+// The right-looking panel loop (lu.hpp:100-177) of S prepared factorisations at
+// once: two launches per 32-column panel for the whole batch (one CTA per member
+// for the panel, a member row of CTAs for the trailing update), on stream st.
+static void lu_panels(ck_lu_s* const* fs, int S, double pivot_tol, cudaStream_t st) {
+  std::vector<BandView> hb((size_t)S);
+  std::vector<LUStatus*> hs((size_t)S);
+  int64_t nmax = 0, klmax = 0, colmax = 0;
+  for (int g = 0; g < S; ++g) {
+    hb[g] = fs[g]->view();
+    hs[g] = fs[g]->status.p;
+    nmax = std::max(nmax, fs[g]->n);
+    klmax = std::max(klmax, fs[g]->kl);
+    colmax = std::max(colmax, fs[g]->kl + fs[g]->ku + 1);
+  }
+  if (nmax == 0) return;
+  DBuf<BandView> db(S);
+  DBuf<LUStatus*> ds(S);
+  CK_CUDA(cudaMemcpyAsync(db.p, hb.data(), sizeof(BandView) * S, cudaMemcpyHostToDevice, st));
+  CK_CUDA(cudaMemcpyAsync(ds.p, hs.data(), sizeof(LUStatus*) * S, cudaMemcpyHostToDevice, st));
+  const size_t usmem = sizeof(double) * kLUBlock * (size_t)(klmax + 1);
   CK_CUDA(allow_max_dynamic_smem(k_gbtrf_update));
-  const int64_t maxcols = f->kl + f->ku + 1;
-  const unsigned ublocks = (unsigned)std::min<int64_t>(148, std::max<int64_t>(1, ceil_div(maxcols, 16)));
-  for (int64_t j0 = 0; j0 < n; j0 += kLUBlock) {
-    const int jb = (int)std::min<int64_t>(kLUBlock, n - j0);
-    k_gbtrf_panel<<<1, 256, 0, st>>>(b, j0, jb, pivot_tol, f->status.p);
-    if (j0 + jb < n) k_gbtrf_update<<<ublocks, 512, usmem, st>>>(b, j0, jb, f->status.p);
+  const unsigned ublocks = (unsigned)std::min<int64_t>(148, std::max<int64_t>(1, ceil_div(colmax, 16)));
+  for (int64_t j0 = 0; j0 < nmax; j0 += kLUBlock) {
+    k_gbtrf_panel<<<dim3(1, (unsigned)S), 256, 0, st>>>(db.p, j0, pivot_tol, ds.p);
+    if (j0 + kLUBlock < nmax) k_gbtrf_update<<<dim3(ublocks, (unsigned)S), 512, usmem, st>>>(db.p, j0, ds.p);
   }
   CK_CUDA(cudaGetLastError());
+  CK_CUDA(cudaStreamSynchronize(st));
+}
+
+// Status check (singular -> error) and the solve-side data of one factorisation.
+static void lu_finish(ck_lu_s* f, ck_matrix_s* m, int64_t* fail_col, double* fail_pivot) {
+  cudaStream_t st = f->stream;
+  const int64_t n = f->n;
   LUStatus s{};
   CK_CUDA(cudaMemcpyAsync(&s, f->status.p, sizeof(s), cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaStreamSynchronize(st));
@@ -408,11 +446,36 @@ void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_co
   f->bperm.alloc(std::max<int64_t>(1, nblk * (1 + 4 * kLUBlock)));
   f->work.alloc(2 * n + 3 * kNormParts + 16);
   f->rdiag.alloc(std::max<int64_t>(1, n));
-  b = f->view();
+  BandView b = f->view();
   if (n > 0) k_convert_l_blocks<<<(unsigned)nblk, 256, 0, st>>>(b);
   if (n > 0) k_pivot_reciprocals<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b);
   CK_CUDA(cudaGetLastError());
   CK_CUDA(cudaStreamSynchronize(st));
+}
+
+void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_col,
+                  double* fail_pivot) {
+  lu_prepare(f, m);
+  ck_lu_s* one[1] = {f};
+  lu_panels(one, 1, pivot_tol, f->stream);
+  lu_finish(f, m, fail_col, fail_pivot);
+}
+
+// Batch: every member prepared, one panel loop for all (the factorisation of a
+// member is launch- and latency-bound alone), then each finished. codes[g] is
+// CK_OK or the member's error status (its factors freed).
+void lu_factorize_batch(ck_lu_s* const* fs, ck_matrix_s* const* ms, int S, double pivot_tol,
+                        int32_t* codes, int64_t* fail_cols, double* fail_pivots) {
+  for (int g = 0; g < S; ++g) lu_prepare(fs[g], ms[g]);
+  lu_panels(fs, S, pivot_tol, fs[0]->stream);
+  for (int g = 0; g < S; ++g) {
+    codes[g] = CK_OK;
+    try {
+      lu_finish(fs[g], ms[g], fail_cols ? fail_cols + g : nullptr, fail_pivots ? fail_pivots + g : nullptr);
+    } catch (const Error& e) {
+      codes[g] = e.code;
+    }
+  }
 }
 
 }  // namespace ck
