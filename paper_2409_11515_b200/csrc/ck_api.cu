@@ -156,10 +156,13 @@ void random_unit_vector_host(void* engine, int64_t n, double* out) {
 // restarts; on large ones the R per-entry gathers bound an R-column sweep and
 // two columns per sweep is the measured optimum.
 // CK_RESTART_GROUP overrides (A/B switch).
-static int restart_group(const ck_matrix_s* m) {
+static int restart_group(const ck_matrix_s* m, uint64_t restarts) {
   const char* e = std::getenv("CK_RESTART_GROUP");
   if (e && e[0] >= '1' && e[0] <= '4') return e[0] - '0';
-  return m->nnz >= (int64_t(1) << 24) ? 2 : kMaxCols;
+  if (m->nnz < (int64_t(1) << 24)) return kMaxCols;
+  // large operators (config 4, per step): R = 1 2.24, 2 4.07, 3 6.19, 4 10.45 ms ->
+  // three restarts in one sweep, otherwise pairs
+  return restarts == 3 ? 3 : 2;
 }
 
 static void check_cfg(const ck_adam_cfg* cfg) {
@@ -495,7 +498,7 @@ ck_status ck_estimate_norm(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restart
     if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
     M(a);
     bool have = false;
-    const int group = restart_group(a);
+    const int group = restart_group(a, restarts);
     for (uint64_t r0 = 0; r0 < restarts; r0 += group) {
       int R = (int)std::min<uint64_t>(group, restarts - r0);
       std::vector<uint64_t> seeds(R);
@@ -717,7 +720,7 @@ ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, doubl
     check_cfg(cfg);
     ck_matrix_s* m = M(a);
     if (m->nrows != m->ncols) fail(CK_ERR_DIMENSION, "cond2: matrix must be square");
-    estimate_norm_groups(cfg, restarts, fwd, nullptr, restart_group(m), [&](ck_session_s* s, const uint64_t* seeds, int R) {
+    estimate_norm_groups(cfg, restarts, fwd, nullptr, restart_group(m, restarts), [&](ck_session_s* s, const uint64_t* seeds, int R) {
       session_create(s, m, cfg, seeds, R);
     });
     *inv = ck_norm_result{};
@@ -828,7 +831,7 @@ ck_status ck_estimate_norm_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg
     if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
     ck_matrix_s* m = M(a);
     std::vector<char> have((size_t)nseg, 0);
-    const int group = restart_group(m);
+    const int group = restart_group(m, restarts);
     for (uint64_t r0 = 0; r0 < restarts; r0 += group) {
       const int R = (int)std::min<uint64_t>(group, restarts - r0);
       std::vector<uint64_t> seeds((size_t)nseg * R);
