@@ -274,7 +274,7 @@ def run_partition(args, rank, world, local, dist, barrier, allmax):
             "config": {"workload": name, "n": n, "nnz": nnz, "path": "sigma_max",
                        "adam": "alpha=1e-2,beta1=.9,beta2=.999,eps=1e-8",
                        "parallelism": f"row-block partition over {world} ranks "
-                                      "(halo exchange + allgathered partials, NCCL)",
+                                      "(one NCCL group per half step: partials + halo)",
                        "rank0_halo": halo,
                        "l2": "inputs larger than L2 per rank; no flush needed"},
             "roofline": roofline,
@@ -282,7 +282,9 @@ def run_partition(args, rank, world, local, dist, barrier, allmax):
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": None,
-            "gpu_launches": args.steps * (6 + 4),
+            # per iteration: k_apply, k_transpose, two control steps, two halo packs,
+            # two halo unpacks (the NCCL kernels are the library's)
+            "gpu_launches": args.steps * 8,
             "setup_s": {"generate": t_gen, "partition": t_part, "upload_and_build": t_up},
         }
         print(json.dumps(line), flush=True)
