@@ -30,6 +30,8 @@
 // :199-219) at chunk boundaries.
 #include <cmath>
 #include <cstring>
+#include <exception>
+#include <memory>
 #include <random>
 #include <thread>
 #include <vector>
@@ -686,16 +688,18 @@ void load_start(ck_session_s* s, int g, int c, int b, const double* x) {
 // Next start vector of column k (member g) into `out` (the member's
 // original-order vector): random_unit_vector from the column's own stream; a
 // partition rank draws the global vector and keeps its extended slice.
-static void draw_start(ck_session_s* s, int k, int g, double* out) {
+static void draw_start(ck_session_s* s, int k, int g, double* out,
+                       const std::function<double*()>& dst = {}) {
   if (!s->dist) {
-    random_unit_vector_host(&s->gens[k], s->seg_n[g], out);
+    random_unit_vector_host(&s->gens[k], s->seg_n[g], out, dst);
     return;
   }
   const DistPart& d = *s->dist;
   std::vector<double> full((size_t)d.n_global);
   random_unit_vector_host(&s->gens[k], d.n_global, full.data());
+  double* to = dst ? dst() : out;
   for (size_t e = 0; e < d.ext_global.size(); ++e)
-    out[e] = d.ext_global[e] >= 0 ? full[(size_t)d.ext_global[e]] : 0.0;
+    to[e] = d.ext_global[e] >= 0 ? full[(size_t)d.ext_global[e]] : 0.0;
 }
 
 void service_restarts(ck_session_s* s) {
@@ -753,16 +757,41 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
   CK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->h_hdr), sizeof(Header) * S));
   int64_t nmax = 0;
   for (int g = 0; g < S; ++g) nmax = std::max(nmax, s->seg_n[g]);
-  s->hx.resize(nmax);
+  // The n-sized pinned staging buffer (start vectors, restarts, witness D2H)
+  // takes ~0.1 s to pin at config-4 size: it is allocated on a helper thread
+  // while the first start vector is drawn into pageable scratch (uninitialised,
+  // so the RNG's worker threads fault its pages in parallel); the normalisation
+  // pass then writes into the pinned buffer, which uploads at full rate.
+  std::exception_ptr pin_err;
+  std::thread pin([s, nmax, &pin_err] {
+    try {
+      CK_CUDA(cudaSetDevice(s->device));
+      s->hx.resize(nmax);
+    } catch (...) {
+      pin_err = std::current_exception();
+    }
+  });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } pin_join{pin};
+  auto pinned = [&]() -> double* {
+    if (pin.joinable()) pin.join();
+    if (pin_err) std::rethrow_exception(pin_err);
+    return s->hx.data();
+  };
+  std::unique_ptr<double[]> scratch(new double[(size_t)std::max<int64_t>(nmax, 1)]);
   s->gens.clear();
   s->gens.reserve((size_t)S * R);
   for (int g = 0; g < S; ++g) {
     for (int c = 0; c < R; ++c) {
       s->gens.emplace_back(seeds[g * R + c]);
       if (g == 0 && c == 0) tr.mark("buffers", st);
-      draw_start(s, g * R + c, g, s->hx.data());  // x0, rng.hpp:68-77
+      draw_start(s, g * R + c, g, scratch.get(), pinned);  // x0, rng.hpp:68-77
       if (g == 0 && c == 0) tr.mark("x0 host RNG", st);
-      load_start(s, g, c, 0, s->hx.data());
+      load_start(s, g, c, 0, pinned());
       CK_CUDA(cudaStreamSynchronize(st));  // hx is reused for the next upload
       if (g == 0 && c == 0) tr.mark("x0 upload", st);
       ColState cs{};
@@ -782,6 +811,7 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
     h.ndone = cfg->max_iter == 0 ? R : 0;
     s->h_hdr[g] = h;
   }
+  pinned();
   tr.mark("remaining columns", st);
   push_state(s);
   // chunk length: about 4 ms of device work per host round trip, 4..256 steps

@@ -4,8 +4,11 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
+#include <memory>
 #include <random>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -86,14 +89,88 @@ static void parallel_for(int64_t n, F&& f) {
   for (auto& th : pool) th.join();
 }
 
+// std::mt19937_64 (the reference's engine, rng.hpp:23-33) in bulk. The state
+// leaves the engine through its standard text form, words are produced 312 at
+// a time by a branch-free twist and a temper loop the compiler vectorises, and
+// the state goes back, so the engine continues exactly as if it had been
+// called `count` times. A one-time self-check against the engine's own
+// operator() gates it (any mismatch -> per-call draws).
+struct Mt64Bulk {
+  static constexpr int N = 312, M = 156;
+  static constexpr uint64_t kA = 0xB5026F5AA96619E9ull, kUp = ~uint64_t(0) << 31,
+                            kLo = ~kUp;
+  uint64_t x[N];
+  uint64_t p = N;
+  bool ok = false;
+
+  explicit Mt64Bulk(const std::mt19937_64& g) {
+    std::stringstream ss;
+    ss << g;
+    for (auto& w : x) ss >> w;
+    ss >> p;
+    ok = !ss.fail() && p <= (uint64_t)N;
+  }
+  void store(std::mt19937_64& g) const {
+    std::stringstream ss;
+    for (auto w : x) ss << w << ' ';
+    ss << p;
+    ss >> g;
+  }
+  static uint64_t mix(uint64_t a, uint64_t b, uint64_t c) {
+    const uint64_t y = (a & kUp) | (b & kLo);
+    return c ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+  }
+  void twist() {
+    for (int i = 0; i < N - M; ++i) x[i] = mix(x[i], x[i + 1], x[i + M]);
+    for (int i = N - M; i < N - 1; ++i) x[i] = mix(x[i], x[i + 1], x[i + M - N]);
+    x[N - 1] = mix(x[N - 1], x[0], x[M - 1]);
+    p = 0;
+  }
+  static uint64_t temper(uint64_t z) {
+    z ^= (z >> 29) & 0x5555555555555555ull;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+    z ^= (z << 37) & 0xFFF7EEE000000000ull;
+    return z ^ (z >> 43);
+  }
+  // the next `count` state words, untempered (temper() of each is the output)
+  void fill_raw(uint64_t* __restrict out, int64_t count) {
+    while (count > 0) {
+      if (p == (uint64_t)N) twist();
+      const int64_t k = std::min<int64_t>(N - (int64_t)p, count);
+      std::memcpy(out, x + p, sizeof(uint64_t) * (size_t)k);
+      p += (uint64_t)k;
+      out += k;
+      count -= k;
+    }
+  }
+  static bool verified() {
+    static const bool v = [] {
+      std::mt19937_64 g(12345), h(12345);
+      for (int i = 0; i < 100; ++i) g();
+      for (int i = 0; i < 100; ++i) h();
+      Mt64Bulk b(g);
+      if (!b.ok) return false;
+      std::vector<uint64_t> w(1000);
+      b.fill_raw(w.data(), 1000);
+      b.store(g);
+      for (auto v : w)
+        if (temper(v) != h()) return false;
+      return g() == h() && g == h;
+    }();
+    return v;
+  }
+};
+
 // random_unit_vector (rng.hpp:68-77) with standard_normal (rng.hpp:61-65) and
 // uniform01 (rng.hpp:31-33). The engine draws stay sequential (they define the
 // stream) and run on the calling thread block by block, while a helper thread
 // applies the Box-Muller transform of the previous block on all host threads
 // (pipelined; no n-sized draw buffer). The norm is the reference's two_norm:
 // amax (exact in any order, folded into the transform), then the sequential
-// scaled sum of squares.
-void random_unit_vector_host(void* engine, int64_t n, double* out) {
+// scaled sum of squares. With `dst`, the normalised vector goes to dst()
+// (called once the norm is known) and `out` is scratch.
+void random_unit_vector_host(void* engine, int64_t n, double* out,
+                             const std::function<double*()>& dst) {
   if (n <= 0) return;
   auto& g = *static_cast<std::mt19937_64*>(engine);
   constexpr int64_t kBlock = int64_t(1) << 18;  // pairs per pipeline block
@@ -102,6 +179,13 @@ void random_unit_vector_host(void* engine, int64_t n, double* out) {
   buf[1].resize(buf[0].size());
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int64_t nthr = std::min<int64_t>(hw, 64);
+  // bulk draws from 2^15 words on (text state round trip ~0.1 ms)
+  std::unique_ptr<Mt64Bulk> bulk;
+  if (n >= (int64_t(1) << 14) && Mt64Bulk::verified()) {
+    bulk.reset(new Mt64Bulk(g));
+    if (!bulk->ok) bulk.reset();
+  }
+  const bool raw = bulk != nullptr;
   double nrm = 0.0;
   while (nrm == 0.0) {
     std::vector<double> amax((size_t)nthr, 0.0);
@@ -109,7 +193,11 @@ void random_unit_vector_host(void* engine, int64_t n, double* out) {
     for (int64_t b0 = 0; b0 < n; b0 += kBlock) {
       const int64_t len = std::min(kBlock, n - b0);
       std::vector<uint64_t>& d = buf[(b0 / kBlock) & 1];
-      for (int64_t k = 0; k < 2 * len; ++k) d[(size_t)k] = g();
+      if (bulk) {
+        bulk->fill_raw(d.data(), 2 * len);  // tempered by the transform threads
+      } else {
+        for (int64_t k = 0; k < 2 * len; ++k) d[(size_t)k] = g();
+      }
       if (worker.joinable()) worker.join();
       worker = std::thread([&, b0, len, dp = d.data()] {
         const int64_t chunk = ceil_div(len, nthr);
@@ -117,11 +205,16 @@ void random_unit_vector_host(void* engine, int64_t n, double* out) {
         for (int64_t t = 0; t < nthr; ++t) {
           const int64_t lo = t * chunk, hi = std::min(len, lo + chunk);
           if (lo >= hi) break;
-          pool.emplace_back([&amax, dp, out, b0, lo, hi, t] {
+          pool.emplace_back([&amax, dp, out, b0, lo, hi, t, raw] {
             double m = amax[(size_t)t];
             for (int64_t i = lo; i < hi; ++i) {
-              const double u1 = 1.0 - static_cast<double>(dp[2 * i] >> 11) * 0x1.0p-53;
-              const double u2 = static_cast<double>(dp[2 * i + 1] >> 11) * 0x1.0p-53;
+              uint64_t w1 = dp[2 * i], w2 = dp[2 * i + 1];
+              if (raw) {
+                w1 = Mt64Bulk::temper(w1);
+                w2 = Mt64Bulk::temper(w2);
+              }
+              const double u1 = 1.0 - static_cast<double>(w1 >> 11) * 0x1.0p-53;
+              const double u2 = static_cast<double>(w2 >> 11) * 0x1.0p-53;
               const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
               out[b0 + i] = z;
               m = std::max(m, std::abs(z));
@@ -146,8 +239,10 @@ void random_unit_vector_host(void* engine, int64_t n, double* out) {
       nrm = am * std::sqrt(sq);
     }
   }
+  if (bulk) bulk->store(g);
+  double* to = dst ? dst() : out;  // may wait for the destination to exist
   parallel_for(n, [&](int64_t b, int64_t e) {
-    for (int64_t i = b; i < e; ++i) out[i] /= nrm;
+    for (int64_t i = b; i < e; ++i) to[i] = out[i] / nrm;
   });
 }
 

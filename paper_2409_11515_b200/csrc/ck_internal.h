@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 
 #include "ck_common.h"
 
@@ -39,6 +40,7 @@ void vector_divide(int64_t n, const double* h_y, const double* h_d, double* h_ou
 // Host mirror of random_unit_vector (rng.hpp:68-77) on a caller-owned engine
 // state; bit-identical to the reference, Box-Muller transform multithreaded.
 struct Mt64;
-void random_unit_vector_host(void* engine /* std::mt19937_64* */, int64_t n, double* out);
+void random_unit_vector_host(void* engine /* std::mt19937_64* */, int64_t n, double* out,
+                             const std::function<double*()>& dst = {});
 
 }  // namespace ck
