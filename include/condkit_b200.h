@@ -98,6 +98,14 @@ ck_status ck_set_device(int32_t device);
 ck_status ck_device_synchronize(void);
 ck_status ck_host_register(void* ptr, uint64_t bytes);
 ck_status ck_host_unregister(void* ptr);
+/* Start drawing random_unit_vector(n) from mt19937_64(seed) (rng.hpp:68-77) on a
+ * host thread, so that the draw overlaps the matrix upload that precedes a
+ * session. The next ck_session_create whose first column has this seed and
+ * dimension takes the vector and the engine state (bit-identical to drawing it
+ * there); anything else ignores it. One slot per process; a new call replaces
+ * (and first joins) the previous one. No reference counterpart: the reference
+ * draws inside projected_adam (condest.hpp:191). */
+ck_status ck_start_vector_prefetch(uint64_t seed, int64_t n);
 void ck_adam_default(ck_adam_cfg* cfg);
 
 /* --------------------------------------------------- rng.hpp mirror (host) */

@@ -124,10 +124,15 @@ class Session:
             raise InvalidArgument("projected_adam: zero-dimensional operator")
         self.oracle = oracle
         self.n = oracle.dimension()
-        handle = _device_handle(oracle)
         lib = _lib.load()
-        self._cfg = _lib.cfg_struct(cfg)
         seeds = np.ascontiguousarray([int(s) & 0xFFFFFFFFFFFFFFFF for s in seeds], np.uint64)
+        if (isinstance(oracle, ExplicitOracle) and oracle.a._dev is None and seeds.size
+                and self.n >= (1 << 20)):
+            # draw the first start vector on a host thread while A uploads
+            _lib.check(lib.ck_start_vector_prefetch(int(seeds[0]), self.n),
+                       "ck_start_vector_prefetch")
+        handle = _device_handle(oracle)
+        self._cfg = _lib.cfg_struct(cfg)
         self.ncols = seeds.size
         h = C.c_void_p()
         _lib.check(lib.ck_session_create(handle, C.byref(self._cfg),

@@ -762,6 +762,11 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
   // while the first start vector is drawn into pageable scratch (uninitialised,
   // so the RNG's worker threads fault its pages in parallel); the normalisation
   // pass then writes into the pinned buffer, which uploads at full rate.
+  // The first start vector, when ck_start_vector_prefetch drew it during the
+  // matrix upload: hx adopts its pinned buffer (then the resize below is a no-op).
+  std::mt19937_64 g0;
+  const bool x0_ready = !s->dist && S == 1 && s->seg_n[0] == nmax &&
+                        take_start_prefetch(seeds[0], nmax, &g0, &s->hx);
   std::exception_ptr pin_err;
   std::thread pin([s, nmax, &pin_err] {
     try {
@@ -789,7 +794,10 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
     for (int c = 0; c < R; ++c) {
       s->gens.emplace_back(seeds[g * R + c]);
       if (g == 0 && c == 0) tr.mark("buffers", st);
-      draw_start(s, g * R + c, g, scratch.get(), pinned);  // x0, rng.hpp:68-77
+      if (g == 0 && c == 0 && x0_ready)
+        s->gens.back() = g0;  // drawn during the matrix upload, already in hx
+      else
+        draw_start(s, g * R + c, g, scratch.get(), pinned);  // x0, rng.hpp:68-77
       if (g == 0 && c == 0) tr.mark("x0 host RNG", st);
       load_start(s, g, c, 0, pinned());
       CK_CUDA(cudaStreamSynchronize(st));  // hx is reused for the next upload

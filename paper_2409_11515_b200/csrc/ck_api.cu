@@ -7,6 +7,7 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <sstream>
 #include <string>
@@ -245,6 +246,89 @@ void random_unit_vector_host(void* engine, int64_t n, double* out,
     for (int64_t i = b; i < e; ++i) to[i] = out[i] / nrm;
   });
 }
+
+// ck_start_vector_prefetch's slot: one start vector drawn on a helper thread
+// into pageable scratch, normalised into a pinned buffer that is pinned
+// meanwhile on a second helper (the session adopts that buffer as its staging).
+namespace {
+struct StartPrefetch {
+  uint64_t seed = 0;
+  int64_t n = 0;
+  int device = 0;
+  std::mt19937_64 g;
+  PinnedBuf<double> pin;
+  std::exception_ptr err;
+  std::thread th;
+  ~StartPrefetch() {
+    if (th.joinable()) th.join();
+  }
+};
+std::mutex g_pf_mu;
+std::unique_ptr<StartPrefetch> g_pf;
+}  // namespace
+
+bool take_start_prefetch(uint64_t seed, int64_t n, void* engine, PinnedBuf<double>* hx) {
+  std::unique_ptr<StartPrefetch> pf;
+  {
+    std::lock_guard<std::mutex> lk(g_pf_mu);
+    if (!g_pf || g_pf->seed != seed || g_pf->n != n) return false;
+    pf = std::move(g_pf);
+  }
+  if (pf->th.joinable()) pf->th.join();
+  if (pf->err || pf->pin.p == nullptr) return false;  // draw it again on the caller's thread
+  *static_cast<std::mt19937_64*>(engine) = pf->g;
+  std::swap(hx->p, pf->pin.p);
+  std::swap(hx->n, pf->pin.n);
+  return true;
+}
+
+}  // namespace ck
+
+extern "C" ck_status ck_start_vector_prefetch(uint64_t seed, int64_t n) {
+  using namespace ck;
+  return guarded([&] {
+    if (n <= 0) fail(CK_ERR_INVALID_ARGUMENT, "ck_start_vector_prefetch: n must be positive");
+    std::unique_ptr<StartPrefetch> old;
+    auto pf = std::make_unique<StartPrefetch>();
+    pf->seed = seed;
+    pf->n = n;
+    pf->g.seed(seed);
+    CK_CUDA(cudaGetDevice(&pf->device));
+    StartPrefetch* p = pf.get();
+    pf->th = std::thread([p] {
+      try {
+        std::exception_ptr pin_err;
+        std::thread pin([p, &pin_err] {
+          try {
+            CK_CUDA(cudaSetDevice(p->device));
+            p->pin.resize(p->n);
+          } catch (...) {
+            pin_err = std::current_exception();
+          }
+        });
+        std::unique_ptr<double[]> scratch(new double[(size_t)p->n]);
+        try {
+          random_unit_vector_host(&p->g, p->n, scratch.get(), [&]() -> double* {
+            if (pin.joinable()) pin.join();
+            if (pin_err) std::rethrow_exception(pin_err);
+            return p->pin.data();
+          });
+        } catch (...) {
+          if (pin.joinable()) pin.join();
+          throw;
+        }
+        if (pin.joinable()) pin.join();
+      } catch (...) {
+        p->err = std::current_exception();
+      }
+    });
+    std::lock_guard<std::mutex> lk(g_pf_mu);
+    old = std::move(g_pf);
+    g_pf = std::move(pf);
+  });
+}
+
+namespace ck {
 
 // Restart columns per explicit-operator sweep (estimate_norm, cond2, batches).
 // Small operators are launch/latency bound and share one sweep among up to 4

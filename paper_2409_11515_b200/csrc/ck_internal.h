@@ -43,4 +43,10 @@ struct Mt64;
 void random_unit_vector_host(void* engine /* std::mt19937_64* */, int64_t n, double* out,
                              const std::function<double*()>& dst = {});
 
+// The prefetched start vector for (seed, n), if ck_start_vector_prefetch made
+// one: *hx adopts the pinned buffer holding the normalised vector, *engine
+// takes the engine state after the draw. False (nothing touched) otherwise.
+bool take_start_prefetch(uint64_t seed, int64_t n, void* engine /* std::mt19937_64* */,
+                         PinnedBuf<double>* hx);
+
 }  // namespace ck

@@ -14,7 +14,10 @@ a2 = ck.SparseMatrix(a.nrows, a.ncols, a.row_offsets, a.col_indices, a.values, v
 for arr in (a2.row_offsets, a2.col_indices, a2.values):
     _lib.load().ck_host_register(arr.ctypes.data, arr.nbytes)
 cfg = configs.baseline_adam(1, max_iter=iters)
+prefetch = len(sys.argv) > 3 and sys.argv[3] == "prefetch"  # norm2's order: x0 drawn during the upload
 t0 = time.perf_counter()
+if prefetch:
+    _lib.check(_lib.load().ck_start_vector_prefetch(cfg.seed, a2.ncols), "prefetch")
 dev = a2.device()
 t1 = time.perf_counter()
 s = ck.Session(ck.ExplicitOracle(a2), cfg, [cfg.seed])

@@ -179,3 +179,25 @@ def test_restart_grouping_is_invisible(port, monkeypatch):
         e = ck.estimate_norm(ck.ExplicitOracle(a), c, 4)
         assert e.value == ref.value and e.iterations == ref.iterations
         assert np.array_equal(e.witness, ref.witness)
+
+
+def test_start_vector_prefetch_is_invisible():
+    # ck_start_vector_prefetch (the first start vector drawn during the upload)
+    # must give the same run bit for bit as drawing it inside the session; a
+    # prefetch for another seed is ignored.
+    from paper_2409_11515_b200 import _lib
+    lap = M.laplacian2d(1024)  # n = 2^20: Session prefetches while A uploads
+    c = M.cfg(alpha=1e-2, max_iter=40, patience=40, seed=9)
+
+    def fresh():
+        return ck.SparseMatrix(lap.nrows, lap.ncols, lap.row_offsets, lap.col_indices, lap.values)
+
+    e1 = ck.norm2(fresh(), c)  # prefetched
+    a2 = fresh()
+    a2.device()
+    e2 = ck.norm2(a2, c)  # drawn in the session
+    _lib.check(_lib.load().ck_start_vector_prefetch(10, lap.ncols), "prefetch")
+    e3 = ck.norm2(a2, c)  # stale slot (seed 10): ignored
+    for e in (e2, e3):
+        assert e.value == e1.value and e.iterations == e1.iterations
+        assert np.array_equal(e.witness, e1.witness)
