@@ -129,21 +129,45 @@ def bytes_per_iteration(nnz: int, n: int, R: int = 1, col_format: int = 0):
     return ea * nnz + 24 * n * R, et * nnz + 72 * n * R
 
 
-def cpu_reference(a, steps_hint: int, threads: int, iters: int):
-    import pyoracle  # noqa: PLC0415  (bench CPU arm only)
-    from paper_2409_11515_b200 import configs  # noqa: PLC0415
-    which = "ref" if pyoracle.available("ref") else "port"
+# Reference-arm copy of configs.CONFIGS (kind, grid, param, name): the reference arm
+# must not import the product package, so its workload table lives here.
+REF_WORKLOADS = {
+    1: (1, 64, 0, "laplacian64_rowscaled"),
+    2: (2, 256, 0, "stokes256"),
+    3: (3, 512, 0, "hydromech512"),
+    4: (3, 2048, 0, "hydromech2048"),
+}
+
+
+def cpu_reference(a, threads: int, iters: int, which: str | None = None):
+    """The reference's projected_adam (oracle/_ref: the unmodified condkit headers) on
+    `threads` host threads, `iters` iterations each; the rate of each run is taken
+    between its first and last iteration (the first iteration, with the x0 draw and the
+    matrix conversion, is untimed)."""
+    import pyoracle  # noqa: PLC0415  (bench CPU arms only)
+    which = which or pyoracle.best_reference()
     o = pyoracle.Oracle(which)
-    cfg = configs.baseline_adam(1, max_iter=iters)
-    if which == "ref":
+    cfg = _RefCfg(iters)
+    host = {"nproc": os.cpu_count(), "cpu_model": pyoracle.cpu_model(),
+            "build": pyoracle.BUILD_FLAGS[which]}
+    if which != "port":
         rate, timed, span = o.time_iterations(a, cfg, threads, iters)
         return dict(value=rate, cores=threads, kind="reference", timed_iterations=timed,
-                    span_s=span)
+                    span_s=span, **host)
     t0 = time.perf_counter()
     e = o.projected_adam_explicit(a, cfg)
     dt = time.perf_counter() - t0
     return dict(value=e.iterations / dt, cores=1, kind="port", timed_iterations=e.iterations,
-                span_s=dt)
+                span_s=dt, **host)
+
+
+class _RefCfg:
+    """AdamConfig fields (condest.hpp:39-48) of the BASELINE runs, without importing the
+    product package."""
+
+    def __init__(self, iters: int, seed: int = 1):
+        self.alpha, self.beta1, self.beta2, self.eps_stab = 1e-2, 0.9, 0.999, 1e-8
+        self.max_iter, self.seed, self.rel_tol, self.patience = iters, seed, 1e-12, iters
 
 
 def host_threads_budget(a) -> int:
@@ -160,29 +184,66 @@ def host_threads_budget(a) -> int:
     return max(1, min(ncpu, fit, 64))
 
 
+def loaded_libraries() -> list[str]:
+    """Shared objects mapped into this process (for the reference arm's cleanliness check)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                parts = line.split()
+                if len(parts) >= 6 and (parts[-1].endswith(".so") or ".so." in parts[-1]):
+                    libs.add(parts[-1])
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference_arm(args):
+    """The reference's CPU projected_adam on the same workload, metric and unit as our arm.
+    A step is one Projected-Adam iteration over the whole matrix; T host threads run
+    independent runs, each 1 + ceil(K / T) iterations with the first untimed,
+    so at least K iterations are timed. The workload comes from oracle/_build/libcondkit_gen.so
+    -- the product library is never loaded in this process (asserted)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    a, name = make_workload(args.config, args.grid)
+    import pyoracle  # noqa: PLC0415
+    kind, grid, param, name = REF_WORKLOADS[args.config]
+    if args.grid is not None:
+        grid, name = args.grid, f"{name}@grid{args.grid}"
+    t0 = time.perf_counter()
+    a = pyoracle.generate(kind, grid, 1, param)
+    t_gen = time.perf_counter() - t0
     threads = args.cpu_threads or host_threads_budget(a)
-    iters = args.cpu_iters
-    res = cpu_reference(a, args.steps, threads, iters)
+    threads = max(1, min(threads, args.steps))
+    per_thread = 1 + -(-args.steps // threads)
+    res = cpu_reference(a, threads, per_thread)
+    timed = int(res["timed_iterations"])
+    product = [p for p in loaded_libraries() if "libcondkit_b200" in p]
+    if product:
+        raise SystemExit(f"reference arm loaded the product library: {product}")
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * res["cores"] / res["value"] if res["value"] else None,
+        "steps": timed, "warmup": threads,
+        "ms_per_step": 1000.0 / res["value"] if res["value"] else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, DESIGN.md section 3)", "impl": "reference",
         "config": {"workload": name, "n": a.nrows, "nnz": a.nnz, "path": "sigma_max",
                    "adam": "alpha=1e-2,beta1=.9,beta2=.999,eps=1e-8"},
         "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["cores"],
-                         "kind": res["kind"],
-                         "sample": f"{res['cores']} concurrent reference runs x {iters} "
-                                   f"iterations each; steady-state rate between first and last "
-                                   f"iteration ({res['timed_iterations']} iterations timed)"},
+                         "kind": res["kind"], "nproc": res["nproc"],
+                         "cpu_model": res["cpu_model"], "build": res["build"],
+                         "sample": f"{res['cores']} concurrent reference projected_adam runs x "
+                                   f"{per_thread} iterations on {name} (first iteration of each "
+                                   f"run untimed: {threads} warm-up iterations); summed "
+                                   f"steady-state rate over {timed} timed iterations, "
+                                   f"{res['span_s']:.1f} s"},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "native_libraries": [p for p in loaded_libraries()
+                             if "condkit" in os.path.basename(p)],
+        "setup_s": {"generate": t_gen},
+        "requested_steps": args.steps,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -443,8 +504,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not ensemble:
         threads = args.cpu_threads or host_threads_budget(a)
-        r = cpu_reference(a, args.steps, threads, args.cpu_iters)
+        r = cpu_reference(a, threads, args.cpu_iters)
         cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+               "nproc": r["nproc"], "cpu_model": r["cpu_model"], "build": r["build"],
                "sample": f"{r['cores']} concurrent reference projected_adam runs x "
                          f"{args.cpu_iters} iterations on {name}; steady-state rate "
                          f"({r['timed_iterations']} iterations timed)"}

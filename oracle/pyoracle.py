@@ -25,8 +25,88 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PATHS = {
     "port": os.path.join(HERE, "_build", "libcondkit_oracle.so"),
     "ref": os.path.join(HERE, "_ref", "libcondkit_ref.so"),
+    # the same reference driver at -O3, for bench.py's CPU arms
+    "ref_v3": os.path.join(HERE, "_ref", "libcondkit_ref_v3.so"),
+    "ref_native": os.path.join(HERE, "_ref", "libcondkit_ref_native.so"),
 }
-PREFIX = {"port": "cko_", "ref": "ckref_"}
+PREFIX = {"port": "cko_", "ref": "ckref_", "ref_v3": "ckref_", "ref_native": "ckref_"}
+BUILD_FLAGS = {
+    "port": "gcc -O2 -ffp-contract=off (C restatement)",
+    "ref": "g++ -O2 -ffp-contract=off -std=c++20",
+    "ref_v3": "g++ -O3 -march=x86-64-v3 -ffp-contract=off -std=c++20",
+    "ref_native": "g++ -O3 -march=native (Sapphire Rapids build host) -ffp-contract=off -std=c++20",
+}
+GEN_PATH = os.path.join(HERE, "_build", "libcondkit_gen.so")
+
+
+def _cpu_flags() -> set:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def best_reference() -> str:
+    """The fastest reference build this host can execute: the -march=native build only
+    where every ISA extension of its build host is present, else -O3 x86-64-v3, else -O2."""
+    flags = _cpu_flags()
+    isa = os.path.join(HERE, "_ref", "native_isa.txt")
+    if available("ref_native") and os.path.exists(isa):
+        with open(isa) as f:
+            need = {w.strip() for w in f if w.strip()}
+        if need and need <= flags:
+            return "ref_native"
+    if available("ref_v3") and {"avx2", "fma", "bmi2"} <= flags:
+        return "ref_v3"
+    return "ref" if available("ref") else "port"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+@dataclass
+class CSR:
+    nrows: int
+    ncols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_offsets[-1])
+
+
+def generate(kind: int, grid: int, seed: int = 1, param: int = 0) -> CSR:
+    """The BASELINE synthetic operators from _build/libcondkit_gen.so,
+    a g++ build of the product's host generator source: bench.py's reference arm builds its
+    workload with this instead of loading libcondkit_b200.so."""
+    lib = C.CDLL(GEN_PATH)
+    f = lib.ck_generate
+    f.argtypes = [C.c_int32, C.c_int64, C.c_int64, C.c_uint64, _i64p, _i64p, _i64p, _i32p, _dp]
+    f.restype = C.c_int
+    n, nnz = C.c_int64(), C.c_int64()
+    if f(kind, grid, param, seed, C.byref(n), C.byref(nnz), None, None, None):
+        raise OracleError(2, "ck_generate(size)")
+    rp = np.empty(n.value + 1, np.int64)
+    ci = np.empty(max(nnz.value, 1), np.int32)
+    va = np.empty(max(nnz.value, 1), np.float64)
+    if f(kind, grid, param, seed, C.byref(n), C.byref(nnz), rp.ctypes.data_as(_i64p),
+         ci.ctypes.data_as(_i32p), va.ctypes.data_as(_dp)):
+        raise OracleError(2, "ck_generate")
+    return CSR(n.value, n.value, rp, ci[: nnz.value], va[: nnz.value])
 
 _dp = C.POINTER(C.c_double)
 _i64p = C.POINTER(C.c_int64)

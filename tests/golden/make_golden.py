@@ -151,8 +151,65 @@ def c2_cond2(ref):
                        "seconds": time.time() - t0})
 
 
+def c2_verify(ref):
+    """verify_solution (error_bounds.hpp:166-217) on config 2 at full size: x* ~ U[-1,1)
+    (seed 17), b = A x*, x^ = x* + 1e-6 ||x*|| u (u = random_unit_vector, seed 19), kappa
+    estimated inside by cond2 with one restart per norm (the c2_cond2 run)."""
+    a = configs.config(2)
+    cfg = configs.baseline_adam(1)
+    xs = ref.uniform_in(17, a.ncols, -1.0, 1.0)
+    b = ref.matvec(a, xs)
+    u = ref.random_unit_vectors(19, a.ncols)[0]
+    xh = xs + 1e-6 * ref.two_norm(xs) * u
+    t0 = time.time()
+    rep = ref.verify_solution(a, xh, b, adam=cfg, restarts=1)
+    _save("c2_verify", {"c2_verify_r1": rep, "inputs": {"x_seed": 17, "u_seed": 19,
+                                                       "rel_delta": 1e-6},
+                        "seconds": time.time() - t0})
+
+
+def _c5_member_sigma_max(idx):
+    ref = pyoracle.Oracle("ref")
+    m = configs.ensemble_member(idx, 1)
+    t0 = time.time()
+    e = ref.estimate_norm_explicit(m, configs.baseline_adam(ref.mix_seed(1, 0x1000 + idx)), 4)
+    return idx, _est(e), time.time() - t0
+
+
+def c5_sigma_max(ref):
+    """estimate_norm(ExplicitOracle, 4 restarts) of the first 8 full-size config-5 members
+    (n = 100k); estimator seed mix_seed(1, 0x1000 + idx) (batch.member_seeds)."""
+    from multiprocessing import Pool
+    with Pool(4) as pool:
+        res = pool.map(_c5_member_sigma_max, range(8))
+    _save("c5_sigma_max", {f"c5_member{i}_estimate_norm_r4": {**e, "seconds": s}
+                           for i, e, s in res})
+
+
+def _c5_cond2(scaled):
+    m = configs.ensemble_member(0, 1)
+    if scaled:
+        m = column_scaled(m)
+    ref = pyoracle.Oracle("ref")
+    cfg = configs.baseline_adam(ref.mix_seed(1, 0x1000))
+    t0 = time.time()
+    c = ref.cond2(m, cfg, 4, 1e-14)
+    return {"kappa": c["kappa"], "operator_norm": _est(c["operator_norm"]),
+            "inverse_norm": _est(c["inverse_norm"]), "seconds": time.time() - t0}
+
+
+def c5_cond2(ref):
+    """cond2 (4 restarts per norm) of full-size config-5 member 0, as generated and
+    column-scaled (run_bench's per-matrix cond2, bench.hpp:430-442)."""
+    from multiprocessing import Pool
+    with Pool(2) as pool:
+        raw, scaled = pool.map(_c5_cond2, [False, True])
+    _save("c5_cond2", {"c5_member0_cond2_r4": raw, "c5_member0_colscaled_cond2_r4": scaled})
+
+
 if __name__ == "__main__":
     job = sys.argv[1] if len(sys.argv) > 1 else "quick"
     ref = pyoracle.Oracle("ref")
     {"quick": quick, "c3_sigma_max": c3_sigma_max, "c4_sigma_max": c4_sigma_max,
-     "c2_cond2": c2_cond2, "c5_scaled": c5_scaled}[job](ref)
+     "c2_cond2": c2_cond2, "c5_scaled": c5_scaled, "c2_verify": c2_verify,
+     "c5_sigma_max": c5_sigma_max, "c5_cond2": c5_cond2}[job](ref)

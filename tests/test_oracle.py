@@ -173,3 +173,38 @@ def test_verify_solution_port_vs_ref(port, ref):
     r1 = port.verify_solution(a, xh, b, kappa=50.0, a_norm=3.0)
     r2 = ref.verify_solution(a, xh, b, kappa=50.0, a_norm=3.0)
     assert r1 == r2
+
+
+@pytest.mark.parametrize("kind,grid,param", [(1, 16, 0), (2, 8, 0), (3, 6, 0), (5, 3000, 256)])
+def test_reference_arm_generator_matches_product(kind, grid, param):
+    # bench.py's reference arm builds its workload with oracle/_build/libcondkit_gen.so (a g++
+    # build of the product's host generator) so that it never loads libcondkit_b200.so; the
+    # two builds must emit the same operator bit for bit.
+    import pyoracle
+    from paper_2409_11515_b200 import configs
+    a = pyoracle.generate(kind, grid, 7, param)
+    b = configs.generate(kind, grid, 7, param)
+    assert a.nrows == b.nrows
+    assert np.array_equal(a.row_offsets, b.row_offsets)
+    assert np.array_equal(a.col_indices, b.col_indices)
+    assert np.array_equal(a.values.view(np.uint64), b.values.view(np.uint64))
+
+
+def test_optimised_reference_builds_agree(ref):
+    # The -O3 builds bench.py times compute the same bits as the
+    # -O2 build the golden fixtures come from.
+    import pyoracle
+    a = M.row_scaled(M.laplacian2d(12), ref, 3)
+    cfg = M.cfg(seed=5, max_iter=60, patience=60, alpha=1e-2)
+    base = ref.projected_adam_explicit(a, cfg, trace=True)
+    flags = pyoracle._cpu_flags()
+    for which in ("ref_v3", "ref_native"):
+        if not pyoracle.available(which) or (which == "ref_native" and
+                                             pyoracle.best_reference() != "ref_native"):
+            continue
+        if which == "ref_v3" and not {"avx2", "fma", "bmi2"} <= flags:
+            continue
+        e = pyoracle.Oracle(which).projected_adam_explicit(a, cfg, trace=True)
+        assert e.value == base.value and e.iterations == base.iterations
+        assert np.array_equal(e.witness, base.witness)
+        assert np.array_equal(e.trace, base.trace)
