@@ -192,10 +192,14 @@ ck_status ck_session_free(ck_session s);
 
 /* ------------------------------------------- LU factors and the InverseOracle */
 /* lu_factorize(A, pivot_tol), lu.hpp:55-177, on the device: band LU with row
- * partial pivoting (first largest candidate), the same singularity tests
- * (NumericallySingular when the best pivot < pivot_tol * column max;
- * StructurallySingular only for an empty column -- the band form does not track
- * structure). On failure *fail_col / *fail_pivot (may be NULL) are set. */
+ * partial pivoting and the reference's pivot rule -- the largest candidate,
+ * ties to the first row in the elimination's touched order (lu.hpp:88-124) --
+ * and its singularity tests: StructurallySingular when no unpivoted row of the
+ * column is touched (lu.hpp:126), NumericallySingular when the best pivot is 0
+ * or < pivot_tol * column max (:127-129). On failure *fail_col / *fail_pivot
+ * (may be NULL) are set. Limits (CK_ERR_UNSUPPORTED / CK_ERR_OUT_OF_MEMORY,
+ * reported before any allocation): kl + ku <= 16319 (the solve window) and
+ * ~(3 kl + ku) * n * 8 bytes of device memory. */
 ck_status ck_lu_factorize(ck_matrix a, double pivot_tol, ck_lu* out, int64_t* fail_col,
                           double* fail_pivot);
 /* lu_factorize of nmem matrices at once (run_bench's per-matrix cond2 over an
@@ -210,6 +214,14 @@ ck_status ck_lu_get_info(ck_lu f, int64_t* n, int64_t* kl, int64_t* ku, double* 
                          int64_t* device_bytes);
 /* LAPACK band layout (ldab = 2kl+ku+1, column major, n columns) and 0-based ipiv. */
 ck_status ck_lu_export(ck_lu f, double* ab, int32_t* ipiv);
+/* LUFactors in the reference's shape (lu.hpp:42-47, 144-176): L strictly lower
+ * in pivot coordinates, U upper with the diagonal first in each row, CSR with
+ * ascending columns, row_perm[k] = original row pivoted at step k. Built on the
+ * device on first request. ck_lu_csr_info gives the entry counts; any output
+ * pointer of ck_lu_export_csr may be NULL. */
+ck_status ck_lu_csr_info(ck_lu f, int64_t* nnz_l, int64_t* nnz_u);
+ck_status ck_lu_export_csr(ck_lu f, int64_t* l_rp, int32_t* l_ci, double* l_va, int64_t* u_rp,
+                           int32_t* u_ci, double* u_va, int64_t* row_perm);
 /* lu_solve (lu.hpp:180-202): x = A^-1 b; lu_transpose_solve (lu.hpp:207-227): x = A^-T b. */
 ck_status ck_lu_solve(ck_lu f, const double* b, double* x);
 ck_status ck_lu_transpose_solve(ck_lu f, const double* b, double* x);

@@ -88,6 +88,8 @@ _SIGS = {
     "ck_lu_get_info": (C.c_int, [C.c_void_p, i64p, i64p, i64p, dp, i64p]),
     "ck_lu_factorize_batch": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_void_p, i32p, i64p, dp]),
     "ck_lu_export": (C.c_int, [C.c_void_p, dp, i32p]),
+    "ck_lu_csr_info": (C.c_int, [C.c_void_p, i64p, i64p]),
+    "ck_lu_export_csr": (C.c_int, [C.c_void_p, i64p, i32p, dp, i64p, i32p, dp, i64p]),
     "ck_lu_solve": (C.c_int, [C.c_void_p, dp, dp]),
     "ck_lu_transpose_solve": (C.c_int, [C.c_void_p, dp, dp]),
     "ck_loss_inverse": (C.c_int, [C.c_void_p, dp, dp]),

@@ -698,6 +698,7 @@ namespace ck {
 void lu_factorize(ck_lu_s* f, ck_matrix_s* m, double pivot_tol, int64_t* fail_col,
                   double* fail_pivot);
 void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st);
+void lu_build_csr(ck_lu_s* f);
 void session_create_inverse(ck_session_s* s, ck_lu_s* lu, const ck_adam_cfg* cfg,
                             const uint64_t* seeds, int R);
 
@@ -829,6 +830,38 @@ ck_status ck_lu_export(ck_lu f, double* ab, int32_t* ipiv) {
     if (ab) CK_CUDA(cudaMemcpyAsync(ab, f->ab.p, f->ab.bytes(), cudaMemcpyDeviceToHost, st));
     if (ipiv) CK_CUDA(cudaMemcpyAsync(ipiv, f->ipiv.p, sizeof(int32_t) * f->n, cudaMemcpyDeviceToHost, st));
     CK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+ck_status ck_lu_csr_info(ck_lu f, int64_t* nnz_l, int64_t* nnz_u) {
+  return guarded([&] {
+    LU(f);
+    lu_build_csr(f);
+    if (nnz_l) *nnz_l = f->nnz_l;
+    if (nnz_u) *nnz_u = f->nnz_u;
+  });
+}
+
+ck_status ck_lu_export_csr(ck_lu f, int64_t* l_rp, int32_t* l_ci, double* l_va, int64_t* u_rp,
+                           int32_t* u_ci, double* u_va, int64_t* row_perm) {
+  return guarded([&] {
+    LU(f);
+    lu_build_csr(f);
+    cudaStream_t st = f->stream;
+    const int64_t n = f->n;
+    auto get = [&](void* dst, const void* src, int64_t bytes) {
+      if (dst && bytes > 0) CK_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, st));
+    };
+    get(l_rp, f->l_rp.p, 8 * (n + 1));
+    get(l_ci, f->l_ci.p, 4 * f->nnz_l);
+    get(l_va, f->l_va.p, 8 * f->nnz_l);
+    get(u_rp, f->u_rp.p, 8 * (n + 1));
+    get(u_ci, f->u_ci.p, 4 * f->nnz_u);
+    get(u_va, f->u_va.p, 8 * f->nnz_u);
+    std::vector<int32_t> rp32((size_t)(row_perm ? n : 0));
+    get(rp32.data(), f->rowperm.p, row_perm ? 4 * n : 0);
+    CK_CUDA(cudaStreamSynchronize(st));
+    for (int64_t k = 0; row_perm && k < n; ++k) row_perm[k] = rp32[(size_t)k];
   });
 }
 

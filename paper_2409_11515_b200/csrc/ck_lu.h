@@ -33,10 +33,28 @@ struct BandView {
   int64_t stage_cap;
   // runs shorter than this many rows are read directly instead of staged
   int64_t stage_min;
+  // ---- factorisation only (ck_lu.cu) -------------------------------------
+  // Touch keys: the reference's `touched` order of each working column
+  // (lu.hpp:88-110), which decides pivot ties and structural singularity.
+  // Entry (i, j) at key[(kv + i - j) + (j % kw) * ldab]: a window of kw
+  // columns (kw = kv + 64 covers every column a panel step can reach).
+  //   kKeyUntouched  never touched;   kKeyOriginal  an entry of A;
+  //   1 + (s - (j - kv)) * (kl + 1) + rank   filled by step s, where rank is the
+  //   row's position in the stored multipliers of column s (lcols[s] order).
+  // Once column j is factored, its L rows hold their rank (kKeyUntouched when
+  // the multiplier is not stored).
+  uint32_t* key;
+  int64_t kw;
+  const uint32_t* abit;  // structure of A, one bit per band position (ab's indexing)
+  int32_t* orig;         // orig[i]: original row now at position i
+  int32_t* rowperm;      // rowperm[j]: original row pivoted at step j (LUFactors::row_perm)
 };
 
+constexpr uint32_t kKeyUntouched = 0xFFFFFFFFu;
+constexpr uint32_t kKeyOriginal = 0xFFFFFFFEu;
+
 struct LUStatus {
-  int32_t code;  // 0 ok, 4 structurally singular, 5 numerically singular
+  int32_t code;  // 0 ok, 4 structurally singular, 5 numerically singular (ck_status values)
   int32_t _pad;
   int64_t column;
   double pivot;
@@ -79,9 +97,18 @@ struct ck_lu_s {
   int64_t n = 0, kl = 0, ku = 0;
   double pivot_min = 0.0;
   ck::DBuf<double> ab, lb, rdiag;
-  ck::DBuf<int32_t> ipiv, bperm;
+  ck::DBuf<int32_t> ipiv, bperm, rowperm;
+  // factorisation-time state (freed by lu_finish)
+  ck::DBuf<uint32_t> key, abit;
+  ck::DBuf<int32_t> orig;
   ck::DBuf<ck::LUStatus> status;
   ck::DBuf<double> work;  // solve scratch
+  // CSR factors in the reference's LUFactors shape (built on request: lu_build_csr)
+  bool csr_built = false;
+  int64_t nnz_l = 0, nnz_u = 0;
+  ck::DBuf<int64_t> l_rp, u_rp;
+  ck::DBuf<int32_t> l_ci, u_ci;
+  ck::DBuf<double> l_va, u_va;
   ck_lu_s() = default;
   ck_lu_s(const ck_lu_s&) = delete;
   ck_lu_s& operator=(const ck_lu_s&) = delete;
@@ -93,6 +120,7 @@ struct ck_lu_s {
   }
   ck::BandView view() {
     return ck::BandView{n, kl, ku, kl + ku, 2 * kl + ku + 1, ab.p, ipiv.p, lb.p,
-                        ck::kLUBlock + kl, bperm.p, rdiag.p, 0};
+                        ck::kLUBlock + kl, bperm.p, rdiag.p, 0, 0,
+                        key.p, kl + ku + 64, abit.p, orig.p, rowperm.p};
   }
 };

@@ -39,6 +39,7 @@ class LUFactors:
         self.n, self.kl, self.ku = n_.value, kl.value, ku.value
         self.pivot_min = pm.value
         self.device_bytes = nb.value
+        self._csr = None
 
     def solve(self, b) -> np.ndarray:
         b = _lib.as_f64(b, self.n, "lu_solve: rhs")
@@ -53,6 +54,40 @@ class LUFactors:
                    "lu_transpose_solve")
         return x
 
+    def export_csr(self):
+        """(L, U, row_perm) in the reference's LUFactors shape (lu.hpp:42-47): L strictly
+        lower in pivot coordinates (unit diagonal implicit), U upper with the diagonal
+        first in each row, both CSR SparseMatrix; row_perm[k] = original row pivoted at
+        step k. Assembled on the device (ck_lu_export_csr)."""
+        if self._csr is None:
+            lib = _lib.load()
+            nl, nu = C.c_int64(), C.c_int64()
+            _lib.check(lib.ck_lu_csr_info(self.handle, C.byref(nl), C.byref(nu)), "ck_lu_csr_info")
+            n = self.n
+            lrp, urp = np.empty(n + 1, np.int64), np.empty(n + 1, np.int64)
+            lci, uci = np.empty(max(nl.value, 1), np.int32), np.empty(max(nu.value, 1), np.int32)
+            lva, uva = np.empty(max(nl.value, 1)), np.empty(max(nu.value, 1))
+            perm = np.empty(n, np.int64)
+            _lib.check(lib.ck_lu_export_csr(self.handle, _lib.i64ptr(lrp), _lib.i32ptr(lci),
+                                            _lib.dptr(lva), _lib.i64ptr(urp), _lib.i32ptr(uci),
+                                            _lib.dptr(uva), _lib.i64ptr(perm)), "ck_lu_export_csr")
+            l = SparseMatrix(n, n, lrp, lci[: nl.value], lva[: nl.value], validate=False)
+            u = SparseMatrix(n, n, urp, uci[: nu.value], uva[: nu.value], validate=False)
+            self._csr = (l, u, perm)
+        return self._csr
+
+    @property
+    def l(self) -> SparseMatrix:
+        return self.export_csr()[0]
+
+    @property
+    def u(self) -> SparseMatrix:
+        return self.export_csr()[1]
+
+    @property
+    def row_perm(self) -> np.ndarray:
+        return self.export_csr()[2]
+
     def export_band(self):
         """(ab, ipiv) in LAPACK band layout: ab[kv + i - j, j] = factor(i, j)."""
         ldab = 2 * self.kl + self.ku + 1
@@ -61,39 +96,6 @@ class LUFactors:
         _lib.check(_lib.load().ck_lu_export(self.handle, _lib.dptr(ab), _lib.i32ptr(ipiv)),
                    "ck_lu_export")
         return ab.reshape(self.n, ldab).T.copy(), ipiv
-
-    def dense_factors(self):
-        """(perm, L, U) with A[perm] = L @ U (dense; small n only, for inspection)."""
-        ab, ipiv = self.export_band()
-        n, kl, ku = self.n, self.kl, self.ku
-        kv = kl + ku
-        L = np.eye(n)
-        U = np.zeros((n, n))
-        for j in range(n):
-            for i in range(max(0, j - kv), j + 1):
-                U[i, j] = ab[kv + i - j, j]
-        perm = np.arange(n)
-        # multipliers of step j are in rows j+1.. of the row order at step j; apply
-        # every later interchange to them to reach final pivot coordinates
-        cols = []
-        for j in range(n):
-            km = min(kl, n - 1 - j)
-            cols.append({j + 1 + r: ab[kv + 1 + r, j] for r in range(km)})
-        for j in range(n):
-            p = int(ipiv[j])
-            if p != j:
-                perm[[j, p]] = perm[[p, j]]
-                for k in range(j):
-                    c = cols[k]
-                    a, b = c.pop(j, 0.0), c.pop(p, 0.0)
-                    if b != 0.0:
-                        c[j] = b
-                    if a != 0.0:
-                        c[p] = a
-        for j in range(n):
-            for i, v in cols[j].items():
-                L[i, j] = v
-        return perm, L, U
 
 
 def lu_factorize(a: SparseMatrix, pivot_tol: float = 1e-12) -> LUFactors:

@@ -144,11 +144,56 @@ def test_config4_full_size():
     _cmp_est(ck.norm2(a, configs.baseline_adam(1)), g["c4_projected_adam"])
 
 
-@pytest.mark.skipif(not os.environ.get("CK_SLOW"),
-                    reason="several minutes: sigma_min at n=196k runs one CTA per sweep (set CK_SLOW=1)")
-def test_config2_cond2_full_size():
-    g = gold("c2_cond2")["c2_cond2_r1"]
-    r = ck.cond2(configs.config(2), configs.baseline_adam(1), 1, 1e-14)
-    assert r.kappa == pytest.approx(g["kappa"], rel=TOL)
-    _cmp_est(r.operator_norm, g["operator_norm"])
-    _cmp_est(r.inverse_norm, g["inverse_norm"])
+def test_config2_verify_solution_full_size():
+    # BASELINE config 2 at full size (n = 196,608): verify_solution (error_bounds.hpp:166-217)
+    # with kappa estimated by cond2 (one restart per norm) against the reference's own report;
+    # the same cond2 run as tests/golden/c2_cond2.json
+    g = gold("c2_verify")
+    inp, want = g["inputs"], g["c2_verify_r1"]
+    a = configs.config(2)
+    cfg = configs.baseline_adam(1)
+    xs = configs.uniform_in(inp["x_seed"], a.ncols, -1.0, 1.0)
+    b = ck.matvec(a, xs)
+    u = ck.random_unit_vector(a.ncols, inp["u_seed"])
+    xh = xs + inp["rel_delta"] * np.linalg.norm(xs) * u
+    rep = ck.verify_solution(a, xh, b, ck.VerifyOptions(adam=cfg, restarts=1))
+    assert rep.residual_norm == pytest.approx(want["residual_norm"], rel=1e-12)
+    assert rep.b_norm == pytest.approx(want["b_norm"], rel=1e-12)
+    assert rep.xhat_norm == pytest.approx(want["xhat_norm"], rel=1e-12)
+    assert rep.a_norm == pytest.approx(want["a_norm"], rel=TOL)
+    assert rep.kappa == pytest.approx(want["kappa"], rel=TOL)
+    assert rep.kappa == pytest.approx(gold("c2_cond2")["c2_cond2_r1"]["kappa"], rel=TOL)
+    for k in ("loose_lower", "loose_upper", "tight_lower", "tight_upper", "true_error_cap",
+              "singularity_cap"):
+        assert getattr(rep, k) == pytest.approx(want[k], rel=TOL), k
+    assert rep.verdict.value == want["verdict"]
+    assert not rep.kappa_supplied
+
+
+def test_config5_full_size_members_sigma_max():
+    # BASELINE config 5 members at full size (n = 100,000, bandwidth 256), 4 restarts each,
+    # through the ensemble driver (estimate_norm_batch: members packed block-diagonally)
+    from paper_2409_11515_b200 import batch
+    g = gold("c5_sigma_max")
+    members = [configs.ensemble_member(i, 1) for i in range(8)]
+    est = batch.estimate_norm_batch(members, configs.baseline_adam(1), 4,
+                                    seeds=batch.member_seeds(8))
+    for i, e in enumerate(est):
+        _cmp_est(e, g[f"c5_member{i}_estimate_norm_r4"])
+
+
+def test_config5_full_size_member_cond2():
+    # run_bench's per-matrix cond2 (bench.hpp:430-442) on full-size member 0, as generated
+    # (kappa ~ 1e19 >= 1/eps) and column-scaled (kappa ~ 1e4), 4 restarts per norm, through
+    # cond2_batch (band LU batch + one CTA per restart)
+    from paper_2409_11515_b200 import batch
+    g = gold("c5_cond2")
+    m = configs.ensemble_member(0, 1)
+    seed = batch.member_seeds(1)[0]
+    res = batch.cond2_batch([m, _column_scaled(m)], configs.baseline_adam(1), 4,
+                            seeds=[seed, seed])
+    for r, key in zip(res, ("c5_member0_cond2_r4", "c5_member0_colscaled_cond2_r4")):
+        want = g[key]
+        assert r.kappa == pytest.approx(want["kappa"], rel=TOL), key
+        _cmp_est(r.operator_norm, want["operator_norm"])
+        _cmp_est(r.inverse_norm, want["inverse_norm"])

@@ -11,36 +11,28 @@ import paper_2409_11515_b200 as ck
 pytestmark = pytest.mark.gpu
 
 
-def oracle_dense_lu(port, a, tol):
-    f = port.lu_factorize(a, tol)
-    e = f.export()
-    n = a.nrows
-    L = np.eye(n)
-    U = np.zeros((n, n))
-    lrp, lci, lva = e["l"]
-    urp, uci, uva = e["u"]
-    for i in range(n):
-        for k in range(lrp[i], lrp[i + 1]):
-            L[i, lci[k]] = lva[k]
-        for k in range(urp[i], urp[i + 1]):
-            U[i, uci[k]] = uva[k]
-    return e["row_perm"], L, U, f
+def assert_same_factors(f, rf, a=None):
+    """Device LUFactors (CSR export, lu.hpp:42-47 shape) == the oracle's, bit for bit."""
+    e = rf.export()
+    l, u, perm = f.export_csr()
+    assert np.array_equal(perm, e["row_perm"])
+    for mine, (rp, ci, va) in ((l, e["l"]), (u, e["u"])):
+        assert np.array_equal(mine.row_offsets, rp)
+        assert np.array_equal(mine.col_indices, ci)
+        assert np.array_equal(mine.values.view(np.uint64), va.view(np.uint64))
+    assert f.pivot_min == rf.pivot_min
+    if a is not None and a.nrows <= 400:
+        d = a.to_dense()
+        L = l.to_dense() + np.eye(a.nrows)
+        assert np.linalg.norm(d[perm] - L @ u.to_dense()) <= 1e-13 * np.linalg.norm(d)
+        assert np.abs(l.values).max(initial=0.0) <= 1.0
 
 
 @pytest.mark.parametrize("n,seed", [(5, 8), (20, 15), (50, 29), (50, 36), (100, 3)])
 def test_factors_match_reference_bitwise(port, n, seed):
     # test_lu.cpp:54-70 fixtures; same pivots and unfused arithmetic -> same factors
     a = M.random_sparse(port, n, 0.3, seed)
-    f = ck.lu_factorize(a, 1e-12)
-    perm, L, U = f.dense_factors()
-    rperm, rL, rU, rf = oracle_dense_lu(port, a, 1e-12)
-    assert np.array_equal(perm, rperm)
-    assert np.array_equal(U, rU)
-    assert np.array_equal(L, rL)
-    assert f.pivot_min == rf.pivot_min
-    d = a.to_dense()
-    assert np.linalg.norm(d[perm] - L @ U) <= 1e-13 * np.linalg.norm(d)
-    assert np.abs(L).max() <= 1.0
+    assert_same_factors(ck.lu_factorize(a, 1e-12), port.lu_factorize(a, 1e-12), a)
 
 
 def test_long_band_factors_match_reference_bitwise(port):
@@ -48,11 +40,8 @@ def test_long_band_factors_match_reference_bitwise(port):
     from paper_2409_11515_b200 import configs
     a = configs.ensemble_member(3, 1, n=1500, bw=200)
     f = ck.lu_factorize(a, 1e-14)
-    perm, L, U = f.dense_factors()
-    rperm, rL, rU, rf = oracle_dense_lu(port, a, 1e-14)
-    assert np.array_equal(perm, rperm)
-    assert np.array_equal(U, rU)
-    assert np.array_equal(L, rL)
+    rf = port.lu_factorize(a, 1e-14)
+    assert_same_factors(f, rf)
     b = port.random_unit_vectors(5, a.nrows)[0]
     assert np.linalg.norm(f.solve(b) - port.lu_solve(rf, b)) <= 1e-12 * np.linalg.norm(port.lu_solve(rf, b))
 
