@@ -21,11 +21,10 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -52,48 +51,63 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region (NVML every 5 ms
+    from a thread, plus one sample at start and one at stop, so even a 40 ms region
+    has a record; nvidia-smi -lms 100 where NVML is missing)."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index: int):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    def __init__(self, index: int, period_s: float = 0.005):
+        import threading
+        self.samples, self.reasons, self.max_mhz = [], set(), 0.0
+        self.source = "nvml"
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
-                stderr=subprocess.DEVNULL)
-        except OSError:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001
+            self.nv = None
+            self.source = "unavailable"
+        self.stop_flag = threading.Event()
+        self.period = period_s
+        self.sample()
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        if self.nv is not None:
+            self.t.start()
+
+    def sample(self):
+        if self.nv is None:
+            return
+        try:
+            self.samples.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+            mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, attr in self.REASONS:
+                if mask & getattr(self.nv, attr, 0):
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _loop(self):
+        while not self.stop_flag.wait(self.period):
+            self.sample()
 
     def stop(self):
-        if self.p is None:
+        if self.nv is None:
             return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.p.kill()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
-        os.unlink(self.f.name)
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            try:
-                sm.append(float(r[0]))
-                mx = max(mx, float(r[1]))
-                for nm, v in zip(names, r[4:8]):
-                    if v.strip().lower() == "active":
-                        reasons.add(nm)
-            except (ValueError, IndexError):
-                continue
-        if not sm:
+        self.stop_flag.set()
+        self.t.join(timeout=2)
+        self.sample()
+        if not self.samples:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": "NVML, 5 ms period + start/stop samples"}
 
 
 def make_ensemble(rank: int, world: int, members: int | None, n: int | None):
@@ -400,8 +414,9 @@ def run_ours(args):
         R = 1
     t_gen = time.perf_counter() - t_gen
     seed = 1 if rank == 0 else ck.mix_seed(1, rank)
-    total_iters = args.warmup + 2 * args.steps + 16  # both timed passes stay inside max_iter
-    cfg = configs.baseline_adam(seed, max_iter=total_iters)
+    # every timed pass (K steps, the kernel split, the >= 1 s sustained pass) stays inside
+    # max_iter, with patience = max_iter: no column finishes in a timed region
+    cfg = configs.baseline_adam(seed, max_iter=10_000_000)
 
     t_up = time.perf_counter()
     dev = a.device()
@@ -429,6 +444,13 @@ def run_ours(args):
     barrier()
     clocks = sampler.stop() if sampler else None
     ms_max = allmax(ms_total)
+    # sustained: the same loop for >= 1 s of device time (the K-step value is a burst)
+    sus_steps = max(args.steps, int(math.ceil(args.sustained_s * 1000.0 * args.steps / ms_max)))
+    barrier()
+    sampler2 = ClockSampler(local) if rank == 0 else None
+    ms_sus = allmax(sum(sess.time(sus_steps, mode=1)[0] for sess in sessions))
+    barrier()
+    clocks_sus = sampler2.stop() if sampler2 else None
     # kernel split (events between the two kernels, no graph) for the roofline
     ms_apply = ms_tr = 0.0
     for sess in sessions:
@@ -438,6 +460,8 @@ def run_ours(args):
     runs_per_step = (len(member_idx) * R) if ensemble else 1
     total_runs = allsum(runs_per_step) if ensemble else world
     value = total_runs * args.steps / (ms_max / 1000.0)
+    sustained = {"value": total_runs * sus_steps / (ms_sus / 1000.0), "unit": UNIT,
+                 "steps": sus_steps, "seconds": ms_sus / 1000.0, "clocks": clocks_sus}
     for sess in sessions:
         sess.close()
 
@@ -533,6 +557,7 @@ def run_ours(args):
             "effective_gbs_per_gpu": step_eff_gbs,
             "bytes_per_iteration": iter_bytes,
             "clocks": clocks,
+            "sustained": sustained,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": 2 * args.steps * len(groups),
@@ -553,6 +578,8 @@ def main():
     p.add_argument("--config", type=int, default=4)
     p.add_argument("--grid", type=int, default=None, help="override the grid (smoke runs)")
     p.add_argument("--e2e-iters", type=int, default=2000)
+    p.add_argument("--sustained-s", type=float, default=1.0,
+                   help="device seconds of the sustained pass reported next to value")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)

@@ -106,6 +106,12 @@ ck_status ck_host_unregister(void* ptr);
  * (and first joins) the previous one. No reference counterpart: the reference
  * draws inside projected_adam (condest.hpp:191). */
 ck_status ck_start_vector_prefetch(uint64_t seed, int64_t n);
+/* Drops the pending prefetch (joins its thread, frees its pinned buffer): for a
+ * caller whose session creation failed after requesting one. A session that
+ * finds a slot for another seed or size drops it too. */
+ck_status ck_start_vector_prefetch_cancel(void);
+/* Slots taken by a session and slots dropped, since the library was loaded. */
+ck_status ck_start_vector_prefetch_stats(uint64_t* taken, uint64_t* dropped);
 void ck_adam_default(ck_adam_cfg* cfg);
 
 /* --------------------------------------------------- rng.hpp mirror (host) */

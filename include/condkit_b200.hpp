@@ -1,6 +1,10 @@
-// condkit_b200.hpp -- C++ drop-in for the reference estimator / error-bound
-// interface (condkit/condest.hpp, lu.hpp, error_bounds.hpp), header-only over
-// the C ABI of condkit_b200.h. Link with libcondkit_b200.so.
+// condkit_b200.hpp -- standalone C++ API over the C ABI of condkit_b200.h
+// (no reference headers needed). Link with libcondkit_b200.so.
+//
+// The drop-in for code written against the reference is proj/include/condkit/
+// (condest.hpp, lu.hpp, error_bounds.hpp in namespace condkit, shadowing the
+// reference's headers of the same names); this header is the same device
+// functionality under namespace condkit_b200 for callers without them.
 //
 // Call sites keep their types: every function is a template over any CSR type
 // with the accessors of condkit::SparseMatrix (nrows(), ncols(),

@@ -56,6 +56,8 @@ _SIGS = {
     "ck_device_synchronize": (C.c_int, []),
     "ck_host_register": (C.c_int, [C.c_void_p, C.c_uint64]),
     "ck_start_vector_prefetch": (C.c_int, [C.c_uint64, C.c_int64]),
+    "ck_start_vector_prefetch_cancel": (C.c_int, []),
+    "ck_start_vector_prefetch_stats": (C.c_int, [u64p, u64p]),
     "ck_host_unregister": (C.c_int, [C.c_void_p]),
     "ck_adam_default": (None, [C.POINTER(AdamCfg)]),
     "ck_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),

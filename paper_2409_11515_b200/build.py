@@ -69,6 +69,7 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
     os.replace(out + ".tmp", out)
     if not prof:
         build_cli()
+        build_dropin()
     return out
 
 
@@ -85,6 +86,51 @@ def build_cli() -> str:
     subprocess.run(cmd, check=True)
     os.replace(CLI + ".tmp", CLI)
     return CLI
+
+
+REF_INC = "/root/reference/proj/include"
+REF_DEMO = "/root/reference/proj/demo"
+DROPIN = os.path.join(ROOT, "build", "dropin")
+DEMOS = ("condition_estimate", "residual_vs_error")
+
+
+def build_dropin() -> list:
+    """The reference's own call sites against the B200 headers of proj/include/condkit
+    (they shadow the reference's condest.hpp, lu.hpp, error_bounds.hpp), built into
+    build/dropin/ where the reference headers exist (this container; the binaries travel
+    to the GPU box with the snapshot, which has no reference tree):
+      condest_checks      tests/cpp/dropin_condest_checks.cpp
+      <demo>              the reference's demo/<demo>.cpp, unchanged
+    and, as the parity anchor, the same demos against the reference alone (ref_<demo>),
+    whose output is recorded in tests/golden/dropin_<demo>.txt."""
+    if not os.path.isdir(os.path.join(REF_INC, "condkit")):
+        return []
+    os.makedirs(DROPIN, exist_ok=True)
+    ours = ["-I", os.path.join(ROOT, "proj", "include"), "-I", os.path.join(ROOT, "include"),
+            "-I", REF_INC]
+    link = ["-L", PKG, "-lcondkit_b200", "-Wl,-rpath,$ORIGIN/../../paper_2409_11515_b200",
+            "-lpthread"]
+    jobs = [(os.path.join(ROOT, "tests", "cpp", "dropin_condest_checks.cpp"), "condest_checks",
+             ours, link)]
+    for d in DEMOS:
+        src = os.path.join(REF_DEMO, d + ".cpp")
+        jobs.append((src, d, ours, link))
+        jobs.append((src, "ref_" + d, ["-I", REF_INC], ["-lpthread"]))
+    procs = []
+    for src, name, inc, lk in jobs:
+        exe = os.path.join(DROPIN, name)
+        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-Wextra"] + inc + [src, "-o", exe] + lk
+        procs.append((exe, subprocess.Popen(cmd)))
+    failed = [exe for exe, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"g++ {failed}")
+    golden = os.path.join(ROOT, "tests", "golden")
+    for d in DEMOS:
+        out = subprocess.run([os.path.join(DROPIN, "ref_" + d)], check=True, capture_output=True,
+                             text=True).stdout
+        with open(os.path.join(golden, f"dropin_{d}.txt"), "w") as f:
+            f.write(out)
+    return [exe for exe, _ in procs]
 
 
 if __name__ == "__main__":

@@ -126,18 +126,24 @@ class Session:
         self.n = oracle.dimension()
         lib = _lib.load()
         seeds = np.ascontiguousarray([int(s) & 0xFFFFFFFFFFFFFFFF for s in seeds], np.uint64)
-        if (isinstance(oracle, ExplicitOracle) and oracle.a._dev is None and seeds.size
-                and self.n >= (1 << 20)):
+        prefetch = (isinstance(oracle, ExplicitOracle) and oracle.a._dev is None and seeds.size
+                    and self.n >= (1 << 20))
+        if prefetch:
             # draw the first start vector on a host thread while A uploads
             _lib.check(lib.ck_start_vector_prefetch(int(seeds[0]), self.n),
                        "ck_start_vector_prefetch")
-        handle = _device_handle(oracle)
         self._cfg = _lib.cfg_struct(cfg)
         self.ncols = seeds.size
         h = C.c_void_p()
-        _lib.check(lib.ck_session_create(handle, C.byref(self._cfg),
-                                         seeds.ctypes.data_as(_lib.u64p), self.ncols, C.byref(h)),
-                   "ck_session_create")
+        try:
+            handle = _device_handle(oracle)
+            _lib.check(lib.ck_session_create(handle, C.byref(self._cfg),
+                                             seeds.ctypes.data_as(_lib.u64p), self.ncols,
+                                             C.byref(h)), "ck_session_create")
+        except BaseException:
+            if prefetch:  # no session took the slot: release its thread and pinned buffer
+                lib.ck_start_vector_prefetch_cancel()
+            raise
         self.handle = h
         self._fin = weakref.finalize(self, lib.ck_session_free, h)
 

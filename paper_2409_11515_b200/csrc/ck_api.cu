@@ -42,7 +42,8 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
 }
 
 template <class F>
-static ck_status guarded(F&& f) {
+static ck_status guarded(const char* name, F&& f) {
+  NvtxRange range(name);  // one NVTX range per C-ABI call (nsys / ncu --nvtx)
   try {
     f();
     return CK_OK;
@@ -265,20 +266,31 @@ struct StartPrefetch {
 };
 std::mutex g_pf_mu;
 std::unique_ptr<StartPrefetch> g_pf;
+uint64_t g_pf_taken = 0, g_pf_dropped = 0;  // ck_start_vector_prefetch_stats
 }  // namespace
 
+// The slot is consumed by the first session that asks: taken when seed and n
+// match, dropped (thread joined, pinned buffer freed) otherwise.
 bool take_start_prefetch(uint64_t seed, int64_t n, void* engine, PinnedBuf<double>* hx) {
   std::unique_ptr<StartPrefetch> pf;
+  bool match = false;
   {
     std::lock_guard<std::mutex> lk(g_pf_mu);
-    if (!g_pf || g_pf->seed != seed || g_pf->n != n) return false;
+    if (!g_pf) return false;
+    match = g_pf->seed == seed && g_pf->n == n;
     pf = std::move(g_pf);
   }
   if (pf->th.joinable()) pf->th.join();
-  if (pf->err || pf->pin.p == nullptr) return false;  // draw it again on the caller's thread
+  if (!match || pf->err || pf->pin.p == nullptr) {  // draw it on the caller's thread
+    std::lock_guard<std::mutex> lk(g_pf_mu);
+    ++g_pf_dropped;
+    return false;
+  }
   *static_cast<std::mt19937_64*>(engine) = pf->g;
   std::swap(hx->p, pf->pin.p);
   std::swap(hx->n, pf->pin.n);
+  std::lock_guard<std::mutex> lk(g_pf_mu);
+  ++g_pf_taken;
   return true;
 }
 
@@ -286,7 +298,7 @@ bool take_start_prefetch(uint64_t seed, int64_t n, void* engine, PinnedBuf<doubl
 
 extern "C" ck_status ck_start_vector_prefetch(uint64_t seed, int64_t n) {
   using namespace ck;
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (n <= 0) fail(CK_ERR_INVALID_ARGUMENT, "ck_start_vector_prefetch: n must be positive");
     std::unique_ptr<StartPrefetch> old;
     auto pf = std::make_unique<StartPrefetch>();
@@ -314,6 +326,25 @@ extern "C" ck_status ck_start_vector_prefetch(uint64_t seed, int64_t n) {
     std::lock_guard<std::mutex> lk(g_pf_mu);
     old = std::move(g_pf);
     g_pf = std::move(pf);
+  });
+}
+
+extern "C" ck_status ck_start_vector_prefetch_cancel(void) {
+  using namespace ck;
+  return guarded(__func__, [&] {
+    std::unique_ptr<StartPrefetch> old;
+    std::lock_guard<std::mutex> lk(g_pf_mu);
+    old = std::move(g_pf);
+    if (old) ++g_pf_dropped;
+  });
+}
+
+extern "C" ck_status ck_start_vector_prefetch_stats(uint64_t* taken, uint64_t* dropped) {
+  using namespace ck;
+  return guarded(__func__, [&] {
+    std::lock_guard<std::mutex> lk(g_pf_mu);
+    if (taken) *taken = g_pf_taken;
+    if (dropped) *dropped = g_pf_dropped;
   });
 }
 
@@ -360,7 +391,7 @@ const char* ck_last_error(void) { return g_last_error.c_str(); }
 int32_t ck_abi_version(void) { return 1; }
 
 ck_status ck_device_count(int32_t* count) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
@@ -374,7 +405,7 @@ ck_status ck_device_count(int32_t* count) {
 }
 
 ck_status ck_device_memory(uint64_t* free_bytes, uint64_t* total_bytes, int32_t* sm_count) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     size_t f = 0, t = 0;
     CK_CUDA(cudaMemGetInfo(&f, &t));
     int dev = 0, sms = 0;
@@ -387,7 +418,7 @@ ck_status ck_device_memory(uint64_t* free_bytes, uint64_t* total_bytes, int32_t*
 }
 
 ck_status ck_set_device(int32_t device) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0) {
@@ -402,18 +433,18 @@ ck_status ck_set_device(int32_t device) {
 }
 
 ck_status ck_device_synchronize(void) {
-  return guarded([&] { CK_CUDA(cudaDeviceSynchronize()); });
+  return guarded(__func__, [&] { CK_CUDA(cudaDeviceSynchronize()); });
 }
 
 ck_status ck_host_register(void* ptr, uint64_t bytes) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (bytes == 0) return;
     CK_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
   });
 }
 
 ck_status ck_host_unregister(void* ptr) {
-  return guarded([&] { CK_CUDA(cudaHostUnregister(ptr)); });
+  return guarded(__func__, [&] { CK_CUDA(cudaHostUnregister(ptr)); });
 }
 
 void ck_adam_default(ck_adam_cfg* c) {
@@ -435,7 +466,7 @@ uint64_t ck_mix_seed(uint64_t base, uint64_t stream) {
 }
 
 ck_status ck_random_unit_vectors(uint64_t seed, int64_t n, int64_t count, double* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (n < 0 || count < 0) fail(CK_ERR_INVALID_ARGUMENT, "negative size");
     std::mt19937_64 g(seed);
     for (int64_t c = 0; c < count; ++c) random_unit_vector_host(&g, n, out + c * n);
@@ -443,7 +474,7 @@ ck_status ck_random_unit_vectors(uint64_t seed, int64_t n, int64_t count, double
 }
 
 ck_status ck_uniform_in(uint64_t seed, int64_t count, double lo, double hi, double* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (count < 0) fail(CK_ERR_INVALID_ARGUMENT, "negative size");
     std::mt19937_64 g(seed);
     for (int64_t i = 0; i < count; ++i)
@@ -453,7 +484,7 @@ ck_status ck_uniform_in(uint64_t seed, int64_t count, double lo, double hi, doub
 
 // ---------------------------------------------- error_bounds.hpp:59-99
 ck_status ck_loose_bounds(double rn, double bn, double kappa, double* lo, double* hi) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!(rn >= 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "residual norm must be >= 0");
     if (!(kappa >= 1.0)) fail(CK_ERR_INVALID_ARGUMENT, "kappa must be >= 1");
     if (bn == 0.0) fail(CK_ERR_ZERO_RHS, "right-hand side has zero norm");
@@ -470,7 +501,7 @@ ck_status ck_loose_bounds(double rn, double bn, double kappa, double* lo, double
 }
 
 ck_status ck_tight_bounds(double rn, double an, double xn, double kappa, double* lo, double* hi) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!(rn >= 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "residual norm must be >= 0");
     if (!(kappa >= 1.0)) fail(CK_ERR_INVALID_ARGUMENT, "kappa must be >= 1");
     if (xn == 0.0) fail(CK_ERR_ZERO_SOLUTION, "candidate solution has zero norm");
@@ -488,14 +519,14 @@ ck_status ck_tight_bounds(double rn, double an, double xn, double kappa, double*
 }
 
 ck_status ck_propagate_bound(double e, double* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!(e >= 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "bound must be >= 0");
     *out = e >= 1.0 ? std::numeric_limits<double>::infinity() : e / (1.0 - e);
   });
 }
 
 ck_status ck_singularity_bound(double kappa, double eps, double* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!(kappa >= 1.0)) fail(CK_ERR_INVALID_ARGUMENT, "kappa must be >= 1");
     if (!(eps > 0.0)) fail(CK_ERR_INVALID_ARGUMENT, "eps_mach must be > 0");
     double ke = kappa * eps;
@@ -506,7 +537,7 @@ ck_status ck_singularity_bound(double kappa, double eps, double* out) {
 // ---------------------------------------------------------- operator
 ck_status ck_matrix_upload(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
                            const double* va, ck_matrix* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (out == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "out is NULL");
     auto* m = new ck_matrix_s();
     try {
@@ -521,7 +552,7 @@ ck_status ck_matrix_upload(int64_t nrows, int64_t ncols, const int64_t* rp, cons
 }
 
 ck_status ck_matrix_free(ck_matrix a) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!a) return;
     cudaSetDevice(a->device);
     cudaStreamSynchronize(a->stream);
@@ -551,27 +582,27 @@ void matrix_info(const ck_matrix_s* a, ck_matrix_info* info) {
 
 extern "C" {
 ck_status ck_matrix_get_info(ck_matrix a, ck_matrix_info* info) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!info) fail(CK_ERR_INVALID_ARGUMENT, "info is NULL");
     matrix_info(M(a), info);
   });
 }
 
 ck_status ck_spmv(ck_matrix a, const double* x, double* y) {
-  return guarded([&] { matrix_apply_host(M(a), false, x, y); });
+  return guarded(__func__, [&] { matrix_apply_host(M(a), false, x, y); });
 }
 
 ck_status ck_spmv_t(ck_matrix a, const double* x, double* y) {
-  return guarded([&] { matrix_apply_host(M(a), true, x, y); });
+  return guarded(__func__, [&] { matrix_apply_host(M(a), true, x, y); });
 }
 
 ck_status ck_residual_norms(ck_matrix a, const double* x, const double* b, double* rn, double* xn,
                             double* bn) {
-  return guarded([&] { residual_norms(M(a), x, b, rn, xn, bn); });
+  return guarded(__func__, [&] { residual_norms(M(a), x, b, rn, xn, bn); });
 }
 
 ck_status ck_loss_explicit(ck_matrix a, const double* x, double* loss) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     bool deg = false;
     double l = loss_explicit_dev(M(a), x, &deg);
     if (deg) fail(CK_ERR_INVALID_ARGUMENT, "operator maps direction to zero (DegenerateDirection)");
@@ -580,7 +611,7 @@ ck_status ck_loss_explicit(ck_matrix a, const double* x, double* loss) {
 }
 
 ck_status ck_grad_explicit(ck_matrix a, const double* x, double* g) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     bool deg = false;
     grad_explicit_dev(M(a), x, g, &deg);
     if (deg) fail(CK_ERR_INVALID_ARGUMENT, "operator maps direction to zero (DegenerateDirection)");
@@ -590,7 +621,7 @@ ck_status ck_grad_explicit(ck_matrix a, const double* x, double* g) {
 // ------------------------------------------------------ sessions
 ck_status ck_session_create(ck_matrix a, const ck_adam_cfg* cfg, const uint64_t* seeds,
                             int32_t ncols, ck_session* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     auto* s = new ck_session_s();
     try {
@@ -604,14 +635,14 @@ ck_status ck_session_create(ck_matrix a, const ck_adam_cfg* cfg, const uint64_t*
 }
 
 ck_status ck_session_run(ck_session s, uint64_t max_steps, int32_t* finished) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     S(s);
     session_run(s, max_steps, finished);
   });
 }
 
 ck_status ck_session_step_observed(ck_session s, ck_step_info* info, double* x, double* x_min) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     S(s);
     if (s->R != 1) fail(CK_ERR_INVALID_ARGUMENT, "observer mode needs a single-column session");
     session_step_observed(s, info, x, x_min);
@@ -620,21 +651,21 @@ ck_status ck_session_step_observed(ck_session s, ck_step_info* info, double* x, 
 
 ck_status ck_session_time(ck_session s, uint64_t steps, int32_t mode, double* ms_total,
                           double* ms_apply, double* ms_transpose) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     S(s);
     session_time(s, steps, mode, ms_total, ms_apply, ms_transpose);
   });
 }
 
 ck_status ck_session_result(ck_session s, int32_t column, ck_norm_result* res, double* witness) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     S(s);
     session_result(s, column, res, witness);
   });
 }
 
 ck_status ck_session_free(ck_session s) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!s) return;
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
@@ -645,7 +676,7 @@ ck_status ck_session_free(ck_session s) {
 // projected_adam / norm2, condest.hpp:184-297, 315-317
 ck_status ck_projected_adam(ck_matrix a, const ck_adam_cfg* cfg, ck_norm_result* res,
                             double* witness) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     ck_session_s s;
     uint64_t seed = cfg->seed;
@@ -661,7 +692,7 @@ ck_status ck_projected_adam(ck_matrix a, const ck_adam_cfg* cfg, ck_norm_result*
 // restarts share each device sweep.
 ck_status ck_estimate_norm(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts,
                            ck_norm_result* res, double* witness) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
     M(a);
@@ -765,7 +796,7 @@ extern "C" {
 
 ck_status ck_lu_factorize(ck_matrix a, double pivot_tol, ck_lu* out, int64_t* fail_col,
                           double* fail_pivot) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (out == nullptr) fail(CK_ERR_INVALID_ARGUMENT, "out is NULL");
     auto* f = new ck_lu_s();
     try {
@@ -780,7 +811,7 @@ ck_status ck_lu_factorize(ck_matrix a, double pivot_tol, ck_lu* out, int64_t* fa
 
 ck_status ck_lu_factorize_batch(const ck_matrix* a, int32_t nmem, double pivot_tol, ck_lu* out,
                                 int32_t* status, int64_t* fail_col, double* fail_pivot) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (nmem < 1 || !a || !out || !status) fail(CK_ERR_INVALID_ARGUMENT, "lu_factorize_batch: bad arguments");
     std::vector<ck_matrix_s*> ms((size_t)nmem);
     for (int g = 0; g < nmem; ++g) ms[g] = M(a[g]);
@@ -804,7 +835,7 @@ ck_status ck_lu_factorize_batch(const ck_matrix* a, int32_t nmem, double pivot_t
 }
 
 ck_status ck_lu_free(ck_lu f) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!f) return;
     cudaSetDevice(f->device);
     delete f;
@@ -813,7 +844,7 @@ ck_status ck_lu_free(ck_lu f) {
 
 ck_status ck_lu_get_info(ck_lu f, int64_t* n, int64_t* kl, int64_t* ku, double* pivot_min,
                          int64_t* device_bytes) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     LU(f);
     *n = f->n;
     *kl = f->kl;
@@ -824,7 +855,7 @@ ck_status ck_lu_get_info(ck_lu f, int64_t* n, int64_t* kl, int64_t* ku, double* 
 }
 
 ck_status ck_lu_export(ck_lu f, double* ab, int32_t* ipiv) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     LU(f);
     cudaStream_t st = f->stream;
     if (ab) CK_CUDA(cudaMemcpyAsync(ab, f->ab.p, f->ab.bytes(), cudaMemcpyDeviceToHost, st));
@@ -834,7 +865,7 @@ ck_status ck_lu_export(ck_lu f, double* ab, int32_t* ipiv) {
 }
 
 ck_status ck_lu_csr_info(ck_lu f, int64_t* nnz_l, int64_t* nnz_u) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     LU(f);
     lu_build_csr(f);
     if (nnz_l) *nnz_l = f->nnz_l;
@@ -844,7 +875,7 @@ ck_status ck_lu_csr_info(ck_lu f, int64_t* nnz_l, int64_t* nnz_u) {
 
 ck_status ck_lu_export_csr(ck_lu f, int64_t* l_rp, int32_t* l_ci, double* l_va, int64_t* u_rp,
                            int32_t* u_ci, double* u_va, int64_t* row_perm) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     LU(f);
     lu_build_csr(f);
     cudaStream_t st = f->stream;
@@ -866,16 +897,16 @@ ck_status ck_lu_export_csr(ck_lu f, int64_t* l_rp, int32_t* l_ci, double* l_va, 
 }
 
 ck_status ck_lu_solve(ck_lu f, const double* b, double* x) {
-  return guarded([&] { lu_solve_host(LU(f), b, x, false); });
+  return guarded(__func__, [&] { lu_solve_host(LU(f), b, x, false); });
 }
 
 ck_status ck_lu_transpose_solve(ck_lu f, const double* b, double* x) {
-  return guarded([&] { lu_solve_host(LU(f), b, x, true); });
+  return guarded(__func__, [&] { lu_solve_host(LU(f), b, x, true); });
 }
 
 ck_status ck_session_create_inverse(ck_lu f, const ck_adam_cfg* cfg, const uint64_t* seeds,
                                     int32_t ncols, ck_session* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     auto* s = new ck_session_s();
     try {
@@ -890,7 +921,7 @@ ck_status ck_session_create_inverse(ck_lu f, const ck_adam_cfg* cfg, const uint6
 
 ck_status ck_inv_projected_adam(ck_lu f, const ck_adam_cfg* cfg, ck_norm_result* res,
                                 double* witness) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     ck_session_s s;
     uint64_t seed = cfg->seed;
@@ -903,7 +934,7 @@ ck_status ck_inv_projected_adam(ck_lu f, const ck_adam_cfg* cfg, ck_norm_result*
 
 ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restarts,
                                ck_norm_result* res, double* witness) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     LU(f);
     estimate_norm_groups(cfg, restarts, res, witness, kInvRestartGroup, [&](ck_session_s* s, const uint64_t* seeds, int R) {
@@ -917,7 +948,7 @@ ck_status ck_inv_estimate_norm(ck_lu f, const ck_adam_cfg* cfg, uint64_t restart
 // factorisation yields kappa = +inf (no error).
 ck_status ck_cond2(ck_matrix a, const ck_adam_cfg* cfg, uint64_t restarts, double pivot_tol,
                    double* kappa, ck_norm_result* fwd, ck_norm_result* inv, int32_t* has_factors) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     ck_matrix_s* m = M(a);
     if (m->nrows != m->ncols) fail(CK_ERR_DIMENSION, "cond2: matrix must be square");
@@ -953,7 +984,7 @@ extern "C" {
 
 // loss / grad of the InverseOracle (condest.hpp:112-123, 142-146) on the device.
 ck_status ck_loss_inverse(ck_lu f, const double* x, double* loss) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     ck_lu_s* F = LU(f);
     cudaStream_t st = F->stream;
     const int64_t n = F->n;
@@ -970,7 +1001,7 @@ ck_status ck_loss_inverse(ck_lu f, const double* x, double* loss) {
 }
 
 ck_status ck_grad_inverse(ck_lu f, const double* x, double* g) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     ck_lu_s* F = LU(f);
     cudaStream_t st = F->stream;
     const int64_t n = F->n;
@@ -1009,7 +1040,7 @@ extern "C" {
 ck_status ck_session_create_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg,
                                   const ck_adam_cfg* cfg, const uint64_t* seeds, int32_t ncols,
                                   ck_session* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     auto* s = new ck_session_s();
     try {
@@ -1027,7 +1058,7 @@ ck_status ck_session_create_batch(ck_matrix a, const int64_t* seg_n, int32_t nse
 ck_status ck_estimate_norm_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg,
                                  const ck_adam_cfg* cfg, const uint64_t* member_seeds,
                                  uint64_t restarts, ck_norm_result* results) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
     ck_matrix_s* m = M(a);
@@ -1062,7 +1093,7 @@ ck_status ck_estimate_norm_batch(ck_matrix a, const int64_t* seg_n, int32_t nseg
 // member per step (the sigma_min half of cond2 for an ensemble, config 5).
 ck_status ck_session_create_inverse_batch(const ck_lu* lus, int32_t nmem, const ck_adam_cfg* cfg,
                                           const uint64_t* seeds, int32_t ncols, ck_session* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     if (nmem < 1) fail(CK_ERR_INVALID_ARGUMENT, "at least one member");
     std::vector<ck_lu_s*> f((size_t)nmem);
@@ -1083,7 +1114,7 @@ ck_status ck_session_create_inverse_batch(const ck_lu* lus, int32_t nmem, const 
 ck_status ck_inv_estimate_norm_batch(const ck_lu* lus, int32_t nmem, const ck_adam_cfg* cfg,
                                      const uint64_t* member_seeds, uint64_t restarts,
                                      ck_norm_result* results) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     if (restarts == 0) fail(CK_ERR_INVALID_ARGUMENT, "estimate_norm: restarts must be >= 1");
     if (nmem < 1) fail(CK_ERR_INVALID_ARGUMENT, "at least one member");
@@ -1117,7 +1148,7 @@ ck_status ck_inv_estimate_norm_batch(const ck_lu* lus, int32_t nmem, const ck_ad
 
 // ---------------------------------------------------------------- scaling
 ck_status ck_column_norms(ck_matrix a, double* norms) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     ck_matrix_s* m = M(a);
     DBuf<double> d(std::max<int64_t>(1, m->ncols));
     matrix_norms(m, true, d.p);
@@ -1126,7 +1157,7 @@ ck_status ck_column_norms(ck_matrix a, double* norms) {
 }
 
 ck_status ck_row_norms(ck_matrix a, double* norms) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     ck_matrix_s* m = M(a);
     DBuf<double> d(std::max<int64_t>(1, m->nrows));
     matrix_norms(m, false, d.p);
@@ -1137,7 +1168,7 @@ ck_status ck_row_norms(ck_matrix a, double* norms) {
 // column_scale, sparse.hpp:271-284
 ck_status ck_column_scale(ck_matrix a, const int32_t* col_indices, const double* values,
                           double* values_out, double* norms, int64_t* zero_index) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     ck_matrix_s* m = M(a);
     if (zero_index) *zero_index = -1;
     DBuf<double> d(std::max<int64_t>(1, m->ncols));
@@ -1158,7 +1189,7 @@ ck_status ck_column_scale(ck_matrix a, const int32_t* col_indices, const double*
 ck_status ck_row_scale(ck_matrix a, const int64_t* row_offsets, const double* values,
                        double* values_out, const double* b, double* b_out, double* norms,
                        int64_t* zero_index) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     ck_matrix_s* m = M(a);
     if (zero_index) *zero_index = -1;
     DBuf<double> d(std::max<int64_t>(1, m->nrows));
@@ -1177,7 +1208,7 @@ ck_status ck_row_scale(ck_matrix a, const int64_t* row_offsets, const double* va
 }
 
 ck_status ck_unscale_solution(int64_t n, const double* y, const double* d, double* x) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (n < 0) fail(CK_ERR_INVALID_ARGUMENT, "negative length");
     int cnt = 0;
     if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0) fail(CK_ERR_NO_DEVICE, "no CUDA device");
@@ -1188,13 +1219,13 @@ ck_status ck_unscale_solution(int64_t n, const double* y, const double* d, doubl
 
 // ------------------------------------------------------ row-block partitions
 ck_status ck_dist_nccl_id(void* id128) {
-  return guarded([&] { dist_nccl_id(id128); });
+  return guarded(__func__, [&] { dist_nccl_id(id128); });
 }
 
 ck_status ck_dist_create(const ck_dist_part* parts, int32_t nparts, int32_t rank0, int32_t nranks,
                          const void* nccl_id, const ck_adam_cfg* cfg, const uint64_t* seeds,
                          int32_t ncols, ck_dist* out) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     check_cfg(cfg);
     ck_dist_s* D = dist_new();
     try {
@@ -1208,35 +1239,35 @@ ck_status ck_dist_create(const ck_dist_part* parts, int32_t nparts, int32_t rank
 }
 
 ck_status ck_dist_run(ck_dist d, uint64_t max_steps, int32_t* finished) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!d) fail(CK_ERR_INVALID_ARGUMENT, "dist handle is NULL");
     dist_run(d, max_steps, finished);
   });
 }
 
 ck_status ck_dist_time(ck_dist d, uint64_t steps, double* ms) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!d) fail(CK_ERR_INVALID_ARGUMENT, "dist handle is NULL");
     *ms = dist_time(d, steps);
   });
 }
 
 ck_status ck_dist_result(ck_dist d, int32_t col, int32_t part, ck_norm_result* res, double* witness) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!d) fail(CK_ERR_INVALID_ARGUMENT, "dist handle is NULL");
     dist_result(d, col, part, res, witness);
   });
 }
 
 ck_status ck_dist_part_info(ck_dist d, int32_t part, ck_matrix_info* info) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (!d || !info) fail(CK_ERR_INVALID_ARGUMENT, "dist handle or info is NULL");
     matrix_info(dist_part_matrix(d, part), info);
   });
 }
 
 ck_status ck_dist_free(ck_dist d) {
-  return guarded([&] {
+  return guarded(__func__, [&] {
     if (d) dist_free(d);
   });
 }

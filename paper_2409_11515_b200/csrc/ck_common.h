@@ -1,6 +1,7 @@
 // Internal definitions shared by the condkit-b200 translation units.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <cstdint>
@@ -32,6 +33,15 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
+// NVTX range for the lifetime of a scope (header-only NVTX 3: no cost without
+// an attached tool).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Phase timer for the setup paths (CK_TRACE=1): synchronises the stream and
 // prints the wall time since the previous mark to stderr.
 struct Trace {
@@ -44,6 +54,7 @@ struct Trace {
     if (on) std::fprintf(stderr, "[ck_trace] %s\n", tag);
   }
   void mark(const char* what, cudaStream_t st) {
+    nvtxMarkA(what);
     if (!on) return;
     cudaStreamSynchronize(st);
     const auto now = std::chrono::steady_clock::now();

@@ -132,3 +132,17 @@ def test_cpp_dropin_header_compiles_against_reference_types(tmp_path):
 
 def test_cpp_dropin_header_compiles_standalone(tmp_path):
     assert _build_dropin(tmp_path, False).exists()
+
+
+def test_reference_demos_build_against_b200_headers():
+    # proj/include/condkit (B200 condest.hpp / lu.hpp / error_bounds.hpp) shadows the
+    # reference's headers: the reference's demos and its unit-test call sites compile
+    # unchanged (-Wall -Wextra); the GPU half runs them (tests/test_gpu_dropin.py)
+    if not os.path.isdir("/root/reference/proj/include/condkit"):
+        pytest.skip("reference headers not present on this machine")
+    from paper_2409_11515_b200 import build
+    exes = build.build_dropin()
+    for name in ("condest_checks", "condition_estimate", "residual_vs_error"):
+        assert os.path.join(build.DROPIN, name) in exes
+    for d in build.DEMOS:
+        assert os.path.getsize(os.path.join(ROOT, "tests", "golden", f"dropin_{d}.txt")) > 0

@@ -192,12 +192,27 @@ def test_start_vector_prefetch_is_invisible():
     def fresh():
         return ck.SparseMatrix(lap.nrows, lap.ncols, lap.row_offsets, lap.col_indices, lap.values)
 
+    import ctypes as C
+    lib = _lib.load()
+
+    def stats():
+        t, d = C.c_uint64(), C.c_uint64()
+        _lib.check(lib.ck_start_vector_prefetch_stats(C.byref(t), C.byref(d)), "stats")
+        return t.value, d.value
+
+    t0, d0 = stats()
     e1 = ck.norm2(fresh(), c)  # prefetched
+    assert stats() == (t0 + 1, d0)  # the session took the prefetched vector
     a2 = fresh()
     a2.device()
     e2 = ck.norm2(a2, c)  # drawn in the session
-    _lib.check(_lib.load().ck_start_vector_prefetch(10, lap.ncols), "prefetch")
-    e3 = ck.norm2(a2, c)  # stale slot (seed 10): ignored
+    assert stats() == (t0 + 1, d0)
+    _lib.check(lib.ck_start_vector_prefetch(10, lap.ncols), "prefetch")
+    e3 = ck.norm2(a2, c)  # stale slot (seed 10): dropped, drawn in the session
+    assert stats() == (t0 + 1, d0 + 1)
+    _lib.check(lib.ck_start_vector_prefetch(10, lap.ncols), "prefetch")
+    _lib.check(lib.ck_start_vector_prefetch_cancel(), "cancel")
+    assert stats() == (t0 + 1, d0 + 2)
     for e in (e2, e3):
         assert e.value == e1.value and e.iterations == e1.iterations
         assert np.array_equal(e.witness, e1.witness)
