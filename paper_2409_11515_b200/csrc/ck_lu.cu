@@ -120,8 +120,11 @@ __device__ __forceinline__ void init_key_slots(const BandView& b, int64_t c0, in
   }
 }
 
-__global__ void k_key_init(const BandView* __restrict__ bs, int64_t c0, int64_t c1) {
-  init_key_slots(bs[blockIdx.y], c0, c1, blockIdx.x, gridDim.x);
+// Key slots of the columns the first panel can reach, [0, kv + 32) of each member
+// (its own kv: the window of a narrower member of a batch is shorter).
+__global__ void k_key_init(const BandView* __restrict__ bs) {
+  const BandView& b = bs[blockIdx.y];
+  init_key_slots(b, 0, b.kv + kLUBlock, blockIdx.x, gridDim.x);
 }
 
 // Fill stamp of step s in column k for a multiplier of rank `rank` (< kl + 1).
@@ -725,7 +728,7 @@ static void lu_panels(ck_lu_s* const* fs, int S, double pivot_tol, cudaStream_t 
   // key slots of the first panel's reach (later ones: k_gbtrf_update)
   {
     const unsigned gx = (unsigned)std::min<int64_t>(148, std::max<int64_t>(1, ceil_div((kvmax + 2 * kLUBlock) * (2 * klmax + kvmax + 1), 4096)));
-    k_key_init<<<dim3(gx, (unsigned)S), 256, 0, st>>>(db.p, 0, kvmax + kLUBlock);
+    k_key_init<<<dim3(gx, (unsigned)S), 256, 0, st>>>(db.p);
   }
   int sort_words = 1;
   while (sort_words < klmax + 1) sort_words <<= 1;

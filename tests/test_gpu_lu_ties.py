@@ -144,3 +144,28 @@ def test_band_limit_reported_before_allocation():
     a = csr(n, [(i, i, 1.0) for i in range(n)] + [(n - 1, 0, 1.0), (0, n - 1, 1.0)])
     with pytest.raises(ck.CondkitError, match="band too wide"):
         ck.lu_factorize(a)
+
+
+def test_batched_factorisation_matches_single(port):
+    # ck_lu_factorize_batch with members of different band widths (each member's key
+    # window is its own): factors identical to separate factorisations and the oracle
+    from paper_2409_11515_b200 import batch, configs
+    rng = np.random.default_rng(21)
+    mem = [configs.ensemble_member(0, 1, n=1000, bw=64), configs.ensemble_member(1, 1, n=513, bw=40),
+           configs.ensemble_member(2, 1, n=700, bw=200)]
+    for n in (40, 90):
+        ent = {(i, int(rng.integers(n))): float(rng.choice([-2, -1, 1, 2])) for i in range(n)}
+        for i in range(n):
+            ent[(i, i)] = float(rng.choice([-2, -1, 1, 2]))
+            for j in np.nonzero(rng.random(n) < 0.08)[0]:
+                ent[(i, int(j))] = float(rng.choice([-2, -1, 1, 2]))
+        mem.append(csr(n, [(r, c, v) for (r, c), v in ent.items()]))
+    facs = batch.lu_factorize_many(mem, 1e-14)
+    for m, f in zip(mem, facs):
+        try:
+            rf = port.lu_factorize(m, 1e-14)
+        except Exception:  # noqa: BLE001
+            assert isinstance(f, (ck.StructurallySingular, ck.NumericallySingular))
+            continue
+        assert_same_factors(f, rf)
+        assert_same_factors(ck.lu_factorize(m, 1e-14), rf)
