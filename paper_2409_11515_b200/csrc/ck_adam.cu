@@ -59,6 +59,22 @@ struct Occ {
   static constexpr int transpose = 4;
 };
 
+// Entries per matrix chunk of the R-column kernels (their values and columns
+// are loaded before any use); measured per R.
+template <int R>
+struct Tune {
+  static constexpr int apply_u = R == 1 ? 8 : 4;
+  static constexpr int transpose_u = R <= 2 ? 8 : 4;
+};
+
+// The window kernels (banded ensembles) hold no gathered operands in
+// registers, so their chunks are wider (config 5, scripts/ab_win.sh).
+template <int R>
+struct WinTune {
+  static constexpr int apply_u = R == 4 ? 16 : 8;
+  static constexpr int apply_occ = R == 1 ? 4 : R == 4 ? 2 : 3;
+};
+
 // Work assignment of CTA `unit`. One operator (S == 1): the tiles are dealt
 // round-robin over the grid, so at any moment the resident CTAs sweep one
 // contiguous window of the matrix and the stencil neighbours of the gathered
@@ -88,13 +104,39 @@ __device__ __forceinline__ double xtilde(double2 p, double rad) {
   return __dsub_rn(p.x, __dsub_rn(p.y, __dmul_rn(rad, p.x)));
 }
 
+// Lockstep buffer rotation. Every active column of an operator reads its
+// (x, delta) pairs from the same iterate buffer (cur) and writes the next pairs
+// to the same buffer (nxt), so a row's R pairs are one contiguous R*16-byte
+// load. A column's best iterate stays behind in whatever buffer it was written
+// to (ColState::best, per column); with R + 2 buffers there is always one that
+// is neither cur nor any column's best.
+template <int R>
+__device__ __forceinline__ int shared_cur(const ColState* sts) {
+  int cur = 0;
+  for (int r = 0; r < R; ++r) {
+    const int ph = sts[r].phase;
+    if (ph == PH_PRO || ph == PH_APPLY || ph == PH_GRAD) cur = sts[r].cur;
+  }
+  return cur;
+}
+
+template <int R>
+__device__ __forceinline__ int pick_shared_nxt(const ColState* sts, int cur, int nbuf) {
+  unsigned used = 1u << cur;
+  for (int r = 0; r < R; ++r) used |= 1u << sts[r].best;
+  for (int b = 0; b < nbuf; ++b)
+    if (!((used >> b) & 1u)) return b;
+  return (cur + 1) % nbuf;  // unreachable with nbuf = R + 2
+}
+
 // Control step after the apply sweep (condest.hpp:251-275 via control_apply)
 // from the global scalars res[r] = {||x~||, ||y'||, x.delta, ||delta||}; one
 // thread. Shared by the fused kernel and the partition combine kernel.
 template <int R, bool OBS>
 __device__ __forceinline__ void control_tail_apply(ColState* sts, Header* hdr, const Params& prm,
-                                                   const double (*res)[4]) {
+                                                   const double (*res)[4], int nbuf) {
   int needT = 0, nwait = 0, ndone = 0;
+  const int nxt = pick_shared_nxt<R>(sts, shared_cur<R>(sts), nbuf);
   for (int r = 0; r < R; ++r) {
     ColState* s = sts + r;
     const int ph = s->phase;
@@ -103,7 +145,7 @@ __device__ __forceinline__ void control_tail_apply(ColState* sts, Header* hdr, c
         s->obs_xd = res[r][2];
         s->obs_dn = res[r][3];
       }
-      control_apply(s, &prm, res[r][0], res[r][1]);
+      control_apply(s, &prm, res[r][0], res[r][1], nxt);
     }
     needT |= s->phase == PH_GRAD;
     nwait += s->phase == PH_WAIT;
@@ -116,7 +158,8 @@ __device__ __forceinline__ void control_tail_apply(ColState* sts, Header* hdr, c
 }
 
 // After the transpose sweep: publish r = x.delta (condest.hpp:231) and move
-// every gradient column on to its apply half; one thread.
+// every gradient column on to its apply half (and to the buffer the sweep just
+// wrote); one thread.
 template <int R>
 __device__ __forceinline__ void control_tail_transpose(ColState* sts, Header* hdr, const double* rad) {
   int needA = 0;
@@ -124,10 +167,8 @@ __device__ __forceinline__ void control_tail_transpose(ColState* sts, Header* hd
     ColState* s = sts + r;
     if (s->phase == PH_GRAD) {
       s->rad = rad[r];
-      if (s->mat) {
-        s->cur = s->nxt;
-        s->pend = 0;
-      }
+      s->cur = s->nxt;
+      s->pend = 0;
       s->phase = PH_APPLY;
     }
     needA |= s->phase == PH_APPLY;
@@ -136,8 +177,8 @@ __device__ __forceinline__ void control_tail_transpose(ColState* sts, Header* hd
   hdr->needT = 0;
 }
 
-template <int R, bool OBS, bool NW, int U = (R == 1 ? 8 : 4)>
-__global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_constant__ LoopArgs a) {
+template <int R, bool OBS, bool NW, bool WIN = false, int U = Tune<R>::apply_u, int OCC = Occ<R>::apply>
+__global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ LoopArgs a) {
   int seg, tile0, tend, stride, u0, u1;
   unit_range(a, blockIdx.x, a.tiles_A, seg, tile0, tend, stride, u0, u1);
   Header* hdr = a.hdr + seg;
@@ -149,7 +190,6 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
 
   bool act[R], pro[R];
   double rad[R];
-  const double2* xc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int ph = sts[r].phase;
@@ -157,7 +197,35 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
     pro[r] = ph == PH_PRO;
     // prologue: delta is zero, so x~ = x exactly (x - (0 - 0 x) = x)
     rad[r] = pro[r] ? 0.0 : sts[r].rad;
-    xc[r] = a.PX + (int64_t)sts[r].cur * a.nc_pad * R + r;  // row i at xc[r][i * R]
+  }
+  // every active column reads the same buffer: row i's pairs at xb[i * R + r]
+  const double2* xb = a.PX + (int64_t)shared_cur<R>(sts) * a.nc_pad * R;
+  // WIN (banded members, a unit's tiles are consecutive): x~ of the tiles t-1,
+  // t, t+1 that tile t's entries reference sits in a four-tile shared-memory
+  // ring, each element computed once and staged one tile ahead; the gathers
+  // are shared-memory reads.
+  __shared__ double s_win[WIN ? 4 * kTile * R : 1];
+  int m0 = 0, m1 = 0;
+  auto win_load = [&](int q, double2* pr) {  // row q * kTile + tid of the live buffer
+    const bool in = q >= m0 && q < m1;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      pr[r] = in ? xb[((int64_t)q * kTile + threadIdx.x) * R + r] : make_double2(0.0, 0.0);
+  };
+  auto win_store = [&](int q, const double2* pr) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      s_win[((q & 3) * kTile + threadIdx.x) * R + r] = act[r] ? xtilde(pr[r], rad[r]) : 0.0;
+  };
+  if (WIN) {
+    m0 = a.seg_t0[seg];
+    m1 = a.seg_t0[seg + 1];
+    double2 pr[R];
+    for (int q = tile0 - 1; q <= tile0 + 1; ++q) {
+      win_load(q, pr);
+      win_store(q, pr);
+    }
+    __syncthreads();
   }
   DD dd[R];
   ES es[R], dn[R];
@@ -190,11 +258,19 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
       L = a.A.len[inext];
       cb = slice_cbase<NW>(a.A, inext >> 5);
     }
-    if (i < a.nc) {  // own column-space element: ||x~||^2 (and observer stats)
+    double2 ahead[R];
+    if (WIN && tile + 1 < tend) win_load(tile + 2, ahead);  // needed by the next tile
+    if (WIN) {  // own column-space element: ||x~||^2 from the staged x~
+      if (i < a.nc) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (act[r]) dd_add_sq(dd[r], s_win[((tile & 3) * kTile + threadIdx.x) * R + r]);
+      }
+    } else if (i < a.nc) {  // own column-space element: ||x~||^2 (and observer stats)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (!act[r]) continue;
-        const double2 p = xc[r][i * R];
+        const double2 p = __ldg(xb + i * R + r);
         if (OBS && !pro[r]) {
           const double dp = __dsub_rn(p.y, __dmul_rn(rad[r], p.x));
           xd[r] = __fma_rn(p.x, dp, xd[r]);
@@ -211,15 +287,27 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
         int c[U];
         double v[U];
         load_chunk<U, NW>(a.A, base, cbc, j0, w, c, v);
+        if (WIN) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (!act[r]) continue;
-          double2 g[U];
+          for (int u = 0; u < U; ++u) {
+            const double* xw = s_win + (c[u] & (4 * kTile - 1)) * R;
+            if (j0 + u < Lc) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) g[u] = __ldg(xc[r] + (int64_t)c[u] * R);
+              for (int r = 0; r < R; ++r)
+                if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xw[r]));
+            }
+          }
+        } else {
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xtilde(g[u], rad[r])));
+          for (int r = 0; r < R; ++r) {
+            if (!act[r]) continue;
+            double2 g[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = __ldg(xb + (int64_t)c[u] * R + r);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xtilde(g[u], rad[r])));
+          }
         }
       }
 #pragma unroll
@@ -228,6 +316,11 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
         a.y[i * R + r] = acc[r];
         es_add(es[r], acc[r]);
       }
+    }
+    if (WIN) {
+      // slot (tile + 2) & 3 held tile - 2, last read before the previous barrier
+      if (tile + 1 < tend) win_store(tile + 2, ahead);
+      __syncthreads();
     }
   }
   // Per-CTA partials.
@@ -298,12 +391,11 @@ __global__ void __launch_bounds__(kTile, Occ<R>::apply) k_apply(const __grid_con
       }
     }
   }
-  if (threadIdx.x == 0 && !a.dist) control_tail_apply<R, OBS>(sts, hdr, a.prm, s_res);
+  if (threadIdx.x == 0 && !a.dist) control_tail_apply<R, OBS>(sts, hdr, a.prm, s_res, a.nbuf);
 }
 
-template <int R, bool NW, int U = (R <= 2 ? 8 : 4)>
-__global__ void __launch_bounds__(kTile, Occ<R>::transpose)
-    k_transpose(const __grid_constant__ LoopArgs a) {
+template <int R, bool NW, bool WIN = false, int U = Tune<R>::transpose_u, int OCC = Occ<R>::transpose>
+__global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant__ LoopArgs a) {
   int seg, tile0, tend, stride, u0, u1;
   unit_range(a, blockIdx.x, a.tiles_T, seg, tile0, tend, stride, u0, u1);
   Header* hdr = a.hdr + seg;
@@ -314,8 +406,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
   const Params& p = a.prm;
   bool act[R], mat[R];
   double rad[R], ndiv[R], ix2[R], iy2[R], mc[R], vc[R];
-  const double2* xc[R];
-  double2* xn_out[R];
+  int nxt = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const ColState& s = sts[r];
@@ -327,14 +418,38 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
     iy2[r] = s.inv_y2;
     mc[r] = s.mc;
     vc[r] = s.vc;
-    xc[r] = a.PX + (int64_t)s.cur * a.nc_pad * R + r;
-    // prologue (mat = 0): x stays where it is and only delta is rewritten
-    xn_out[r] = a.PX + (int64_t)(mat[r] ? s.nxt : s.cur) * a.nc_pad * R + r;
+    if (act[r]) nxt = s.nxt;
   }
+  // gradient columns read buffer cur and write buffer nxt in lockstep (a
+  // prologue column, mat = 0, carries its x over unchanged)
+  const double2* xb = a.PX + (int64_t)shared_cur<R>(sts) * a.nc_pad * R;
+  double2* xo = a.PX + (int64_t)nxt * a.nc_pad * R;
   const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
   double dot[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) dot[r] = 0.0;
+  // WIN: y' of the row tiles t-1, t, t+1 in a four-tile shared-memory ring (see k_apply)
+  __shared__ double s_win[WIN ? 4 * kTile * R : 1];
+  int m0 = 0, m1 = 0;
+  auto win_load = [&](int q, double* yr) {
+    const bool in = q >= m0 && q < m1;
+#pragma unroll
+    for (int r = 0; r < R; ++r) yr[r] = in ? a.y[((int64_t)q * kTile + threadIdx.x) * R + r] : 0.0;
+  };
+  auto win_store = [&](int q, const double* yr) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) s_win[((q & 3) * kTile + threadIdx.x) * R + r] = yr[r];
+  };
+  if (WIN) {
+    m0 = a.seg_t0[seg];
+    m1 = a.seg_t0[seg + 1];
+    double yr[R];
+    for (int q = tile0 - 1; q <= tile0 + 1; ++q) {
+      win_load(q, yr);
+      win_store(q, yr);
+    }
+    __syncthreads();
+  }
   const int64_t jstep = (int64_t)stride * kTile;
   int64_t j = (int64_t)tile0 * kTile + threadIdx.x;
   int64_t sp0 = 0, sp1 = 0;
@@ -356,6 +471,8 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
       L = a.AT.len[jn];
       cb = slice_cbase<NW>(a.AT, jn >> 5);
     }
+    double ahead[R];
+    if (WIN && tile + 1 < tend) win_load(tile + 2, ahead);
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
@@ -363,15 +480,27 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
       int c[U];
       double v[U];
       load_chunk<U, NW>(a.AT, base, cbc, j0, w, c, v);
+      if (WIN) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!act[r]) continue;
-        double yg[U];
+        for (int u = 0; u < U; ++u) {
+          const double* yw = s_win + (c[u] & (4 * kTile - 1)) * R;
+          if (j0 + u < Lc) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) yg[u] = __ldg(a.y + (int64_t)c[u] * R + r);
+            for (int r = 0; r < R; ++r)
+              if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], yw[r]));
+          }
+        }
+      } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], yg[u]));
+        for (int r = 0; r < R; ++r) {
+          if (!act[r]) continue;
+          double yg[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) yg[u] = __ldg(a.y + (int64_t)c[u] * R + r);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], yg[u]));
+        }
       }
     }
     if (j < a.nc) {
@@ -379,7 +508,7 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
       for (int r = 0; r < R; ++r) {
         if (!act[r]) continue;
         const int64_t e = j * R + r;
-        const double2 px = xc[r][j * R];
+        const double2 px = xb[e];
         const double xn = mat[r] ? __ddiv_rn(xtilde(px, rad[r]), ndiv[r]) : px.x;  // :240-247
         const double z = __ddiv_rn(acc[r], ndiv[r]);                               // A^T A x_{t+1}
         const double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(z, iy2[r]));  // :105
@@ -389,9 +518,13 @@ __global__ void __launch_bounds__(kTile, Occ<R>::transpose)
         const double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
                                    __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));  // :228
         a.MV[e] = make_double2(mm, vv);
-        xn_out[r][j * R] = make_double2(xn, d);
+        xo[e] = make_double2(xn, d);
         dot[r] = __fma_rn(xn, d, dot[r]);
       }
+    }
+    if (WIN) {
+      if (tile + 1 < tend) win_store(tile + 2, ahead);
+      __syncthreads();
     }
   }
 #pragma unroll
@@ -437,7 +570,7 @@ __global__ void k_dist_control_apply(LoopArgs a, const double* __restrict__ g, i
     res[r][1] = es_norm(e);
     res[r][2] = res[r][3] = 0.0;
   }
-  control_tail_apply<R, false>(a.st, a.hdr, a.prm, res);
+  control_tail_apply<R, false>(a.st, a.hdr, a.prm, res, a.nbuf);
 }
 
 template <int R>
@@ -469,14 +602,46 @@ __global__ void k_store_x(int64_t n, int R, const double* __restrict__ x, double
   if (j < n) px[j * R] = make_double2(x[j], 0.0);
 }
 
+// One column's pairs from one buffer to another (stride R).
+__global__ void k_copy_col(int64_t n, int R, const double2* __restrict__ src, double2* dst) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) dst[j * R] = src[j * R];
+}
+
 __global__ void k_zero_moments(int64_t n, int R, int col, double2* mv) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < n) mv[j * R + col] = make_double2(0.0, 0.0);
 }
 
+// Largest distance, in 256-row tiles, between a stored entry's row and column
+// positions (the window kernels need <= 1).
+__global__ void k_tile_reach(SellView A, int64_t nrows_pad, int* out) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nrows_pad) return;
+  const int64_t base = sell_rowbase(A.sp[p >> 5], p);
+  const int L = A.len[p];
+  int reach = 0;
+  for (int j = 0; j < L; ++j) {
+    const int col = sell_col(A, p >> 5, sell_at(base, j));
+    reach = max(reach, abs((col >> 8) - (int)(p >> 8)));
+  }
+  if (reach > 0) atomicMax(out, reach);
+}
+
 // ---------------------------------------------------------------- host side
 
 static unsigned grid256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
+
+static int tile_reach(const Sell& m, cudaStream_t st) {
+  static_assert(kTile == 256, "k_tile_reach shifts by 8");
+  DBuf<int> d(1);
+  CK_CUDA(cudaMemsetAsync(d.p, 0, sizeof(int), st));
+  k_tile_reach<<<grid256(m.nrows_pad), 256, 0, st>>>(view(m), m.nrows_pad, d.p);
+  int h = 0;
+  CK_CUDA(cudaMemcpyAsync(&h, d.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
 
 template <int R>
 static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
@@ -486,6 +651,11 @@ static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
       k_apply<R, true, true><<<s->args.units_A, kTile, 0, st>>>(s->args);
     else
       k_apply<R, true, false><<<s->args.units_A, kTile, 0, st>>>(s->args);
+  } else if (s->args.win) {
+    if (nw)
+      k_apply<R, false, true, true, WinTune<R>::apply_u, WinTune<R>::apply_occ><<<s->args.units_A, kTile, 0, st>>>(s->args);
+    else
+      k_apply<R, false, false, true, WinTune<R>::apply_u, WinTune<R>::apply_occ><<<s->args.units_A, kTile, 0, st>>>(s->args);
   } else {
     if (nw)
       k_apply<R, false, true><<<s->args.units_A, kTile, 0, st>>>(s->args);
@@ -496,6 +666,13 @@ static void launch_apply_r(const ck_session_s* s, cudaStream_t st) {
 
 template <int R>
 static void launch_transpose_r(const ck_session_s* s, cudaStream_t st) {
+  if (s->args.win) {
+    if (s->A->at.narrow)
+      k_transpose<R, true, true><<<s->args.units_T, kTile, 0, st>>>(s->args);
+    else
+      k_transpose<R, false, true><<<s->args.units_T, kTile, 0, st>>>(s->args);
+    return;
+  }
   if (s->A->at.narrow)
     k_transpose<R, true><<<s->args.units_T, kTile, 0, st>>>(s->args);
   else
@@ -710,7 +887,27 @@ void service_restarts(ck_session_s* s) {
       ColState& cs = s->h_st[k];
       if (cs.phase != PH_WAIT) continue;
       draw_start(s, k, g, s->hx.data());
-      const int b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
+      int b;
+      if (s->kind == 1) {  // inverse loop: every column rotates its own three buffers
+        b = cs.cur != cs.best ? cs.cur : (cs.best + 1) % 3;
+      } else {
+        // explicit sweeps: the operator's columns share their live buffer. Join
+        // the running columns there; if this column's x_min sits in that buffer,
+        // move it to another one first (only this column's slots are touched).
+        b = cs.cur;
+        for (int c2 = 0; c2 < s->R; ++c2) {
+          const int ph = s->h_st[g * s->R + c2].phase;
+          if (c2 != c && (ph == PH_PRO || ph == PH_APPLY || ph == PH_GRAD)) b = s->h_st[g * s->R + c2].cur;
+        }
+        if (b == cs.best) {
+          const int f = (b + 1) % s->args.nbuf;
+          const int64_t off = s->seg_off[g], pad = s->seg_pad[g];
+          k_copy_col<<<grid256(pad), 256, 0, s->stream>>>(pad, s->R, col_buf(s, cs.best, c) + off * s->R,
+                                                         col_buf(s, f, c) + off * s->R);
+          CK_CUDA(cudaGetLastError());
+          cs.best = f;
+        }
+      }
       load_start(s, g, c, b, s->hx.data());
       cs.cur = b;
       cs.b1p = 1.0;
@@ -883,13 +1080,16 @@ void session_setup_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* 
   if (S == 1) {
     a.units_A = (int)std::min<int64_t>(a.tiles_A, 148 * occ_apply(R));
     a.units_T = (int)std::min<int64_t>(a.tiles_T, 148 * occ_transpose(R));
-    a.unit_seg = a.unit_t0 = a.unit_t1 = a.seg_u0 = nullptr;
+    a.unit_seg = a.unit_t0 = a.unit_t1 = a.seg_u0 = a.seg_t0 = nullptr;
+    a.win = 0;
   } else {
     // members are tile-aligned; each unit takes up to 32 consecutive tiles of one member
-    std::vector<int32_t> useg, ut0, ut1, su0(S + 1, 0);
+    std::vector<int32_t> useg, ut0, ut1, su0(S + 1, 0), st0(S + 1, 0);
     for (int g = 0; g < S; ++g) {
       const int t0 = (int)(s->seg_off[g] / kTile), nt = (int)(s->seg_pad[g] / kTile);
       su0[g] = (int)useg.size();
+      st0[g] = t0;
+      st0[g + 1] = t0 + nt;
       for (int t = 0; t < nt; t += 32) {
         useg.push_back(g);
         ut0.push_back(t0 + t);
@@ -898,7 +1098,7 @@ void session_setup_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* 
     }
     su0[S] = (int)useg.size();
     a.units_A = a.units_T = (int)useg.size();
-    s->units.alloc(3 * (int64_t)useg.size() + S + 1);
+    s->units.alloc(3 * (int64_t)useg.size() + 2 * (S + 1));
     int32_t* d = s->units.p;
     CK_CUDA(cudaMemcpy(d, useg.data(), sizeof(int32_t) * useg.size(), cudaMemcpyHostToDevice));
     CK_CUDA(cudaMemcpy(d + useg.size(), ut0.data(), sizeof(int32_t) * useg.size(), cudaMemcpyHostToDevice));
@@ -907,13 +1107,19 @@ void session_setup_explicit(ck_session_s* s, ck_matrix_s* A, const ck_adam_cfg* 
     a.unit_seg = d;
     a.unit_t0 = d + useg.size();
     a.unit_t1 = d + 2 * useg.size();
+    CK_CUDA(cudaMemcpy(d + 3 * useg.size() + S + 1, st0.data(), sizeof(int32_t) * (S + 1), cudaMemcpyHostToDevice));
     a.seg_u0 = d + 3 * useg.size();
+    a.seg_t0 = a.seg_u0 + S + 1;
+    // banded members: gather from the sliding shared-memory window (CK_NO_WINDOW=1: A/B)
+    a.win = !std::getenv("CK_NO_WINDOW") && tile_reach(A->a, s->stream) <= 1 &&
+            tile_reach(A->at, s->stream) <= 1;
   }
   s->partA.alloc((int64_t)a.units_A * R * kPA);
   s->partT.alloc((int64_t)a.units_T * R * kPT);
   const int64_t yw = std::max(a.nr_pad, a.nc_pad) * R;
   a.prm = s->prm;
-  s->PX.alloc(3 * R * s->npad);
+  a.nbuf = R + 2;  // lockstep rotation: cur, nxt and one best per column
+  s->PX.alloc((int64_t)a.nbuf * R * s->npad);
   s->MV.alloc(s->npad * R);
   s->y.alloc(yw);
   s->st.alloc((int64_t)S * R);

@@ -34,7 +34,12 @@ __device__ __forceinline__ void begin_iteration(ColState& s, const Params& p) {
 }
 
 // Control step after k_apply's reductions (thread 0 of the last CTA).
-static __device__ __noinline__ void control_apply(ColState* sp, const Params* pp, double N, double yn) {
+// nxt_shared >= 0: the iterate buffer every active column of the operator moves
+// to in this step (explicit sweeps: the columns rotate their (x, delta) buffers
+// in lockstep, so one wide load gathers all of them); < 0: the column picks its
+// own free buffer (inverse loop, three buffers per column).
+static __device__ __noinline__ void control_apply(ColState* sp, const Params* pp, double N, double yn,
+                                                  int nxt_shared) {
   ColState& s = *sp;
   const Params& p = *pp;
   s.xnorm = N;
@@ -51,6 +56,7 @@ static __device__ __noinline__ void control_apply(ColState* sp, const Params* pp
     s.inv_y2 = 1.0 / (yn * yn);
     s.ndiv = 1.0;
     s.mat = 0;
+    if (nxt_shared >= 0) s.nxt = nxt_shared;
     s.phase = PH_GRAD;
     return;
   }
@@ -70,7 +76,7 @@ static __device__ __noinline__ void control_apply(ColState* sp, const Params* pp
   s.n_loss += 1;
   bool improved = !isfinite(s.loss_min) || s.loss_min - loss > p.rel_tol * fabs(s.loss_min);
   s.since = improved ? 0 : s.since + 1;
-  s.nxt = pick_free(s.cur, s.best);
+  s.nxt = nxt_shared >= 0 ? nxt_shared : pick_free(s.cur, s.best);
   s.ndiv = N;
   if (loss < s.loss_min) {
     s.loss_min = loss;

@@ -110,8 +110,8 @@ __global__ void k_unpack_x(int64_t n, int R, const int32_t* __restrict__ pos, co
 }
 
 // Pack side, before the transpose control step runs: the buffer that step
-// makes live (control_tail_transpose: a gradient column whose x was
-// materialised moves on to nxt; every other column keeps cur).
+// makes live (control_tail_transpose: a gradient column moves on to nxt;
+// every other column keeps cur).
 __global__ void k_pack_x_next(int64_t n, int R, const int32_t* __restrict__ pos,
                               const double2* __restrict__ px, int64_t nc_pad,
                               const ColState* __restrict__ st, double2* buf) {
@@ -119,7 +119,7 @@ __global__ void k_pack_x_next(int64_t n, int R, const int32_t* __restrict__ pos,
   if (k >= n * R) return;
   const int r = (int)(k % R);
   const ColState& c = st[r];
-  const int b = (c.phase == PH_GRAD && c.mat) ? c.nxt : c.cur;
+  const int b = c.phase == PH_GRAD ? c.nxt : c.cur;
   buf[k] = px[((int64_t)b * nc_pad + pos[k / R]) * R + r];
 }
 

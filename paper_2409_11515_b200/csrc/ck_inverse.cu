@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
             s->obs_xd = s_res[r][2];
             s->obs_dn = s_res[r][3];
           }
-          control_apply(s, &a.prm, s_res[r][0], s_res[r][1]);
+          control_apply(s, &a.prm, s_res[r][0], s_res[r][1], -1);
         }
       }
     }

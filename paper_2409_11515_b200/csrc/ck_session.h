@@ -42,7 +42,8 @@ struct LoopArgs {
   int64_t nr, nc, nr_pad, nc_pad;
   int tiles_A, tpu_A, units_A;
   int tiles_T, tpu_T, units_T;
-  double2* PX;  // [3][nc_pad][R] (x, delta) pairs; three rotating iterate buffers
+  double2* PX;  // [nbuf][nc_pad][R] (x, delta) pairs; nbuf = R + 2 rotating iterate buffers
+  int nbuf;
   double2* MV;  // [nc_pad][R]    (m, v) Adam moments
   double* y;    // [nr_pad][R]    A x~
   double* partA;
@@ -56,6 +57,10 @@ struct LoopArgs {
   const int32_t* unit_t0;
   const int32_t* unit_t1;
   const int32_t* seg_u0;  // [S + 1]
+  const int32_t* seg_t0;  // [S + 1] first tile of each member
+  // every entry's column lies in the tile before, of, or after its row (A and
+  // A^T, banded members): the sweeps gather from a sliding shared-memory window
+  int win;
   // row-block partition (ck_dist.cu): the last CTA publishes this rank's
   // merged partials in rank_part instead of running the control step
   int dist;

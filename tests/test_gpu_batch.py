@@ -137,3 +137,31 @@ def test_auto_wave_fills_the_device(port):
     want = batch.cond2_batch(mem, M.cfg(alpha=1e-2, max_iter=100, patience=100), restarts=2, wave=1)
     for g, h in zip(got, want):
         assert g.kappa == h.kappa
+
+
+def test_window_sweeps_match_gathers_bitwise(port, monkeypatch):
+    """Banded ensembles gather x~ / y' from a sliding shared-memory window (every
+    column within one 256-row tile of its row); same operands, same order: the
+    results are those of the global-memory gathers, bit for bit. A member with a
+    far entry switches the whole batch to the gathers."""
+    mem = [configs.ensemble_member(i, 1, n=n, bw=bw) for i, (n, bw) in
+           enumerate([(3000, 200), (1500, 255), (700, 30), (2049, 128)])]
+    cfg = M.cfg(alpha=1e-2, max_iter=150, patience=150)
+    seeds = batch.member_seeds(len(mem))
+    for restarts in (1, 2, 3, 4):
+        win = batch.estimate_norm_batch(mem, cfg, restarts=restarts, seeds=seeds)
+        monkeypatch.setenv("CK_NO_WINDOW", "1")
+        ref = batch.estimate_norm_batch(mem, cfg, restarts=restarts, seeds=seeds)
+        monkeypatch.delenv("CK_NO_WINDOW")
+        for w, r in zip(win, ref):
+            assert w.value == r.value and w.iterations == r.iterations
+            assert np.array_equal(w.witness, r.witness)
+    # reach > 1: entry (0, 900) in the first member
+    far = mem[0]
+    rp, ci, va = far.row_offsets.copy(), list(far.col_indices), list(far.values)
+    trip = [(i, ci[k], va[k]) for i in range(far.nrows) for k in range(rp[i], rp[i + 1])]
+    trip.append((0, 900, 0.5))
+    far2 = ck.SparseMatrix.from_triplets(far.nrows, far.ncols, trip)
+    got = batch.estimate_norm_batch([far2, mem[1]], cfg, restarts=2, seeds=seeds[:2])
+    alone = ck.estimate_norm(ck.ExplicitOracle(far2), M.cfg(alpha=1e-2, max_iter=150, patience=150, seed=seeds[0]), 2)
+    assert got[0].value == pytest.approx(alone.value, rel=1e-12)
