@@ -357,9 +357,9 @@ def run_partition(args, rank, world, local, dist, barrier, allmax):
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": None,
-            # per iteration: k_apply, k_transpose, two control steps, two halo packs,
-            # two halo unpacks (the NCCL kernels are the library's)
-            "gpu_launches": args.steps * 8,
+            # per iteration: k_apply, k_transpose, two pack kernels (halo + partials), two
+            # combine kernels (control step + halo scatter); the NCCL kernels are the library's
+            "gpu_launches": args.steps * 6,
             "setup_s": {"generate": t_gen, "partition": t_part, "upload_and_build": t_up},
         }
         print(json.dumps(line), flush=True)
@@ -376,6 +376,10 @@ def run_ours(args):
     _lib.ensure_device()
     dist = None
     if world > 1:
+        # NCCL's own init lines (ranks, devices, transport) on stderr: the evidence that
+        # the N ranks really are N processes on N GPUs over NVLink
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch  # noqa: PLC0415
         import torch.distributed as td  # noqa: PLC0415
         torch.cuda.set_device(local)

@@ -231,6 +231,14 @@ ck_status ck_lu_export_csr(ck_lu f, int64_t* l_rp, int32_t* l_ci, double* l_va, 
 /* lu_solve (lu.hpp:180-202): x = A^-1 b; lu_transpose_solve (lu.hpp:207-227): x = A^-T b. */
 ck_status ck_lu_solve(ck_lu f, const double* b, double* x);
 ck_status ck_lu_transpose_solve(ck_lu f, const double* b, double* x);
+/* The dense-block sweeps the InverseOracle loop runs on narrow bands
+ * (max(kl, kl + ku) <= 192; same solves as ck_lu_solve / ck_lu_transpose_solve,
+ * lu.hpp:180-227, with the 32 x 32 head triangles of every block inverted once
+ * per factorisation). available = 0: the band is too wide or a head's growth
+ * factor || |Hinv| |H| || exceeds 1e4, and the loop keeps the substitution
+ * sweeps; ck_lu_dense_solve then returns CK_ERR_UNSUPPORTED. */
+ck_status ck_lu_dense_info(ck_lu f, int32_t* available, double* growth);
+ck_status ck_lu_dense_solve(ck_lu f, int32_t transpose, const double* b, double* x);
 /* InverseOracle::loss / grad_inverse (condest.hpp:112-123, 142-146) on the device. */
 ck_status ck_loss_inverse(ck_lu f, const double* x, double* loss);
 ck_status ck_grad_inverse(ck_lu f, const double* x, double* g);

@@ -126,7 +126,8 @@ __device__ __forceinline__ int pick_shared_nxt(const ColState* sts, int cur, int
   for (int r = 0; r < R; ++r) used |= 1u << sts[r].best;
   for (int b = 0; b < nbuf; ++b)
     if (!((used >> b) & 1u)) return b;
-  return (cur + 1) % nbuf;  // unreachable with nbuf = R + 2
+  CK_DASSERT(false);  // unreachable with nbuf = R + 2
+  return (cur + 1) % nbuf;
 }
 
 // Control step after the apply sweep (condest.hpp:251-275 via control_apply)
@@ -291,6 +292,8 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const double* xw = s_win + (c[u] & (4 * kTile - 1)) * R;
+            CK_DASSERT(!(j0 + u < Lc) || ((c[u] >> 8) >= max(tile - 1, m0) && (c[u] >> 8) <= tile + 1 &&
+                                          (c[u] >> 8) < m1));
             if (j0 + u < Lc) {
 #pragma unroll
               for (int r = 0; r < R; ++r)
@@ -303,7 +306,10 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
             if (!act[r]) continue;
             double2 g[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) g[u] = __ldg(xb + (int64_t)c[u] * R + r);
+            for (int u = 0; u < U; ++u) {
+              CK_DASSERT(c[u] >= 0 && c[u] < a.nc_pad);
+              g[u] = __ldg(xb + (int64_t)c[u] * R + r);
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u)
               if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xtilde(g[u], rad[r])));
@@ -420,6 +426,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
     vc[r] = s.vc;
     if (act[r]) nxt = s.nxt;
   }
+  CK_DASSERT(nxt >= 0 && nxt < a.nbuf && nxt != shared_cur<R>(sts));
   // gradient columns read buffer cur and write buffer nxt in lockstep (a
   // prologue column, mat = 0, carries its x over unchanged)
   const double2* xb = a.PX + (int64_t)shared_cur<R>(sts) * a.nc_pad * R;
@@ -484,6 +491,8 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const double* yw = s_win + (c[u] & (4 * kTile - 1)) * R;
+          CK_DASSERT(!(j0 + u < Lc) || ((c[u] >> 8) >= max(tile - 1, m0) && (c[u] >> 8) <= tile + 1 &&
+                                        (c[u] >> 8) < m1));
           if (j0 + u < Lc) {
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -496,7 +505,10 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
           if (!act[r]) continue;
           double yg[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) yg[u] = __ldg(a.y + (int64_t)c[u] * R + r);
+          for (int u = 0; u < U; ++u) {
+            CK_DASSERT(c[u] >= 0 && c[u] < max(a.nr_pad, a.nc_pad));
+            yg[u] = __ldg(a.y + (int64_t)c[u] * R + r);
+          }
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (j0 + u < Lc) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], yg[u]));
@@ -555,8 +567,8 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
 // control step of the single-device kernels. One thread; g holds per rank the
 // R*kPA apply partials followed by the R transpose partials.
 template <int R>
-__global__ void k_dist_control_apply(LoopArgs a, const double* __restrict__ g, int nranks) {
-  if (threadIdx.x != 0 || !a.hdr->needA) return;
+__device__ __forceinline__ void dist_control_apply(const LoopArgs& a, const double* __restrict__ g, int nranks) {
+  if (!a.hdr->needA) return;
   double res[R][4];
   for (int r = 0; r < R; ++r) {
     DD d = dd_zero();
@@ -574,8 +586,9 @@ __global__ void k_dist_control_apply(LoopArgs a, const double* __restrict__ g, i
 }
 
 template <int R>
-__global__ void k_dist_control_transpose(LoopArgs a, const double* __restrict__ g, int nranks) {
-  if (threadIdx.x != 0 || !a.hdr->needT) return;
+__device__ __forceinline__ void dist_control_transpose(const LoopArgs& a, const double* __restrict__ g,
+                                                       int nranks) {
+  if (!a.hdr->needT) return;
   double rad[R];
   for (int r = 0; r < R; ++r) {
     double s = 0.0;
@@ -583,6 +596,40 @@ __global__ void k_dist_control_transpose(LoopArgs a, const double* __restrict__ 
     rad[r] = s;
   }
   control_tail_transpose<R>(a.st, a.hdr, rad);
+}
+
+// Combine kernels of a partition rank (ck_dist.cu): thread 0 merges every
+// rank's partials and runs the control step; all threads scatter the received
+// halo (n entries x R columns at permuted positions pos).
+template <int R>
+__global__ void k_combine_apply(LoopArgs a, const double* __restrict__ g, int nranks, int64_t n,
+                                const int32_t* __restrict__ pos, const double* __restrict__ buf) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k == 0) dist_control_apply<R>(a, g, nranks);
+  if (k >= n * R) return;
+  a.y[(int64_t)pos[k / R] * R + k % R] = buf[k];
+}
+
+// The (x, delta) halo lands in the buffer the control step makes live. The
+// control thread runs concurrently with the scatter threads: a column read
+// before the step is a gradient column (-> nxt), read after it an apply column
+// whose cur is that same buffer (cur is written before phase, nxt not at all).
+template <int R>
+__global__ void k_combine_transpose(LoopArgs a, const double* __restrict__ g, int nranks, int64_t n,
+                                    const int32_t* __restrict__ pos, const double2* __restrict__ buf) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int r = (int)(k % R);
+  int b = 0;
+  double2 v = make_double2(0.0, 0.0);
+  if (k < n * R) {
+    const volatile ColState* c = a.st + r;
+    const int ph = c->phase;
+    const int nx = c->nxt;
+    b = ph == PH_GRAD ? nx : c->cur;
+    v = buf[k];
+  }
+  if (k == 0) dist_control_transpose<R>(a, g, nranks);
+  if (k < n * R) a.PX[((int64_t)b * a.nc_pad + pos[k / R]) * R + r] = v;
 }
 
 // x_{t+1} = x~ / N from (x, delta) pairs, into a plain vector (epilogue / observer).
@@ -680,6 +727,8 @@ static void launch_transpose_r(const ck_session_s* s, cudaStream_t st) {
 }
 
 void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st, int cl);
+void launch_inv_step_dense(const InvArgs* args, int S, int half, cudaStream_t st);
+void lu_dense_solve_launch(ck_lu_s* f, double* x, bool transpose, cudaStream_t st);
 bool inv_cluster_fits(int cl, int S, int R, size_t smem);
 void prepare_inv_step(size_t smem, int R);
 size_t inv_step_smem(const BandView& b, int R);
@@ -688,6 +737,10 @@ int64_t lu_stage_cap(const BandView& b, int R);
 void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaStream_t st);
 
 static void launch_inv_half(ck_session_s* s, int half, cudaStream_t st) {
+  if (s->inv_dense) {
+    launch_inv_step_dense(s->dargs.p, s->S, half, st);
+    return;
+  }
   launch_inv_step(s->dargs.p, s->S, s->R, s->inv_smem, half, st, s->inv_cl);
 }
 
@@ -749,15 +802,17 @@ void session_set_tiles(ck_session_s* s, int t0, int t1) {
   a.units_T = std::max(1, std::min(t1 - t0, 148 * occ_transpose(s->R)));
 }
 
-void launch_dist_control(ck_session_s* s, bool apply, const double* gathered, int nranks,
-                         cudaStream_t st) {
+void launch_dist_combine(ck_session_s* s, bool apply, const double* gathered, int nranks, int64_t n,
+                         const int32_t* pos, const void* buf, cudaStream_t st) {
   const LoopArgs& a = s->args;
-#define CK_DC(RR)                                                                   \
-  case RR:                                                                          \
-    if (apply)                                                                      \
-      k_dist_control_apply<RR><<<1, 32, 0, st>>>(a, gathered, nranks);             \
-    else                                                                            \
-      k_dist_control_transpose<RR><<<1, 32, 0, st>>>(a, gathered, nranks);         \
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, ceil_div(n * s->R, 256));
+#define CK_DC(RR)                                                                                  \
+  case RR:                                                                                         \
+    if (apply)                                                                                     \
+      k_combine_apply<RR><<<blocks, 256, 0, st>>>(a, gathered, nranks, n, pos, (const double*)buf); \
+    else                                                                                           \
+      k_combine_transpose<RR><<<blocks, 256, 0, st>>>(a, gathered, nranks, n, pos,                 \
+                                                      (const double2*)buf);                        \
     break;
   switch (s->R) {
     CK_DC(1)
@@ -1211,11 +1266,17 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
   };
   // cluster size (scripts/check_cluster.py): 12 CTAs from kl + ku >= 1024 (config 2),
   // 8 from >= 256 (config-5 member), when the clusters fit; CK_LU_CLUSTER forces
+  // narrow bands, one column per system: the dense-block sweeps (ck_lu_dense.cuh)
+  bool dense = R == 1;
+  for (int g = 0; g < S; ++g) dense = dense && lus[g]->dense_ok;
+  s->inv_dense = dense;
   int cl = 1;
   auto try_cl = [&](int c) {
     if (cl == 1 && c > 1 && inv_cluster_fits(c, S, R, clu_smem(c))) cl = c;
   };
-  if (const char* e = std::getenv("CK_LU_CLUSTER")) {
+  if (dense) {
+    // no cluster split: the sweeps are bound by the block chain, not by bandwidth
+  } else if (const char* e = std::getenv("CK_LU_CLUSTER")) {
     try_cl(std::max(1, std::min(16, std::atoi(e))));
   } else if (R == 1) {  // measured with one column per system; 4 columns ran slower split (214 vs 134 ms)
     if (wide.kv >= 4 * kLUClusterMinRows && S * 12 <= 148) try_cl(12);
@@ -1251,6 +1312,7 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
     a.cl_ts = ts;
     a.cl_dpart_off = dpart_off;
     a.b.stage_min = lu_stage_min();
+    a.dv = dense ? lus[g]->dense_view() : DenseView{};
     a.PX = s->PX.p + o * R;
     a.pstride = s->npad * R;
     a.MV = s->MV.p + o * R;
@@ -1362,7 +1424,10 @@ static double op_norm(ck_session_s* s, int g, const double* v, cudaStream_t st) 
   double* w = lu->work.p;
   CK_CUDA(cudaMemcpyAsync(w, v + s->seg_off[g], sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   double* xs[1] = {w};
-  lu_solve_launch(lu, xs, 1, false, st);
+  if (s->inv_dense)
+    lu_dense_solve_launch(lu, w, false, st);  // the solver the loop evaluated its losses with
+  else
+    lu_solve_launch(lu, xs, 1, false, st);
   return device_norm(w, n, w + n, st);
 }
 

@@ -753,6 +753,7 @@ static void lu_solve_host(ck_lu_s* f, const double* b, double* x, bool transpose
 // CTA each, sharing the factors -- rather than as columns of one sweep: the
 // sweeps are a latency chain, so R columns on one CTA cost ~1.5x a single one
 // while R CTAs run side by side. Column k of the session is restart k.
+void lu_dense_solve_launch(ck_lu_s* f, double* x, bool transpose, cudaStream_t st);
 constexpr int kInvRestartGroup = 64;
 void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S, const ck_adam_cfg* cfg,
                                   const uint64_t* seeds, int R);
@@ -902,6 +903,27 @@ ck_status ck_lu_solve(ck_lu f, const double* b, double* x) {
 
 ck_status ck_lu_transpose_solve(ck_lu f, const double* b, double* x) {
   return guarded(__func__, [&] { lu_solve_host(LU(f), b, x, true); });
+}
+
+ck_status ck_lu_dense_info(ck_lu f, int32_t* available, double* growth) {
+  return guarded(__func__, [&] {
+    ck_lu_s* lu = LU(f);
+    if (available) *available = lu->dense_ok ? 1 : 0;
+    if (growth) *growth = lu->dense_growth;
+  });
+}
+
+ck_status ck_lu_dense_solve(ck_lu f, int32_t transpose, const double* b, double* x) {
+  return guarded(__func__, [&] {
+    ck_lu_s* lu = LU(f);
+    if (!lu->dense_ok) fail(CK_ERR_UNSUPPORTED, "dense-block sweeps not available for these factors");
+    cudaStream_t st = lu->stream;
+    double* w = lu->work.p;
+    CK_CUDA(cudaMemcpyAsync(w, b, sizeof(double) * lu->n, cudaMemcpyHostToDevice, st));
+    lu_dense_solve_launch(lu, w, transpose != 0, st);
+    CK_CUDA(cudaMemcpyAsync(x, w, sizeof(double) * lu->n, cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+  });
 }
 
 ck_status ck_session_create_inverse(ck_lu f, const ck_adam_cfg* cfg, const uint64_t* seeds,

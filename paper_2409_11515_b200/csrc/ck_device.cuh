@@ -7,6 +7,22 @@
 
 #include "ck_common.h"
 
+// Device-side index checks of the checked build (-DCK_CHECKED, scripts/
+// checked_build.sh): compute-sanitizer is not available on every pool, so the
+// kernels carry their own bounds assertions, compiled out of the product build.
+#ifdef CK_CHECKED
+#include <cstdio>
+#define CK_DASSERT(c)                                                     \
+  do {                                                                    \
+    if (!(c)) {                                                           \
+      printf("CK_DASSERT failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);   \
+      __trap();                                                           \
+    }                                                                     \
+  } while (0)
+#else
+#define CK_DASSERT(c) ((void)0)
+#endif
+
 namespace ck {
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }

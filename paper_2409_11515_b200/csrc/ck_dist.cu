@@ -85,37 +85,29 @@ static NcclApi& nccl() {
   } while (0)
 
 // ------------------------------------------------------------- halo kernels
+// Two small kernels frame every exchange. The pack kernel gathers the outgoing
+// halo into the send buffer and files this rank's reduction partials in its
+// own slot of the gather buffer; the combine kernel (k_combine_apply /
+// k_combine_transpose, ck_adam.cu) merges every rank's partials into the
+// control step and scatters the received halo. Block 0 carries the scalar
+// work, so a rank without halo (one rank) still launches one block.
 __global__ void k_pack_y(int64_t n, int R, const int32_t* __restrict__ pos, const double* __restrict__ y,
-                         double* buf) {
+                         double* buf, const double* __restrict__ part, double* slot, int words) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < words) slot[k] = part[k];
   if (k >= n * R) return;
   buf[k] = y[(int64_t)pos[k / R] * R + k % R];
 }
 
-__global__ void k_unpack_y(int64_t n, int R, const int32_t* __restrict__ pos, const double* __restrict__ buf,
-                           double* y) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n * R) return;
-  y[(int64_t)pos[k / R] * R + k % R] = buf[k];
-}
-
-// (x, delta) of every column's live buffer (ColState::cur) -- after the
-// transpose control step (unpack side).
-__global__ void k_unpack_x(int64_t n, int R, const int32_t* __restrict__ pos, const double2* __restrict__ buf,
-                           int64_t nc_pad, const ColState* __restrict__ st, double2* px) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n * R) return;
-  const int r = (int)(k % R);
-  px[((int64_t)st[r].cur * nc_pad + pos[k / R]) * R + r] = buf[k];
-}
-
-// Pack side, before the transpose control step runs: the buffer that step
-// makes live (control_tail_transpose: a gradient column moves on to nxt;
-// every other column keeps cur).
+// (x, delta) of the buffer the transpose control step is about to make live
+// (control_tail_transpose: a gradient column moves on to nxt; every other
+// column keeps cur).
 __global__ void k_pack_x_next(int64_t n, int R, const int32_t* __restrict__ pos,
                               const double2* __restrict__ px, int64_t nc_pad,
-                              const ColState* __restrict__ st, double2* buf) {
+                              const ColState* __restrict__ st, double2* buf,
+                              const double* __restrict__ part, double* slot, int words) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < words) slot[k] = part[k];
   if (k >= n * R) return;
   const int r = (int)(k % R);
   const ColState& c = st[r];
@@ -133,30 +125,30 @@ static unsigned blocks_for(int64_t n) { return (unsigned)std::max<int64_t>(1, (n
 // pays one communication latency.
 static void pack_halo(ck_session_s* const* ss, int np, bool x_side, cudaStream_t st) {
   const int R = ss[0]->R;
+  const int w = partial_words(R);
   for (int p = 0; p < np; ++p) {
     ck_session_s* s = ss[p];
     DistPart& d = *s->dist;
     const int64_t n = x_side ? d.xs_off.back() : d.ys_off.back();
-    if (n == 0) continue;
+    double* slot = d.gather.p + (size_t)d.rank * w;
+    const unsigned blocks = blocks_for(std::max<int64_t>(n * R, w));
     if (x_side)
-      k_pack_x_next<<<blocks_for(n * R), 256, 0, st>>>(n, R, d.xs_pos.p, s->PX.p, s->npad, s->st.p,
-                                                      d.xs_buf.p);
+      k_pack_x_next<<<blocks, 256, 0, st>>>(n, R, d.xs_pos.p, s->PX.p, s->npad, s->st.p, d.xs_buf.p,
+                                            d.part.p, slot, w);
     else
-      k_pack_y<<<blocks_for(n * R), 256, 0, st>>>(n, R, d.ys_pos.p, s->y.p, d.ys_buf.p);
+      k_pack_y<<<blocks, 256, 0, st>>>(n, R, d.ys_pos.p, s->y.p, d.ys_buf.p, d.part.p, slot, w);
   }
 }
 
-static void unpack_halo(ck_session_s* const* ss, int np, bool x_side, cudaStream_t st) {
-  const int R = ss[0]->R;
+// Control step of every rank (all ranks merge the same gathered partials in
+// rank order) fused with the scatter of the received halo.
+static void combine(ck_session_s* const* ss, int np, bool x_side, cudaStream_t st) {
   for (int q = 0; q < np; ++q) {
     ck_session_s* s = ss[q];
     DistPart& d = *s->dist;
     const int64_t n = x_side ? d.xr_off.back() : d.yr_off.back();
-    if (n == 0) continue;
-    if (x_side)
-      k_unpack_x<<<blocks_for(n * R), 256, 0, st>>>(n, R, d.xr_pos.p, d.xr_buf.p, s->npad, s->st.p, s->PX.p);
-    else
-      k_unpack_y<<<blocks_for(n * R), 256, 0, st>>>(n, R, d.yr_pos.p, d.yr_buf.p, s->y.p);
+    launch_dist_combine(s, !x_side, d.gather.p, d.nranks, n, x_side ? d.xr_pos.p : d.yr_pos.p,
+                        x_side ? (const void*)d.xr_buf.p : (const void*)d.yr_buf.p, st);
   }
 }
 
@@ -167,8 +159,6 @@ static void transfer(ck_session_s* const* ss, int np, bool x_side, cudaStream_t 
   const DistPart& d0 = *ss[0]->dist;
   if (d0.nccl) {
     const DistPart& d = d0;
-    CK_CUDA(cudaMemcpyAsync(d.gather.p + (size_t)d.rank * w, d.part.p, w * sizeof(double),
-                            cudaMemcpyDeviceToDevice, st));
     const char* sb = x_side ? (const char*)d.xs_buf.p : (const char*)d.ys_buf.p;
     char* rb = x_side ? (char*)d.xr_buf.p : (char*)d.yr_buf.p;
     const auto& so = x_side ? d.xs_off : d.ys_off;
@@ -186,10 +176,11 @@ static void transfer(ck_session_s* const* ss, int np, bool x_side, cudaStream_t 
     CK_NCCL(nccl().GroupEnd());
     return;
   }
-  for (int q = 0; q < np; ++q)  // partials
+  for (int q = 0; q < np; ++q)  // partials (a rank's own slot was filed by its pack kernel)
     for (int p = 0; p < np; ++p)
-      CK_CUDA(cudaMemcpyAsync(ss[q]->dist->gather.p + (size_t)p * w, ss[p]->dist->part.p,
-                              w * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if (p != q)
+        CK_CUDA(cudaMemcpyAsync(ss[q]->dist->gather.p + (size_t)p * w, ss[p]->dist->part.p,
+                                w * sizeof(double), cudaMemcpyDeviceToDevice, st));
   for (int p = 0; p < np; ++p)  // halos
     for (int q = 0; q < np; ++q) {
       const DistPart& a = *ss[p]->dist;  // sender
@@ -207,18 +198,15 @@ static void transfer(ck_session_s* const* ss, int np, bool x_side, cudaStream_t 
 
 // One Projected-Adam iteration of every rank in ss.
 static void run_step(ck_session_s* const* ss, int np, cudaStream_t st) {
+  // four launches and one exchange per half step: sweep, pack, [exchange], combine
   for (int p = 0; p < np; ++p) launch_apply_only(ss[p], st);
   pack_halo(ss, np, false, st);
   transfer(ss, np, false, st);  // apply partials + y' halo
-  for (int p = 0; p < np; ++p)
-    launch_dist_control(ss[p], true, ss[p]->dist->gather.p, ss[p]->dist->nranks, st);
-  unpack_halo(ss, np, false, st);
+  combine(ss, np, false, st);
   for (int p = 0; p < np; ++p) launch_transpose_only(ss[p], st);
   pack_halo(ss, np, true, st);  // the buffers the control step below makes live
   transfer(ss, np, true, st);   // transpose partials + (x, delta) halo
-  for (int p = 0; p < np; ++p)
-    launch_dist_control(ss[p], false, ss[p]->dist->gather.p, ss[p]->dist->nranks, st);
-  unpack_halo(ss, np, true, st);
+  combine(ss, np, true, st);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -407,20 +395,36 @@ double dist_time(ck_dist_s* D, uint64_t steps) {
     session_time(D->sess[0], steps, 1, &ms, &a, &t);
     return ms;
   }
+  // in-process ranks: the steps are replayed from a CUDA graph, so the figure is
+  // device time (sweeps, pack / combine kernels, the copies standing in for the
+  // exchange), not the host's launch rate
   ck_session_s* const* ss = D->sess.data();
   const int np = (int)D->sess.size();
+  const uint64_t chunk = std::min<uint64_t>(steps, 10);
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  CK_CUDA(cudaStreamSynchronize(D->stream));
+  CK_CUDA(cudaStreamBeginCapture(D->stream, cudaStreamCaptureModeThreadLocal));
+  for (uint64_t k = 0; k < chunk; ++k) run_step(ss, np, D->stream);
+  CK_CUDA(cudaStreamEndCapture(D->stream, &g));
+  CK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  CK_CUDA(cudaGraphDestroy(g));
   cudaEvent_t e0, e1;
   CK_CUDA(cudaEventCreate(&e0));
   CK_CUDA(cudaEventCreate(&e1));
+  CK_CUDA(cudaGraphLaunch(ge, D->stream));  // warm
   CK_CUDA(cudaStreamSynchronize(D->stream));
   CK_CUDA(cudaEventRecord(e0, D->stream));
-  for (uint64_t k = 0; k < steps; ++k) run_step(ss, np, D->stream);
+  uint64_t k = 0;
+  for (; k + chunk <= steps; k += chunk) CK_CUDA(cudaGraphLaunch(ge, D->stream));
+  for (; k < steps; ++k) run_step(ss, np, D->stream);
   CK_CUDA(cudaEventRecord(e1, D->stream));
   CK_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
   CK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
   return ms;
 }
 

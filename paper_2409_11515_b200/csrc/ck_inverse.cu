@@ -223,6 +223,109 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
   if (CLU) clu_sync();  // no rank leaves while another may still touch its shared memory
 }
 
+// The same loop trip on the dense-block sweeps (narrow bands, ck_lu_dense.cuh):
+// one column per system, kDenseThreads threads.
+__global__ void __launch_bounds__(kDenseThreads, 1) k_inv_step_dense(const InvArgs* __restrict__ args, int half) {
+  const InvArgs& a = args[blockIdx.x];
+  __shared__ double smem[3 * kDenseThreads];
+  __shared__ double s_h[32], s_l[32];
+  __shared__ int s_e[32], s_f[32];
+  __shared__ double s_res[4];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t n = a.n;
+  double* ys = a.y;
+  ColState* s = a.st;
+
+  // ---------------- apply half: y' = A^{-1} x~ and the control step
+  const int ph = s->phase;
+  if ((ph == PH_PRO || ph == PH_APPLY) && half != 2) {
+    const bool pro = ph == PH_PRO;
+    const double rad = pro ? 0.0 : s->rad;
+    const double2* xc = a.PX + s->cur * a.pstride;
+    DD dd = dd_zero();
+    ES dn = es_zero();
+    double xd = 0.0;
+    for (int64_t i = tid; i < n; i += nt) {
+      const double2 p = xc[i];
+      const double xt = xtilde_inv(p, rad);
+      ys[i] = xt;
+      dd_add_sq(dd, xt);
+      if (!pro) {
+        const double dp = __dsub_rn(p.y, __dmul_rn(rad, p.x));
+        xd = __fma_rn(p.x, dp, xd);
+        es_add(dn, dp);
+      }
+    }
+    dd = block_dd(dd, s_h, s_l);
+    const double x2 = block_sum(xd, s_h);
+    const ES e2 = block_es(dn, s_h, s_e, s_f);
+    if (tid == 0) {
+      s_res[0] = sqrt(__dadd_rn(dd.hi, dd.lo));
+      s_res[2] = x2;
+      s_res[3] = es_norm(e2);
+    }
+    __syncthreads();
+    dense_solve(a.dv, ys, smem, false);
+    ES e = es_zero();
+    for (int64_t i = tid; i < n; i += nt) es_add(e, ys[i]);
+    e = block_es(e, s_h, s_e, s_f);
+    if (tid == 0) {
+      s_res[1] = es_norm(e);
+      if (ph == PH_APPLY) {
+        s->obs_xd = s_res[2];
+        s->obs_dn = s_res[3];
+      }
+      control_apply(s, &a.prm, s_res[0], s_res[1], -1);
+    }
+    __syncthreads();
+  }
+
+  // ---------------- transpose half: z = A^{-T} y', Adam, r = x.delta
+  if (s->phase == PH_GRAD && half != 1) {
+    const bool mat = s->mat != 0;
+    const double rad = s->rad, ndiv = s->ndiv, ix2 = s->inv_x2, iy2 = s->inv_y2, mc = s->mc, vc = s->vc;
+    const double2* xc = a.PX + s->cur * a.pstride;
+    double2* xn_out = a.PX + (mat ? s->nxt : s->cur) * a.pstride;
+    __syncthreads();  // every thread has read the control state
+    dense_solve(a.dv, ys, smem, true);
+    const Params& p = a.prm;
+    const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
+    double dot = 0.0;
+    for (int64_t j = tid; j < n; j += nt) {
+      const double2 px = xc[j];
+      const double xn = mat ? __ddiv_rn(xtilde_inv(px, rad), ndiv) : px.x;
+      const double zz = __ddiv_rn(ys[j], ndiv);
+      const double g = __dsub_rn(__dmul_rn(xn, ix2), __dmul_rn(zz, iy2));
+      const double2 mv = a.MV[j];
+      const double mm = __dadd_rn(__dmul_rn(p.beta1, mv.x), __dmul_rn(om1, g));
+      const double vv = __dadd_rn(__dmul_rn(p.beta2, mv.y), __dmul_rn(__dmul_rn(om2, g), g));
+      const double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc)),
+                                 __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc)), p.eps));
+      a.MV[j] = make_double2(mm, vv);
+      xn_out[j] = make_double2(xn, d);
+      dot = __fma_rn(xn, d, dot);
+    }
+    const double sdot = block_sum(dot, s_h);
+    if (tid == 0) {
+      s->rad = sdot;
+      if (s->mat) {
+        s->cur = s->nxt;
+        s->pend = 0;
+      }
+      s->phase = PH_APPLY;
+    }
+  }
+  if (tid == 0) {
+    a.hdr->nwait = s->phase == PH_WAIT;
+    a.hdr->ndone = s->phase == PH_DONE;
+    a.hdr->needA = 1;
+  }
+}
+
+void launch_inv_step_dense(const InvArgs* args, int S, int half, cudaStream_t st) {
+  k_inv_step_dense<<<S, kDenseThreads, 0, st>>>(args, half);
+}
+
 void prepare_inv_step(size_t smem, int R) {
   switch (R) {
     case 1:

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "ck_common.h"
@@ -570,6 +571,141 @@ __global__ void __launch_bounds__(256) k_convert_l_blocks(BandView b) {
   }
 }
 
+// ------------------------------------------------ dense blocks (ck_lu_dense.cuh)
+// Composite block matrices of the dense sweeps, one CTA per 32-row block:
+// inverses of the block's head triangles (substitution on the identity, one
+// thread per column), their products with the band coefficients the block
+// reaches, the interchange maps, and the growth factor || |Hinv| |H| ||_inf of
+// both heads (atomicMax over the blocks; doubles >= 0 order like their bits).
+__global__ void __launch_bounds__(256) k_dense_blocks(BandView b, double* clf, double* clt, double* cub,
+                                                      double* cut, uint8_t* pinv, uint8_t* psrc,
+                                                      unsigned long long* growth) {
+  const int64_t blk = blockIdx.x, J = blk * kLUBlock, n = b.n;
+  const int tid = threadIdx.x;
+  const int kl = (int)b.kl, kv = (int)b.kv, wl = kLUBlock + kl, wu = kLUBlock + kv;
+  __shared__ double Lh[32][33], Uh[32][33], Li[32][33], Ui[32][33];
+  // heads: Lh(r, c) multipliers r > c (unit diagonal), Uh(r, c) r <= c; rows and
+  // columns past n are the identity
+  for (int q = tid; q < 1024; q += blockDim.x) {
+    const int r = q >> 5, c = q & 31;
+    double l = 0.0, u = r == c ? 1.0 : 0.0;
+    if (J + r < n && J + c < n) {
+      if (r > c) l = b.lb[(blk * kLUBlock + c) * b.lb_ld + r];
+      if (r <= c && c - r <= kv) u = AB(b, J + r, J + c);
+    }
+    Lh[r][c] = l;
+    Uh[r][c] = u;
+    Li[r][c] = 0.0;
+    Ui[r][c] = 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {  // column c of Linv: forward substitution on e_c
+    const int c = tid;
+    Li[c][c] = 1.0;
+    for (int i = c + 1; i < 32; ++i) {
+      double s = 0.0;
+      for (int k = c; k < i; ++k) s = __fma_rn(Lh[i][k], Li[k][c], s);
+      Li[i][c] = -s;
+    }
+  } else if (tid < 64) {  // column c of Uinv: backward substitution on e_c
+    const int c = tid - 32;
+    Ui[c][c] = 1.0 / Uh[c][c];
+    for (int i = c - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1; k <= c; ++k) s = __fma_rn(Uh[i][k], Ui[k][c], s);
+      Ui[i][c] = -s / Uh[i][i];
+    }
+  }
+  __syncthreads();
+  if (tid < 64) {  // growth: row sums of |Hinv| |H|
+    const int i = tid & 31;
+    const bool low = tid < 32;
+    double row = 0.0;
+    for (int j = 0; j < 32; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < 32; ++k) {
+        const double hi = low ? Li[i][k] : Ui[i][k];
+        const double h = low ? (k == j ? 1.0 : Lh[k][j]) : Uh[k][j];
+        s += fabs(hi) * fabs(h);
+      }
+      row += s;
+    }
+    if (!(row == row)) row = INFINITY;
+    atomicMax(growth, (unsigned long long)__double_as_longlong(row));
+  }
+  // interchange maps
+  for (int q = tid; q < wl; q += blockDim.x) {
+    pinv[blk * wl + q] = (uint8_t)q;
+    psrc[blk * wl + q] = (uint8_t)q;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int32_t* pp = b.perm + blk * (1 + 4 * kLUBlock);
+    const int np = pp[0];
+    for (int t = 0; t < np; ++t) {
+      const int dst = pp[1 + 2 * t], src = pp[2 + 2 * t];
+      psrc[blk * wl + dst] = (uint8_t)src;
+      pinv[blk * wl + src] = (uint8_t)dst;
+    }
+  }
+  double* F = clf + blk * 32 * wl;   // [c][r]
+  double* T = clt + blk * wl * 32;   // [k][c]
+  double* B = cub + blk * 32 * wu;   // [c][r]
+  double* G = cut + blk * 32 * wu;   // [c][r]
+  // L: rows r < 32 Linv, rows 32 + m: -(Tl Linv)(m, c), Tl(m, k) = lb[k][32 + m]
+  for (int q = tid; q < 32 * wl; q += blockDim.x) {
+    const int c = q / wl, r = q % wl;
+    double v;
+    if (r < 32) {
+      v = Li[r][c];
+    } else {
+      const int m = r - 32;
+      double s = 0.0;
+      if (J + 32 + m < n)
+        for (int k = c; k < 32; ++k)
+          if (J + k < n) s = __fma_rn(b.lb[(blk * kLUBlock + k) * b.lb_ld + 32 + m], Li[k][c], s);
+      v = -s;
+    }
+    F[q] = v;
+    T[r * 32 + c] = v;
+  }
+  // U backward: rows m < kv: -(Tu Uinv)(m, c), Tu(m, k) = U(J - kv + m, J + k) for
+  // m >= k; rows kv + r: Uinv(r, c)
+  for (int q = tid; q < 32 * wu; q += blockDim.x) {
+    const int c = q / wu, r = q % wu;
+    double v;
+    if (r >= kv) {
+      v = Ui[r - kv][c];
+    } else {
+      const int64_t i = J - kv + r;
+      double s = 0.0;
+      if (i >= 0)
+        for (int k = 0; k <= c && k <= r; ++k)
+          if (J + k < n) s = __fma_rn(AB(b, i, J + k), Ui[k][c], s);
+      v = -s;
+    }
+    B[q] = v;
+  }
+  // U^T forward: rows r < 32: Uinv^T(r, c) = Uinv(c, r); rows 32 + q2:
+  // -(G Uinv^T)(q2, c), G(q2, k) = U(J + k, J + 32 + q2) inside the band
+  for (int q = tid; q < 32 * wu; q += blockDim.x) {
+    const int c = q / wu, r = q % wu;
+    double v;
+    if (r < 32) {
+      v = Ui[c][r];
+    } else {
+      const int q2 = r - 32;
+      const int64_t col = J + 32 + q2;
+      double s = 0.0;
+      if (col < n)
+        for (int k = c; k < 32; ++k)
+          if (J + k < n && 32 + q2 - k <= kv) s = __fma_rn(AB(b, J + k, col), Ui[c][k], s);
+      v = -s;
+    }
+    G[q] = v;
+  }
+}
+
 template <int R>
 __global__ void __launch_bounds__(1024) k_lu_solve(BandView b, double* x0, double* x1, double* x2,
                                                    double* x3, int transpose, int ring_size) {
@@ -785,7 +921,43 @@ static void lu_finish(ck_lu_s* f, int64_t* fail_col, double* fail_pivot) {
   if (n > 0) k_convert_l_blocks<<<(unsigned)nblk, 256, 0, st>>>(b);
   if (n > 0) k_pivot_reciprocals<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b);
   CK_CUDA(cudaGetLastError());
+  // narrow bands: the composite blocks of the dense sweeps (CK_LU_DENSE=0: A/B)
+  f->dense_ok = false;
+  const char* de = std::getenv("CK_LU_DENSE");
+  if (n > 0 && std::max(f->kl, f->kl + f->ku) <= kDenseMaxBand && !(de && de[0] == '0')) {
+    const int wl = kLUBlock + (int)f->kl, wu = kLUBlock + (int)(f->kl + f->ku);
+    f->dense_cf.alloc(nblk * 32 * (2 * (int64_t)wl + 2 * (int64_t)wu));
+    f->dense_perm.alloc(2 * nblk * wl);
+    DBuf<unsigned long long> g(1);
+    CK_CUDA(cudaMemsetAsync(g.p, 0, sizeof(unsigned long long), st));
+    double* c = f->dense_cf.p;
+    const int64_t sl = nblk * 32 * wl, su = nblk * 32 * wu;
+    k_dense_blocks<<<(unsigned)nblk, 256, 0, st>>>(b, c, c + sl, c + 2 * sl, c + 2 * sl + su,
+                                                   f->dense_perm.p, f->dense_perm.p + nblk * wl, g.p);
+    CK_CUDA(cudaGetLastError());
+    unsigned long long bits = 0;
+    CK_CUDA(cudaMemcpyAsync(&bits, g.p, sizeof(bits), cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(&f->dense_growth, &bits, sizeof(double));
+    f->dense_ok = f->dense_growth <= kDenseMaxGrowth || (de && de[0] == '2');  // 2: force (tests)
+    if (!f->dense_ok) {
+      f->dense_cf.reset();
+      f->dense_perm.reset();
+    }
+  }
   CK_CUDA(cudaStreamSynchronize(st));
+}
+
+// Standalone dense-block solve (the witness check of a dense inverse session).
+__global__ void __launch_bounds__(kDenseThreads, 1) k_dense_solve(DenseView d, double* x, int transpose) {
+  __shared__ double smem[3 * kDenseThreads];
+  dense_solve(d, x, smem, transpose != 0);
+}
+
+void lu_dense_solve_launch(ck_lu_s* f, double* x, bool transpose, cudaStream_t st) {
+  if (!f->dense_ok) fail(CK_ERR_LOGIC, "dense blocks not built");
+  k_dense_solve<<<1, kDenseThreads, 0, st>>>(f->dense_view(), x, transpose ? 1 : 0);
+  CK_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------ LUFactors in the reference's shape

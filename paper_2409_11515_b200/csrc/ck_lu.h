@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "ck_common.h"
+#include "ck_lu_dense.cuh"
 
 namespace ck {
 
@@ -103,6 +104,19 @@ struct ck_lu_s {
   ck::DBuf<int32_t> orig;
   ck::DBuf<ck::LUStatus> status;
   ck::DBuf<double> work;  // solve scratch
+  // dense-block sweeps of narrow bands (ck_lu_dense.cuh), built by lu_finish
+  bool dense_ok = false;
+  double dense_growth = 0.0;  // max over blocks of || |Hinv| |H| ||_inf
+  ck::DBuf<double> dense_cf;  // clf | clt | cub | cut
+  ck::DBuf<uint8_t> dense_perm;  // pinv | psrc
+  ck::DenseView dense_view() const {
+    const int nb = (int)((n + ck::kLUBlock - 1) / ck::kLUBlock);
+    const int wl = ck::kLUBlock + (int)kl, wu = ck::kLUBlock + (int)(kl + ku);
+    const double* c = dense_cf.p;
+    const int64_t sl = (int64_t)nb * 32 * wl, su = (int64_t)nb * 32 * wu;
+    return ck::DenseView{n, nb, (int)kl, (int)(kl + ku), wl, wu, c, c + sl, c + 2 * sl, c + 2 * sl + su,
+                         dense_perm.p, dense_perm.p + (int64_t)nb * wl};
+  }
   // CSR factors in the reference's LUFactors shape (built on request: lu_build_csr)
   bool csr_built = false;
   int64_t nnz_l = 0, nnz_u = 0;

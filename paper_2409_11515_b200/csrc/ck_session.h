@@ -87,6 +87,8 @@ struct InvArgs {
   // and dot partials [cl][R][32]
   int cl;
   int64_t cl_tsum_off, cl_ts, cl_dpart_off;
+  // narrow bands: composite blocks of the dense sweeps (ck_lu_dense.cuh)
+  DenseView dv;
 };
 
 // Row-block partition rank (ck_dist.cu): this rank owns global rows/columns
@@ -127,6 +129,7 @@ struct ck_session_s {
   DBuf<ck::InvArgs> dargs;    // kind 1: per-member step arguments
   size_t inv_smem = 0;        // kind 1: dynamic shared memory of the step CTA
   int inv_cl = 1;             // kind 1: CTAs per system (cluster split of the sweeps)
+  bool inv_dense = false;     // kind 1: dense-block sweeps (narrow bands, one column per system)
   cudaStream_t stream = nullptr;
   int device = 0;
   int64_t n = 0;            // operator dimension (columns of A)
@@ -180,8 +183,8 @@ void session_run(ck_session_s* s, uint64_t max_steps, int32_t* finished);
 void session_time(ck_session_s* s, uint64_t steps, int32_t mode, double* ms_total,
                   double* ms_apply, double* ms_transpose);
 void session_set_tiles(ck_session_s* s, int t0, int t1);
-void launch_dist_control(ck_session_s* s, bool apply, const double* gathered, int nranks,
-                         cudaStream_t st);
+void launch_dist_combine(ck_session_s* s, bool apply, const double* gathered, int nranks, int64_t n,
+                         const int32_t* pos, const void* buf, cudaStream_t st);
 int partial_words(int R);
 void dist_step(ck_session_s* s, cudaStream_t st);
 double dist_op_norm(ck_session_s* s, const double* xbest_internal, cudaStream_t st);

@@ -54,6 +54,22 @@ class LUFactors:
                    "lu_transpose_solve")
         return x
 
+    def dense_info(self):
+        """(available, growth) of the dense-block sweeps the InverseOracle loop uses on
+        narrow bands (ck_lu_dense_info): growth = max over 32-row blocks of
+        || |Hinv| |H| ||_inf of the head triangles."""
+        ok, g = C.c_int32(), C.c_double()
+        _lib.check(_lib.load().ck_lu_dense_info(self.handle, C.byref(ok), C.byref(g)), "ck_lu_dense_info")
+        return bool(ok.value), g.value
+
+    def dense_solve(self, b, transpose: bool = False) -> np.ndarray:
+        """lu_solve / lu_transpose_solve through the dense-block sweeps (parity tests)."""
+        b = _lib.as_f64(b, self.n, "lu_dense_solve: rhs")
+        x = np.empty(self.n)
+        _lib.check(_lib.load().ck_lu_dense_solve(self.handle, 1 if transpose else 0, _lib.dptr(b),
+                                                 _lib.dptr(x)), "lu_dense_solve")
+        return x
+
     def export_csr(self):
         """(L, U, row_perm) in the reference's LUFactors shape (lu.hpp:42-47): L strictly
         lower in pivot coordinates (unit diagonal implicit), U upper with the diagonal

@@ -89,7 +89,10 @@ def test_inverse_batch_matches_members(port):
     for m, f, g, sd in zip(mem, facs, got, seeds):
         c = M.cfg(alpha=1e-2, max_iter=300, patience=300, seed=sd)
         alone = ck.estimate_norm(ck.InverseOracle(f), c, 3)
-        assert g.value == alone.value and g.iterations == alone.iterations
+        # the batch sweeps 3 restart columns per member by substitution; a member alone
+        # runs its restarts one CTA each, on the dense-block sweeps where the band is
+        # narrow (ck_lu_dense.cuh): same solves to rounding
+        assert g.value == pytest.approx(alone.value, rel=1e-11) and g.iterations == alone.iterations
         o = port.estimate_norm_inverse(port.lu_factorize(m, 1e-14), c, 3)
         assert g.iterations == o.iterations and g.converged == o.converged
         assert g.value == pytest.approx(o.value, rel=1e-9)
@@ -107,7 +110,10 @@ def test_inverse_batch_session_witnesses(port):
             e = s.member_result(g, c)
             alone = ck.projected_adam(ck.InverseOracle(f), M.cfg(alpha=1e-2, max_iter=150,
                                                                   patience=150, seed=seeds[g * 2 + c]))
-            assert e.value == alone.value and np.array_equal(e.witness, alone.witness)
+            # alone: one CTA per run on the dense-block sweeps (narrow bands); the
+            # session sweeps 2 columns per member by substitution -- same solves to rounding
+            assert e.value == pytest.approx(alone.value, rel=1e-11)
+            assert np.linalg.norm(e.witness - alone.witness) <= 1e-9
             assert np.linalg.norm(f.solve(e.witness)) == pytest.approx(e.value, rel=1e-12)
 
 
@@ -122,7 +128,7 @@ def test_cond2_batch_matches_cond2(port):
     for m, r, sd in zip(mem[:4], got, seeds):
         c = M.cfg(alpha=1e-2, max_iter=300, patience=300, seed=sd)
         want = ck.cond2(m, c, restarts=2)
-        assert r.kappa == want.kappa
+        assert r.kappa == pytest.approx(want.kappa, rel=1e-11)  # substitution vs dense-block sweeps
         o = port.cond2(m, c, restarts=2)
         assert r.kappa == pytest.approx(o["kappa"], rel=1e-9)
     assert got[4].kappa == float("inf")

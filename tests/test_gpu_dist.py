@@ -73,3 +73,18 @@ def test_nccl_backend_single_rank(port):
     assert e.iterations == one.iterations
     assert e.value == pytest.approx(one.value, rel=1e-12)
     assert s.time(3) > 0.0
+
+
+@pytest.mark.parametrize("kind", ["hm", "banded"])
+def test_partition_eight_ranks(port, kind):
+    """BASELINE's 8-rank row-block partition, all ranks in one process: one exchange
+    (partials + halo) per half step framed by the fused pack / combine kernels."""
+    a = {"hm": lambda: configs.generate(3, 24), "banded": lambda: configs.ensemble_member(2, 1, n=6000, bw=100)}[kind]()
+    cfg = M.cfg(alpha=1e-2, max_iter=200, patience=200, seed=7)
+    got = dist.projected_adam_partitioned(a, 8, cfg, seeds=[7, 8])
+    for e, sd in zip(got, [7, 8]):
+        c = M.cfg(alpha=1e-2, max_iter=200, patience=200, seed=sd)
+        one = ck.projected_adam(ck.ExplicitOracle(a), c)
+        assert e.iterations == one.iterations
+        assert e.value == pytest.approx(one.value, rel=1e-10)
+        assert np.linalg.norm(port.matvec(a, e.witness)) == pytest.approx(e.value, rel=1e-12)

@@ -272,3 +272,51 @@ def test_cluster_sweeps_several_columns(port, monkeypatch):
     for e1, e8 in zip(res["1"], res["8"]):
         assert e8.iterations == e1.iterations
         assert e8.value == pytest.approx(e1.value, rel=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["random40", "laplacian24", "banded700", "rowscaled64", "odd1000", "tiny3"])
+def test_dense_block_sweeps_match_substitution(port, kind):
+    """Narrow bands: the InverseOracle loop sweeps with the inverted 32 x 32 head
+    triangles (ck_lu_dense.cuh). Same solves as lu_solve / lu_transpose_solve
+    (lu.hpp:180-227): within 1e-10 of the oracle (observed ~1e-14), growth-guarded."""
+    from paper_2409_11515_b200 import configs
+    a = {"random40": lambda: M.random_sparse(port, 40, 0.2, 4),
+         "laplacian24": lambda: M.laplacian2d(24),
+         "banded700": lambda: _banded(700, 45, 2),
+         "rowscaled64": lambda: M.row_scaled(M.laplacian2d(64), port, 1),
+         "odd1000": lambda: _banded(1003, 70, 5),
+         "tiny3": lambda: M.diag_matrix([5.0, 3.0, 8.0])}[kind]()
+    f = ck.lu_factorize(a, 1e-14)
+    rf = port.lu_factorize(a, 1e-14)
+    ok, growth = f.dense_info()
+    assert ok and 1.0 <= growth <= 1e4
+    for k in range(3):
+        b = port.random_unit_vectors(11 + k, a.nrows)[0]
+        for tr in (False, True):
+            want = port.lu_transpose_solve(rf, b) if tr else port.lu_solve(rf, b)
+            got = f.dense_solve(b, transpose=tr)
+            assert np.linalg.norm(got - want) <= 1e-10 * np.linalg.norm(want)
+            exact = f.transpose_solve(b) if tr else f.solve(b)
+            assert np.linalg.norm(got - exact) <= 1e-11 * np.linalg.norm(exact)
+
+
+def test_dense_sweeps_guard_and_loop(port, monkeypatch):
+    """Wide bands and ill-conditioned heads keep the substitution sweeps; on narrow
+    bands the loop's sigma_min agrees with the substitution loop and the oracle."""
+    from paper_2409_11515_b200 import configs
+    wide = configs.ensemble_member(3, 1, n=1500, bw=150)  # kl + ku ~ 300 > 192
+    assert not ck.lu_factorize(wide, 1e-14).dense_info()[0]
+    ill = configs.ensemble_member(0, 1, n=600, bw=20)  # column scales 10^U(-8, 8)
+    fi = ck.lu_factorize(ill, 1e-14)
+    ok, growth = fi.dense_info()
+    assert ok == (growth <= 1e4)
+    a = M.row_scaled(M.laplacian2d(40), port, 3)
+    cfg = M.cfg(alpha=1e-2, max_iter=300, patience=300, seed=5)
+    dense = ck.inv_norm2(ck.lu_factorize(a, 1e-14), cfg)
+    monkeypatch.setenv("CK_LU_DENSE", "0")
+    subst = ck.inv_norm2(ck.lu_factorize(a, 1e-14), cfg)
+    monkeypatch.delenv("CK_LU_DENSE")
+    want = port.projected_adam_inverse(port.lu_factorize(a, 1e-14), cfg)
+    assert dense.iterations == subst.iterations == want.iterations
+    assert dense.value == pytest.approx(subst.value, rel=1e-9)
+    assert dense.value == pytest.approx(want.value, rel=1e-9)
