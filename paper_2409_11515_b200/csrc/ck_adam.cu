@@ -727,7 +727,8 @@ static void launch_transpose_r(const ck_session_s* s, cudaStream_t st) {
 }
 
 void launch_inv_step(const InvArgs* args, int S, int R, size_t smem, int half, cudaStream_t st, int cl);
-void launch_inv_step_dense(const InvArgs* args, int S, int half, cudaStream_t st);
+void launch_inv_step_dense(const InvArgs* args, int S, int half, size_t dyn, cudaStream_t st);
+void prepare_inv_step_dense(size_t dyn);
 void lu_dense_solve_launch(ck_lu_s* f, double* x, bool transpose, cudaStream_t st);
 bool inv_cluster_fits(int cl, int S, int R, size_t smem);
 void prepare_inv_step(size_t smem, int R);
@@ -738,7 +739,7 @@ void lu_solve_launch(ck_lu_s* f, double* const* x, int R, bool transpose, cudaSt
 
 static void launch_inv_half(ck_session_s* s, int half, cudaStream_t st) {
   if (s->inv_dense) {
-    launch_inv_step_dense(s->dargs.p, s->S, half, st);
+    launch_inv_step_dense(s->dargs.p, s->S, half, s->inv_smem, st);
     return;
   }
   launch_inv_step(s->dargs.p, s->S, s->R, s->inv_smem, half, st, s->inv_cl);
@@ -1286,6 +1287,13 @@ void session_create_inverse_batch(ck_session_s* s, ck_lu_s* const* lus, int S,
     smem = clu_smem(cl);
     s->inv_smem = smem;
     prepare_inv_step(smem, R);
+  }
+  if (dense) {  // the block ring of the widest member
+    size_t dyn = 0;
+    for (int g = 0; g < S; ++g)
+      dyn = std::max(dyn, dense_dyn_smem(kLUBlock + (int)lus[g]->kl, kLUBlock + (int)(lus[g]->kl + lus[g]->ku)));
+    s->inv_smem = dyn;
+    prepare_inv_step_dense(dyn);
   }
   const int64_t dyn = (int64_t)(smem / sizeof(double));
   const int64_t dpart_off = cl > 1 ? dyn - 32 - 2 * (int64_t)cl * R * kLUBlock : dyn;  // two slots

@@ -225,9 +225,12 @@ __global__ void __launch_bounds__(1024) k_inv_step(const InvArgs* __restrict__ a
 
 // The same loop trip on the dense-block sweeps (narrow bands, ck_lu_dense.cuh):
 // one column per system, kDenseThreads threads.
-__global__ void __launch_bounds__(kDenseThreads, 1) k_inv_step_dense(const InvArgs* __restrict__ args, int half) {
+__global__ void __launch_bounds__(kDenseThreads, 1) k_inv_step_dense(const InvArgs* __restrict__ args, int half,
+                                                                     unsigned dyn_bytes) {
   const InvArgs& a = args[blockIdx.x];
   __shared__ double smem[3 * kDenseThreads];
+  extern __shared__ __align__(16) double dyn[];
+  DenseRing ring = dense_ring(a.dv, dyn, dyn_bytes);
   __shared__ double s_h[32], s_l[32];
   __shared__ int s_e[32], s_f[32];
   __shared__ double s_res[4];
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_inv_step_dense(const InvAr
       s_res[3] = es_norm(e2);
     }
     __syncthreads();
-    dense_solve(a.dv, ys, smem, false);
+    dense_solve(a.dv, ys, smem, ring, false);
     ES e = es_zero();
     for (int64_t i = tid; i < n; i += nt) es_add(e, ys[i]);
     e = block_es(e, s_h, s_e, s_f);
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_inv_step_dense(const InvAr
     const double2* xc = a.PX + s->cur * a.pstride;
     double2* xn_out = a.PX + (mat ? s->nxt : s->cur) * a.pstride;
     __syncthreads();  // every thread has read the control state
-    dense_solve(a.dv, ys, smem, true);
+    dense_solve(a.dv, ys, smem, ring, true);
     const Params& p = a.prm;
     const double om1 = 1.0 - p.beta1, om2 = 1.0 - p.beta2;
     double dot = 0.0;
@@ -322,8 +325,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_inv_step_dense(const InvAr
   }
 }
 
-void launch_inv_step_dense(const InvArgs* args, int S, int half, cudaStream_t st) {
-  k_inv_step_dense<<<S, kDenseThreads, 0, st>>>(args, half);
+// dyn: dynamic shared memory of the block ring (dense_dyn_smem of the widest member)
+void launch_inv_step_dense(const InvArgs* args, int S, int half, size_t dyn, cudaStream_t st) {
+  k_inv_step_dense<<<S, kDenseThreads, dyn, st>>>(args, half, (unsigned)dyn);
+}
+
+void prepare_inv_step_dense(size_t dyn) {
+  CK_CUDA(cudaFuncSetAttribute(k_inv_step_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
 }
 
 void prepare_inv_step(size_t smem, int R) {

@@ -949,14 +949,20 @@ static void lu_finish(ck_lu_s* f, int64_t* fail_col, double* fail_pivot) {
 }
 
 // Standalone dense-block solve (the witness check of a dense inverse session).
-__global__ void __launch_bounds__(kDenseThreads, 1) k_dense_solve(DenseView d, double* x, int transpose) {
+__global__ void __launch_bounds__(kDenseThreads, 1) k_dense_solve(DenseView d, double* x, int transpose,
+                                                                  unsigned dyn_bytes) {
   __shared__ double smem[3 * kDenseThreads];
-  dense_solve(d, x, smem, transpose != 0);
+  extern __shared__ __align__(16) double dyn[];
+  DenseRing R = dense_ring(d, dyn, dyn_bytes);
+  dense_solve(d, x, smem, R, transpose != 0);
 }
 
 void lu_dense_solve_launch(ck_lu_s* f, double* x, bool transpose, cudaStream_t st) {
   if (!f->dense_ok) fail(CK_ERR_LOGIC, "dense blocks not built");
-  k_dense_solve<<<1, kDenseThreads, 0, st>>>(f->dense_view(), x, transpose ? 1 : 0);
+  const DenseView d = f->dense_view();
+  const size_t dyn = dense_dyn_smem(d.wl, d.wu);
+  CK_CUDA(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  k_dense_solve<<<1, kDenseThreads, dyn, st>>>(d, x, transpose ? 1 : 0, (unsigned)dyn);
   CK_CUDA(cudaGetLastError());
 }
 

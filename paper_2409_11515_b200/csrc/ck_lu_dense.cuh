@@ -55,15 +55,95 @@ struct DenseView {
   const uint8_t* psrc;  // [nb][wl]
 };
 
-// 32 products in four independent chains, merged in a fixed order.
-__device__ __forceinline__ double dense_dot32(const double* cf, const double* h) {
+// ---------------------------------------------------------------- block ring
+// The composite blocks of a sweep arrive by TMA bulk copies (cp.async.bulk, one
+// thread, completion on an mbarrier per stage) in a ring of kDenseStages stages,
+// issued kDenseStages blocks ahead of their use: a 24-57 KB block is several L2
+// latencies of plain loads, and a one-block-ahead register prefetch left the
+// sweep waiting (1640 cycles per block step against ~400 of shared-memory time).
+constexpr int kDenseStagesMax = 4;
+
+struct DenseRing {
+  double* buf;           // [ns][stage] doubles, 16-byte aligned
+  uint64_t* bar;         // [ns] mbarriers
+  int ns;                // stages in use
+  int64_t stage;         // doubles per stage (>= 32 * max(wl, wu))
+  // blocks streamed so far (same in every thread): the stages are used round
+  // robin across sweeps, so a stage's mbarrier phase is (count / ns) & 1
+  uint32_t count;
+};
+
+// Shared memory of a dense CTA in doubles: window buffers, L^T partials, ring.
+__host__ __device__ __forceinline__ int64_t dense_ring_stage(int wl, int wu) {
+  return (int64_t)32 * (wl > wu ? wl : wu);
+}
+
+__device__ __forceinline__ void ring_init(const DenseRing& R) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < R.ns; ++s) {
+      const uint32_t a = (uint32_t)__cvta_generic_to_shared(R.bar + s);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// One thread: request `bytes` of block data into stage s.
+__device__ __forceinline__ void ring_issue(const DenseRing& R, int s, const double* src, uint32_t bytes) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(R.bar + s);
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(R.buf + (int64_t)s * R.stage);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+__device__ __forceinline__ void ring_wait(const DenseRing& R, int s, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(R.bar + s);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  }
+}
+
+// The k-th block a sweep visits is block first + k * step; its data is `bytes`
+// at C + block * (bytes / 8). Prologue: the first ns blocks in flight.
+struct RingFeed {
+  const double* C;
+  int first, step, nb;
+  uint32_t bytes;
+  __device__ __forceinline__ void issue(const DenseRing& R, int k) const {
+    if (threadIdx.x == 0 && k < nb)
+      ring_issue(R, (int)((R.count + k) % R.ns), C + (int64_t)(first + k * step) * (bytes / 8), bytes);
+  }
+  // every stage is free here: the previous sweep waited for all it issued
+  __device__ __forceinline__ void start(const DenseRing& R) const {
+    for (int k = 0; k < R.ns; ++k) issue(R, k);
+  }
+  __device__ __forceinline__ const double* wait(const DenseRing& R, int k) const {
+    const uint32_t g = R.count + (uint32_t)k;
+    ring_wait(R, (int)(g % R.ns), (g / R.ns) & 1u);
+    return R.buf + (int64_t)(g % R.ns) * R.stage;
+  }
+  __device__ __forceinline__ void finish(DenseRing& R) const { R.count += (uint32_t)nb; }
+};
+
+// 32 products in four independent chains, merged in a fixed order; the
+// coefficients of this thread's row at cf[c * ld].
+__device__ __forceinline__ double dense_dot32(const double* cf, int64_t ld, const double* h) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int c = 0; c < 32; c += 4) {
-    a0 = __fma_rn(cf[c], h[c], a0);
-    a1 = __fma_rn(cf[c + 1], h[c + 1], a1);
-    a2 = __fma_rn(cf[c + 2], h[c + 2], a2);
-    a3 = __fma_rn(cf[c + 3], h[c + 3], a3);
+    a0 = __fma_rn(cf[c * ld], h[c], a0);
+    a1 = __fma_rn(cf[(c + 1) * ld], h[c + 1], a1);
+    a2 = __fma_rn(cf[(c + 2) * ld], h[c + 2], a2);
+    a3 = __fma_rn(cf[(c + 3) * ld], h[c + 3], a3);
   }
   return __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
 }
@@ -72,38 +152,30 @@ __device__ __forceinline__ double dense_dot32(const double* cf, const double* h)
 // [J, J + W), head = positions [0, 32). x is solved in place.
 template <bool PERM>
 __device__ void dense_forward(const DenseView& d, const double* __restrict__ C, int W, double* x,
-                              double* wa, double* wb) {
+                              double* wa, double* wb, DenseRing& R) {
   const int tid = threadIdx.x;
   const int64_t n = d.n;
   double* in = wa;
   double* out = wb;
+  const RingFeed feed{C, 0, 1, d.nb, (uint32_t)(32 * W * sizeof(double))};
+  feed.start(R);
   for (int q = tid; q < W; q += kDenseThreads) {
     const int pos = PERM ? d.pinv[q] : q;
     CK_DASSERT(pos >= 0 && pos < W);
     in[pos] = q < n ? x[q] : 0.0;
   }
-  double cf[32];
-  if (tid < W) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c) cf[c] = C[(int64_t)c * W + tid];
-  }
   __syncthreads();
   for (int blk = 0; blk < d.nb; ++blk) {
     const int64_t J = (int64_t)blk * 32;
     const bool more = blk + 1 < d.nb;
-    double cn[32];
     double fresh = 0.0;
-    if (more && tid < W) {
-      const double* Cn = C + (int64_t)(blk + 1) * 32 * W;
-#pragma unroll
-      for (int c = 0; c < 32; ++c) cn[c] = Cn[(int64_t)c * W + tid];
-    }
     if (tid >= W && tid < W + 32) {  // the 32 rows entering the next window
       const int64_t g = J + W + (tid - W);
       fresh = g < n ? x[g] : 0.0;
     }
+    const double* cf = feed.wait(R, blk);
     if (tid < W) {
-      const double acc = dense_dot32(cf, in);
+      const double acc = dense_dot32(cf + tid, W, in);
       if (tid < 32) {
         if (J + tid < n) x[J + tid] = acc;  // head rows are final
       } else if (more) {
@@ -119,22 +191,24 @@ __device__ void dense_forward(const DenseView& d, const double* __restrict__ C, 
       out[pos] = fresh;
     }
     __syncthreads();
+    feed.issue(R, blk + R.ns);  // the stage just read is free again
     double* t = in;
     in = out;
     out = t;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) cf[c] = cn[c];
   }
+  feed.finish(R);
 }
 
 // U backward: window rows [J - kv, J + 32), head = positions [kv, kv + 32).
-static __device__ void dense_u_backward(const DenseView& d, double* x, double* wa, double* wb) {
+static __device__ void dense_u_backward(const DenseView& d, double* x, double* wa, double* wb,
+                                        DenseRing& R) {
   const int tid = threadIdx.x;
   const int64_t n = d.n;
   const int W = d.wu, kv = d.kv;
-  const double* __restrict__ C = d.cub;
   double* in = wa;
   double* out = wb;
+  const RingFeed feed{d.cub, d.nb - 1, -1, d.nb, (uint32_t)(32 * W * sizeof(double))};
+  feed.start(R);
   {
     const int64_t J = (int64_t)(d.nb - 1) * 32;
     for (int q = tid; q < W; q += kDenseThreads) {
@@ -142,29 +216,19 @@ static __device__ void dense_u_backward(const DenseView& d, double* x, double* w
       in[q] = (row >= 0 && row < n) ? x[row] : 0.0;
     }
   }
-  double cf[32];
-  if (tid < W) {
-    const double* C0 = C + (int64_t)(d.nb - 1) * 32 * W;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) cf[c] = C0[(int64_t)c * W + tid];
-  }
   __syncthreads();
-  for (int blk = d.nb - 1; blk >= 0; --blk) {
+  for (int k = 0; k < d.nb; ++k) {
+    const int blk = d.nb - 1 - k;
     const int64_t J = (int64_t)blk * 32;
     const bool more = blk > 0;
-    double cn[32];
     double fresh = 0.0;
-    if (more && tid < W) {
-      const double* Cn = C + (int64_t)(blk - 1) * 32 * W;
-#pragma unroll
-      for (int c = 0; c < 32; ++c) cn[c] = Cn[(int64_t)c * W + tid];
-    }
     if (tid >= W && tid < W + 32) {  // rows entering below: J - 32 - kv + t
       const int64_t g = J - 32 - kv + (tid - W);
       fresh = g >= 0 ? x[g] : 0.0;
     }
+    const double* cf = feed.wait(R, k);
     if (tid < W) {
-      const double acc = dense_dot32(cf, in + kv);
+      const double acc = dense_dot32(cf + tid, W, in + kv);
       if (tid >= kv) {
         const int64_t row = J + (tid - kv);
         if (row < n) x[row] = acc;
@@ -175,45 +239,64 @@ static __device__ void dense_u_backward(const DenseView& d, double* x, double* w
       out[tid - W] = fresh;
     }
     __syncthreads();
+    feed.issue(R, k + R.ns);
     double* t = in;
     in = out;
     out = t;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) cf[c] = cn[c];
   }
+  feed.finish(R);
 }
 
 // L^T backward: window rows [J, J + wl); the 32 head outputs are reductions
 // over the whole window (parts of 32 inputs per warp, merged in part order),
 // then the block's inverse interchange. part: [8][32] doubles of scratch.
-static __device__ void dense_lt_backward(const DenseView& d, double* x, double* wa, double* wb, double* part) {
+static __device__ void dense_lt_backward(const DenseView& d, double* x, double* wa, double* wb, double* part,
+                                         DenseRing& R) {
   const int tid = threadIdx.x, p = tid >> 5, c = tid & 31;
   const int64_t n = d.n;
   const int W = d.wl, kl = d.kl;
   const int P = (W + 31) >> 5;
-  const double* __restrict__ C = d.clt;
   double* in = wa;
   double* out = wb;
+  const RingFeed feed{d.clt, d.nb - 1, -1, d.nb, (uint32_t)(32 * W * sizeof(double))};
+  feed.start(R);
   {
     const int64_t J = (int64_t)(d.nb - 1) * 32;
     for (int q = tid; q < W; q += kDenseThreads) in[q] = J + q < n ? x[J + q] : 0.0;
   }
-  auto load_cf = [&](int blk, double* cf) {
-    const double* Cb = C + ((int64_t)blk * W + p * 32) * 32 + c;
-#pragma unroll
-    for (int kk = 0; kk < 32; ++kk) cf[kk] = (p < P && p * 32 + kk < W) ? Cb[(int64_t)kk * 32] : 0.0;
-  };
-  double cf[32];
-  load_cf(d.nb - 1, cf);
   __syncthreads();
-  for (int blk = d.nb - 1; blk >= 0; --blk) {
+  for (int k = 0; k < d.nb; ++k) {
+    const int blk = d.nb - 1 - k;
     const int64_t J = (int64_t)blk * 32;
     const bool more = blk > 0;
-    double cn[32];
     double fresh = 0.0;
-    if (more) load_cf(blk - 1, cn);
     if (more && tid < 32) fresh = x[J - 32 + tid];  // rows entering above (J >= 32 here)
-    if (p < P) part[p * 32 + c] = dense_dot32(cf, in + p * 32);
+    const double* cf = feed.wait(R, k);
+    if (p < P) {
+      // inputs k' = p * 32 + kk of this part; coefficient (k', c) at cf[k' * 32 + c]
+      const int kmax = W - p * 32 < 32 ? W - p * 32 : 32;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* cp = cf + (int64_t)p * 32 * 32 + c;
+      const double* ip = in + p * 32;
+      if (kmax == 32) {
+#pragma unroll
+        for (int kk = 0; kk < 32; kk += 4) {
+          a0 = __fma_rn(cp[kk * 32], ip[kk], a0);
+          a1 = __fma_rn(cp[(kk + 1) * 32], ip[kk + 1], a1);
+          a2 = __fma_rn(cp[(kk + 2) * 32], ip[kk + 2], a2);
+          a3 = __fma_rn(cp[(kk + 3) * 32], ip[kk + 3], a3);
+        }
+      } else {
+        for (int kk = 0; kk < kmax; ++kk) {  // same chain assignment as the unrolled form
+          const double t = cp[kk * 32];
+          if ((kk & 3) == 0) a0 = __fma_rn(t, ip[kk], a0);
+          if ((kk & 3) == 1) a1 = __fma_rn(t, ip[kk], a1);
+          if ((kk & 3) == 2) a2 = __fma_rn(t, ip[kk], a2);
+          if ((kk & 3) == 3) a3 = __fma_rn(t, ip[kk], a3);
+        }
+      }
+      part[p * 32 + c] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+    }
     __syncthreads();
     if (tid < W) {
       double v;
@@ -233,17 +316,19 @@ static __device__ void dense_lt_backward(const DenseView& d, double* x, double* 
     }
     if (more && tid < 32) out[tid] = fresh;
     __syncthreads();
+    feed.issue(R, k + R.ns);
     double* t = in;
     in = out;
     out = t;
-#pragma unroll
-    for (int kk = 0; kk < 32; ++kk) cf[kk] = cn[kk];
   }
+  feed.finish(R);
 }
 
 // x := U^-1 L^-1 P x  (transpose: x := P^T L^-T U^-T x), one CTA of
-// kDenseThreads threads; smem: 2 * 256 + 256 doubles.
-__device__ __forceinline__ void dense_solve(const DenseView& d, double* x, double* smem, bool transpose) {
+// kDenseThreads threads. smem: 3 * 256 doubles of window / partial scratch;
+// R: the block ring (dynamic shared memory of the kernel).
+__device__ __forceinline__ void dense_solve(const DenseView& d, double* x, double* smem, DenseRing& R,
+                                            bool transpose) {
   double* wa = smem;
   double* wb = smem + kDenseThreads;
   double* part = smem + 2 * kDenseThreads;
@@ -252,15 +337,39 @@ __device__ __forceinline__ void dense_solve(const DenseView& d, double* x, doubl
   wb[threadIdx.x] = 0.0;
   __syncthreads();
   if (!transpose) {
-    dense_forward<true>(d, d.clf, d.wl, x, wa, wb);
+    dense_forward<true>(d, d.clf, d.wl, x, wa, wb, R);
     __syncthreads();
-    dense_u_backward(d, x, wa, wb);
+    dense_u_backward(d, x, wa, wb, R);
   } else {
-    dense_forward<false>(d, d.cut, d.wu, x, wa, wb);
+    dense_forward<false>(d, d.cut, d.wu, x, wa, wb, R);
     __syncthreads();
-    dense_lt_backward(d, x, wa, wb, part);
+    dense_lt_backward(d, x, wa, wb, part, R);
   }
   __syncthreads();
+}
+
+// Ring of a dense CTA from its dynamic shared memory (dyn, 16-byte aligned,
+// dyn_bytes long): the mbarriers first, then as many stages as fit (<= 4).
+__device__ __forceinline__ DenseRing dense_ring(const DenseView& d, double* dyn, size_t dyn_bytes) {
+  DenseRing R;
+  R.bar = reinterpret_cast<uint64_t*>(dyn);
+  R.buf = dyn + 8;  // 64 bytes of barriers
+  R.stage = dense_ring_stage(d.wl, d.wu);
+  const int64_t fit = ((int64_t)(dyn_bytes / sizeof(double)) - 8) / R.stage;
+  R.ns = (int)(fit < kDenseStagesMax ? fit : kDenseStagesMax);
+  R.count = 0;
+  ring_init(R);
+  return R;
+}
+
+// Dynamic shared memory (bytes) a dense CTA asks for: up to 4 stages within budget.
+inline size_t dense_dyn_smem(int wl, int wu) {
+  const size_t stage = (size_t)dense_ring_stage(wl, wu) * sizeof(double);
+  const size_t budget = 200 * 1024;
+  size_t ns = budget / stage;
+  if (ns > (size_t)kDenseStagesMax) ns = kDenseStagesMax;
+  if (ns < 2) ns = 2;
+  return 64 + ns * stage;
 }
 
 }  // namespace ck
