@@ -428,9 +428,12 @@ def run_ours(args):
     info = dev.info()
     if ensemble:
         # the restarts in groups of restart columns per sweep, as estimate_norm_batch
-        # runs them (restart_group, ck_api.cu: 2 per sweep above 2^24 nonzeros)
+        # runs them (ck_restart_group: the library's own choice)
         ms = batch.member_seeds(configs.CONFIGS[5]["count"])
-        rg = int(os.environ.get("CK_RESTART_GROUP", "0")) or (2 if a.nnz >= (1 << 24) else R)
+        import ctypes  # noqa: PLC0415
+        grp = ctypes.c_int32(0)
+        _lib.check(_lib.load().ck_restart_group(dev.handle, R, 1, ctypes.byref(grp)), "ck_restart_group")
+        rg = grp.value
         groups = [list(range(r0, min(R, r0 + rg))) for r0 in range(0, R, rg)]
         sessions = [batch.BatchSession(packed, cfg, [ms[i] if r == 0 else ck.mix_seed(ms[i], r)
                                                      for i in member_idx for r in g])

@@ -231,6 +231,10 @@ ck_status ck_lu_export_csr(ck_lu f, int64_t* l_rp, int32_t* l_ci, double* l_va, 
 /* lu_solve (lu.hpp:180-202): x = A^-1 b; lu_transpose_solve (lu.hpp:207-227): x = A^-T b. */
 ck_status ck_lu_solve(ck_lu f, const double* b, double* x);
 ck_status ck_lu_transpose_solve(ck_lu f, const double* b, double* x);
+/* Restart columns that share one sweep of the operator in ck_estimate_norm (batch = 0)
+ * and ck_estimate_norm_batch (batch = 1): estimate_norm's restarts (condest.hpp:301-312)
+ * are independent runs, grouped for throughput only. */
+ck_status ck_restart_group(ck_matrix a, uint64_t restarts, int32_t batch, int32_t* group);
 /* The dense-block sweeps the InverseOracle loop runs on narrow bands
  * (max(kl, kl + ku) <= 192; same solves as ck_lu_solve / ck_lu_transpose_solve,
  * lu.hpp:180-227, with the 32 x 32 head triangles of every block inverted once

@@ -93,6 +93,7 @@ _SIGS = {
     "ck_lu_csr_info": (C.c_int, [C.c_void_p, i64p, i64p]),
     "ck_lu_export_csr": (C.c_int, [C.c_void_p, i64p, i32p, dp, i64p, i32p, dp, i64p]),
     "ck_lu_solve": (C.c_int, [C.c_void_p, dp, dp]),
+    "ck_restart_group": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.POINTER(C.c_int32)]),
     "ck_lu_dense_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), dp]),
     "ck_lu_dense_solve": (C.c_int, [C.c_void_p, C.c_int32, dp, dp]),
     "ck_lu_transpose_solve": (C.c_int, [C.c_void_p, dp, dp]),

@@ -71,9 +71,23 @@ struct Tune {
 // registers, so their chunks are wider (config 5, scripts/ab_win.sh).
 template <int R>
 struct WinTune {
-  static constexpr int apply_u = R == 4 ? 16 : 8;
+  static constexpr int apply_u = 8;
   static constexpr int apply_occ = R == 1 ? 4 : R == 4 ? 2 : 3;
+  static constexpr int transpose_u = R == 4 ? 8 : Tune<R>::transpose_u;
+  static constexpr int transpose_occ = R == 4 ? 3 : Occ<R>::transpose;
 };
+
+// Window ring of the banded-ensemble sweeps: element (ring position q in
+// [0, 4 * kTile), column r). Column pairs form planes of 16-byte slots, so the
+// gather of a row's pair is one 16-byte read whose 8 lanes per wavefront spread
+// over all 8 slots of the bank row (a [q][R] layout with R = 4 reaches 4).
+template <int R>
+__device__ __forceinline__ int win_idx(int q, int r) {
+  if constexpr (R % 2 == 0)
+    return ((r >> 1) * 4 * kTile + q) * 2 + (r & 1);
+  else
+    return q * R + r;
+}
 
 // Work assignment of CTA `unit`. One operator (S == 1): the tiles are dealt
 // round-robin over the grid, so at any moment the resident CTAs sweep one
@@ -205,7 +219,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
   // t, t+1 that tile t's entries reference sits in a four-tile shared-memory
   // ring, each element computed once and staged one tile ahead; the gathers
   // are shared-memory reads.
-  __shared__ double s_win[WIN ? 4 * kTile * R : 1];
+  __shared__ __align__(16) double s_win[WIN ? 4 * kTile * R : 2];
   int m0 = 0, m1 = 0;
   auto win_load = [&](int q, double2* pr) {  // row q * kTile + tid of the live buffer
     const bool in = q >= m0 && q < m1;
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
   auto win_store = [&](int q, const double2* pr) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      s_win[((q & 3) * kTile + threadIdx.x) * R + r] = act[r] ? xtilde(pr[r], rad[r]) : 0.0;
+      s_win[win_idx<R>((q & 3) * kTile + threadIdx.x, r)] = act[r] ? xtilde(pr[r], rad[r]) : 0.0;
   };
   if (WIN) {
     m0 = a.seg_t0[seg];
@@ -265,7 +279,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
       if (i < a.nc) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (act[r]) dd_add_sq(dd[r], s_win[((tile & 3) * kTile + threadIdx.x) * R + r]);
+          if (act[r]) dd_add_sq(dd[r], s_win[win_idx<R>((tile & 3) * kTile + threadIdx.x, r)]);
       }
     } else if (i < a.nc) {  // own column-space element: ||x~||^2 (and observer stats)
 #pragma unroll
@@ -291,13 +305,25 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
         if (WIN) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const double* xw = s_win + (c[u] & (4 * kTile - 1)) * R;
+            const int qw = c[u] & (4 * kTile - 1);
             CK_DASSERT(!(j0 + u < Lc) || ((c[u] >> 8) >= max(tile - 1, m0) && (c[u] >> 8) <= tile + 1 &&
                                           (c[u] >> 8) < m1));
             if (j0 + u < Lc) {
+              double xv[R];
+              if constexpr (R % 2 == 0) {  // a row's column pair is one 16-byte read
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                  const double2 t = *reinterpret_cast<const double2*>(s_win + win_idx<R>(qw, r));
+                  xv[r] = t.x;
+                  xv[r + 1] = t.y;
+                }
+              } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) xv[r] = s_win[win_idx<R>(qw, r)];
+              }
 #pragma unroll
               for (int r = 0; r < R; ++r)
-                if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xw[r]));
+                if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], xv[r]));
             }
           }
         } else {
@@ -436,7 +462,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
 #pragma unroll
   for (int r = 0; r < R; ++r) dot[r] = 0.0;
   // WIN: y' of the row tiles t-1, t, t+1 in a four-tile shared-memory ring (see k_apply)
-  __shared__ double s_win[WIN ? 4 * kTile * R : 1];
+  __shared__ __align__(16) double s_win[WIN ? 4 * kTile * R : 2];
   int m0 = 0, m1 = 0;
   auto win_load = [&](int q, double* yr) {
     const bool in = q >= m0 && q < m1;
@@ -445,7 +471,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
   };
   auto win_store = [&](int q, const double* yr) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) s_win[((q & 3) * kTile + threadIdx.x) * R + r] = yr[r];
+    for (int r = 0; r < R; ++r) s_win[win_idx<R>((q & 3) * kTile + threadIdx.x, r)] = yr[r];
   };
   if (WIN) {
     m0 = a.seg_t0[seg];
@@ -490,13 +516,25 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
       if (WIN) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const double* yw = s_win + (c[u] & (4 * kTile - 1)) * R;
+          const int qw = c[u] & (4 * kTile - 1);
           CK_DASSERT(!(j0 + u < Lc) || ((c[u] >> 8) >= max(tile - 1, m0) && (c[u] >> 8) <= tile + 1 &&
                                         (c[u] >> 8) < m1));
           if (j0 + u < Lc) {
+            double yv[R];
+            if constexpr (R % 2 == 0) {
+#pragma unroll
+              for (int r = 0; r < R; r += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(s_win + win_idx<R>(qw, r));
+                yv[r] = t.x;
+                yv[r + 1] = t.y;
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < R; ++r) yv[r] = s_win[win_idx<R>(qw, r)];
+            }
 #pragma unroll
             for (int r = 0; r < R; ++r)
-              if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], yw[r]));
+              if (act[r]) acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u], yv[r]));
           }
         }
       } else {
@@ -679,6 +717,12 @@ __global__ void k_tile_reach(SellView A, int64_t nrows_pad, int* out) {
 
 static unsigned grid256(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
 
+static int tile_reach(const Sell& m, cudaStream_t st);
+// Every entry of A and A^T within one tile of its row: the window sweeps apply.
+bool matrix_window_ok(ck_matrix_s* m) {
+  return tile_reach(m->a, m->stream) <= 1 && tile_reach(m->at, m->stream) <= 1;
+}
+
 static int tile_reach(const Sell& m, cudaStream_t st) {
   static_assert(kTile == 256, "k_tile_reach shifts by 8");
   DBuf<int> d(1);
@@ -715,9 +759,11 @@ template <int R>
 static void launch_transpose_r(const ck_session_s* s, cudaStream_t st) {
   if (s->args.win) {
     if (s->A->at.narrow)
-      k_transpose<R, true, true><<<s->args.units_T, kTile, 0, st>>>(s->args);
+      k_transpose<R, true, true, WinTune<R>::transpose_u, WinTune<R>::transpose_occ>
+          <<<s->args.units_T, kTile, 0, st>>>(s->args);
     else
-      k_transpose<R, false, true><<<s->args.units_T, kTile, 0, st>>>(s->args);
+      k_transpose<R, false, true, WinTune<R>::transpose_u, WinTune<R>::transpose_occ>
+          <<<s->args.units_T, kTile, 0, st>>>(s->args);
     return;
   }
   if (s->A->at.narrow)

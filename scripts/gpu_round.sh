@@ -19,3 +19,4 @@ ncu --set full --clock-control none --import-source on -k regex:'k_apply|k_trans
 ncu --set full --clock-control none --import-source on -k regex:'k_apply|k_transpose' -s 10 -c 2 -f -o $O/${TAG}_full_c5 \
   python bench.py --config 5 --steps 10 --warmup 3 --no-e2e --no-cpu > $O/${TAG}_ncu_full_c5.log 2>&1
 ls -la $O
+CK_TRACE=1 python scripts/trace_e2e.py 4 > $O/${TAG}_trace_e2e_c4.txt 2>&1

@@ -3,6 +3,8 @@ on config 4); run with CK_TRACE=1 for the native phase marks."""
 import sys
 import time
 
+import sys
+sys.path.insert(0, ".")
 import paper_2409_11515_b200 as ck
 from paper_2409_11515_b200 import _lib, configs
 
