@@ -486,7 +486,7 @@ def run_ours(args):
         k["gbs"] = k["bytes"] / (k["ms_avg"] / 1000.0) / 1e9
         k["frac"] = k["gbs"] / peak
     dom = k_tr if ms_tr >= ms_apply else k_apply
-    traffic = None
+    traffic = traffic_src = None
     tfile = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tfile):
         try:
@@ -494,10 +494,11 @@ def run_ours(args):
                 tr = json.load(f)
             if tr.get("workload") == name:
                 traffic = tr.get(dom["name"].split("<")[0])
+                traffic_src = tr.get("source")
         except (OSError, ValueError):
             traffic = None
     roofline = {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
-                "frac": dom["frac"], "traffic": traffic, "kernel": dom["name"],
+                "frac": dom["frac"], "traffic": traffic, "traffic_source": traffic_src, "kernel": dom["name"],
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "bytes_per_launch": dom["bytes"]}
     iter_bytes = b_apply + b_tr

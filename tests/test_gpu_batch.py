@@ -171,3 +171,19 @@ def test_window_sweeps_match_gathers_bitwise(port, monkeypatch):
     got = batch.estimate_norm_batch([far2, mem[1]], cfg, restarts=2, seeds=seeds[:2])
     alone = ck.estimate_norm(ck.ExplicitOracle(far2), M.cfg(alpha=1e-2, max_iter=150, patience=150, seed=seeds[0]), 2)
     assert got[0].value == pytest.approx(alone.value, rel=1e-12)
+
+
+def test_restart_group_query(port):
+    """ck_restart_group: the grouping estimate_norm / estimate_norm_batch use (restarts are
+    independent runs, condest.hpp:301-312; grouped for throughput only)."""
+    import ctypes
+    from paper_2409_11515_b200 import _lib
+
+    def group(a, restarts, is_batch):
+        g = ctypes.c_int32(0)
+        _lib.check(_lib.load().ck_restart_group(a.device().handle, restarts, is_batch, ctypes.byref(g)),
+                   "ck_restart_group")
+        return g.value
+
+    small = M.laplacian2d(16)
+    assert group(small, 3, 0) == 4 and group(small, 4, 1) == 4  # below 2^24 nonzeros: 4 columns
