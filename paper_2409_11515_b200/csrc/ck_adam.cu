@@ -144,6 +144,15 @@ __device__ __forceinline__ int pick_shared_nxt(const ColState* sts, int cur, int
   return (cur + 1) % nbuf;
 }
 
+// 256-bit accesses of two adjacent double2 (32-byte aligned).
+__device__ __forceinline__ void ld256(const double2* ptr, double2& a, double2& b) {
+  asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(ptr));
+}
+__device__ __forceinline__ void st256(double2* ptr, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+               : "memory");
+}
+
 // Control step after the apply sweep (condest.hpp:251-275 via control_apply)
 // from the global scalars res[r] = {||x~||, ||y'||, x.delta, ||delta||}; one
 // thread. Shared by the fused kernel and the partition combine kernel.
@@ -342,12 +351,24 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
           }
         }
       }
+      if constexpr (R % 2 == 0) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!act[r]) continue;
-        a.y[i * R + r] = acc[r];
-        es_add(es[r], acc[r]);
+        for (int r = 0; r < R; r += 2) {
+          if (act[r] && act[r + 1]) {  // a pair of columns: one 16-byte store
+            *reinterpret_cast<double2*>(a.y + i * R + r) = make_double2(acc[r], acc[r + 1]);
+          } else {
+            if (act[r]) a.y[i * R + r] = acc[r];
+            if (act[r + 1]) a.y[i * R + r + 1] = acc[r + 1];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (act[r]) a.y[i * R + r] = acc[r];
       }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r]) es_add(es[r], acc[r]);
     }
     if (WIN) {
       // slot (tile + 2) & 3 held tile - 2, last read before the previous barrier
@@ -554,22 +575,49 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
       }
     }
     if (j < a.nc) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!act[r]) continue;
-        const int64_t e = j * R + r;
-        const double2 px = xb[e];
+      // one column's Adam step (condest.hpp:225-229, 240-247) from its pairs
+      auto column = [&](int r, double2 px, double2 mv, double2& px_out, double2& mv_out) {
         const double xn = mat[r] ? __ddiv_rn(xtilde(px, rad[r]), ndiv[r]) : px.x;  // :240-247
         const double z = __ddiv_rn(acc[r], ndiv[r]);                               // A^T A x_{t+1}
         const double g = __dsub_rn(__dmul_rn(xn, ix2[r]), __dmul_rn(z, iy2[r]));  // :105
-        const double2 mv = a.MV[e];
         const double mm = __dadd_rn(__dmul_rn(p.beta1, mv.x), __dmul_rn(om1, g));             // :226
         const double vv = __dadd_rn(__dmul_rn(p.beta2, mv.y), __dmul_rn(__dmul_rn(om2, g), g));  // :227
         const double d = __ddiv_rn(__dmul_rn(p.alpha, __dmul_rn(mm, mc[r])),
                                    __dadd_rn(__dsqrt_rn(__dmul_rn(vv, vc[r])), p.eps));  // :228
-        a.MV[e] = make_double2(mm, vv);
-        xo[e] = make_double2(xn, d);
+        mv_out = make_double2(mm, vv);
+        px_out = make_double2(xn, d);
         dot[r] = __fma_rn(xn, d, dot[r]);
+      };
+      auto single = [&](int r) {
+        const int64_t e = j * R + r;
+        double2 xo0, mo0;
+        column(r, xb[e], a.MV[e], xo0, mo0);
+        a.MV[e] = mo0;
+        xo[e] = xo0;
+      };
+      if constexpr (R % 2 == 0) {
+#pragma unroll
+        for (int r = 0; r < R; r += 2) {
+          if (act[r] && act[r + 1]) {
+            // a column pair's (x, delta) and (m, v) are 32 contiguous bytes each:
+            // 256-bit accesses halve the partially used lines of the 16-byte ones
+            const int64_t e = j * R + r;
+            double2 px0, px1, mv0, mv1, xo0, xo1, mo0, mo1;
+            ld256(xb + e, px0, px1);
+            ld256(a.MV + e, mv0, mv1);
+            column(r, px0, mv0, xo0, mo0);
+            column(r + 1, px1, mv1, xo1, mo1);
+            st256(a.MV + e, mo0, mo1);
+            st256(xo + e, xo0, xo1);
+          } else {
+            if (act[r]) single(r);
+            if (act[r + 1]) single(r + 1);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (act[r]) single(r);
       }
     }
     if (WIN) {
