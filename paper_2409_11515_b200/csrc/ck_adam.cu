@@ -232,9 +232,17 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
   int m0 = 0, m1 = 0;
   auto win_load = [&](int q, double2* pr) {  // row q * kTile + tid of the live buffer
     const bool in = q >= m0 && q < m1;
+    const double2* row = xb + ((int64_t)q * kTile + threadIdx.x) * R;
+    if constexpr (R % 2 == 0) {  // a column pair's (x, delta) pairs: one 256-bit load
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      pr[r] = in ? xb[((int64_t)q * kTile + threadIdx.x) * R + r] : make_double2(0.0, 0.0);
+      for (int r = 0; r < R; r += 2) {
+        pr[r] = pr[r + 1] = make_double2(0.0, 0.0);
+        if (in) ld256(row + r, pr[r], pr[r + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) pr[r] = in ? row[r] : make_double2(0.0, 0.0);
+    }
   };
   auto win_store = [&](int q, const double2* pr) {
 #pragma unroll
