@@ -18,9 +18,12 @@
 // A x_{t+1} is computed once per iteration and serves both the loss of
 // iteration t and the gradient of iteration t+1 (the reference evaluates it
 // twice on bitwise-identical input). The best iterate is tracked by rotating
-// three iterate buffers instead of copying x_min (:264-267). R independent runs
+// R + 2 iterate buffers instead of copying x_min (:264-267). R independent runs
 // (restarts, :301-312) share one sweep over the matrix as columns of a
-// multi-vector; each column's arithmetic is independent of R.
+// multi-vector; each column's arithmetic is independent of R. The columns
+// rotate their buffers in lockstep (shared_cur / pick_shared_nxt), so a row's R
+// (x, delta) pairs are contiguous. Banded ensembles (config 5) sweep from a
+// sliding shared-memory window of x~ / y' (WIN).
 //
 // Layout: (x, delta) and (m, v) are stored as double2 pairs, so the SpMV gather
 // of x~ is one 16-byte load and the Adam update moves 16-byte vectors.

@@ -9,6 +9,9 @@
 //
 // State layout and control are those of the explicit path (ck_adam.cu), so the
 // host session, restarts, best tracking and observer mode are shared.
+// Two step kernels: k_inv_step (substitution sweeps, ck_lu_sweeps.cuh; any band,
+// 1..4 columns, optional cluster split) and k_inv_step_dense (narrow bands, one
+// column: dense-block sweeps, ck_lu_dense.cuh).
 #include <cmath>
 #include <cooperative_groups.h>
 #include <cstdlib>

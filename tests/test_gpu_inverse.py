@@ -274,7 +274,8 @@ def test_cluster_sweeps_several_columns(port, monkeypatch):
         assert e8.value == pytest.approx(e1.value, rel=1e-12)
 
 
-@pytest.mark.parametrize("kind", ["random40", "laplacian24", "banded700", "rowscaled64", "odd1000", "tiny3"])
+@pytest.mark.parametrize("kind", ["random40", "laplacian24", "banded700", "rowscaled64", "odd1000", "tiny3",
+                                  "limit190"])
 def test_dense_block_sweeps_match_substitution(port, kind):
     """Narrow bands: the InverseOracle loop sweeps with the inverted 32 x 32 head
     triangles (ck_lu_dense.cuh). Same solves as lu_solve / lu_transpose_solve
@@ -285,6 +286,7 @@ def test_dense_block_sweeps_match_substitution(port, kind):
          "banded700": lambda: _banded(700, 45, 2),
          "rowscaled64": lambda: M.row_scaled(M.laplacian2d(64), port, 1),
          "odd1000": lambda: _banded(1003, 70, 5),
+         "limit190": lambda: _banded(900, 95, 9),  # kl + ku = 190: the widest band of the dense path
          "tiny3": lambda: M.diag_matrix([5.0, 3.0, 8.0])}[kind]()
     f = ck.lu_factorize(a, 1e-14)
     rf = port.lu_factorize(a, 1e-14)
