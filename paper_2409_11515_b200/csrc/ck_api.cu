@@ -34,6 +34,9 @@ void fail(ck_status c, const std::string& msg) { throw Error(c, msg); }
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaSuccess) return;
+  // the error is reported through the status / exception: clear the runtime's
+  // per-thread "last error" so it does not resurface in an unrelated later call
+  cudaGetLastError();
   std::string m = std::string(what) + " failed: " + cudaGetErrorString(e) + " (" + file + ":" +
                   std::to_string(line) + ")";
   if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) throw Error(CK_ERR_NO_DEVICE, m);
@@ -248,6 +251,119 @@ void random_unit_vector_host(void* engine, int64_t n, double* out,
   });
 }
 
+// Device allocations from the default stream-ordered pool (ck_common.h).
+// CK_PLAIN_MALLOC=1 goes back to cudaMalloc / cudaFree (A/B switch).
+namespace {
+bool use_pool() {
+  static const bool on = std::getenv("CK_PLAIN_MALLOC") == nullptr;
+  return on;
+}
+void pool_configure_once(int dev) {
+  static std::mutex mu;
+  static std::vector<char> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)done.size() <= dev) done.resize(dev + 1, 0);
+  if (done[dev]) return;
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;  // freed blocks stay in the pool until device_trim()
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[dev] = 1;
+}
+}  // namespace
+
+cudaError_t device_alloc(void** p, size_t bytes) {
+  if (!use_pool()) return cudaMalloc(p, bytes);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  pool_configure_once(dev);
+  e = cudaMallocAsync(p, bytes, cudaStreamPerThread);
+  if (e == cudaErrorMemoryAllocation) {  // cached blocks of other sizes in the way: release them and retry
+    cudaGetLastError();
+    device_trim();
+    e = cudaMallocAsync(p, bytes, cudaStreamPerThread);
+  }
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(cudaStreamPerThread);  // usable on every stream from here on
+}
+
+void device_free(void* p) {
+  if (p == nullptr) return;
+  if (!use_pool()) {
+    cudaFree(p);
+    return;
+  }
+  cudaDeviceSynchronize();  // cudaFree's implicit wait: no stream may still use the block
+  cudaFreeAsync(p, cudaStreamPerThread);
+}
+
+void device_trim() {
+  if (!use_pool()) return;
+  int dev = 0;
+  cudaMemPool_t pool = nullptr;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+  cudaGetLastError();
+}
+
+// Process-wide cache of released pinned staging buffers (ck_common.h).
+namespace {
+struct PinnedCache {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> free_list;  // never freed at exit: the driver may be gone
+};
+PinnedCache& pinned_cache() {
+  static PinnedCache* c = new PinnedCache();
+  return *c;
+}
+constexpr size_t kPinnedCacheBuffers = 2;
+constexpr size_t kPinnedCacheBytes = size_t(1) << 30;
+}  // namespace
+
+void* pinned_acquire(size_t bytes, size_t* got_bytes) {
+  {
+    PinnedCache& c = pinned_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    int best = -1;
+    for (int i = 0; i < (int)c.free_list.size(); ++i)  // smallest cached buffer that fits
+      if (c.free_list[i].second >= bytes && (best < 0 || c.free_list[i].second < c.free_list[best].second))
+        best = i;
+    if (best >= 0) {
+      void* p = c.free_list[best].first;
+      *got_bytes = c.free_list[best].second;
+      c.free_list.erase(c.free_list.begin() + best);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  *got_bytes = bytes;
+  return p;
+}
+
+void pinned_release(void* p, size_t bytes) {
+  if (p == nullptr) return;
+  {
+    PinnedCache& c = pinned_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    size_t total = bytes;
+    for (auto& e : c.free_list) total += e.second;
+    if (c.free_list.size() < kPinnedCacheBuffers && total <= kPinnedCacheBytes) {
+      c.free_list.emplace_back(p, bytes);
+      return;
+    }
+  }
+  cudaFreeHost(p);
+}
+
 // ck_start_vector_prefetch's slot: one start vector drawn on a helper thread
 // into pageable scratch, then normalised into a pinned buffer (the session
 // adopts that buffer as its staging).
@@ -412,6 +528,7 @@ ck_status ck_device_count(int32_t* count) {
 ck_status ck_device_memory(uint64_t* free_bytes, uint64_t* total_bytes, int32_t* sm_count) {
   return guarded(__func__, [&] {
     size_t f = 0, t = 0;
+    device_trim();  // cached pool blocks count as free
     CK_CUDA(cudaMemGetInfo(&f, &t));
     int dev = 0, sms = 0;
     CK_CUDA(cudaGetDevice(&dev));
@@ -444,7 +561,12 @@ ck_status ck_device_synchronize(void) {
 ck_status ck_host_register(void* ptr, uint64_t bytes) {
   return guarded(__func__, [&] {
     if (bytes == 0) return;
-    CK_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+    const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {  // pinned already: nothing to do
+      cudaGetLastError();
+      return;
+    }
+    CK_CUDA(e);
   });
 }
 

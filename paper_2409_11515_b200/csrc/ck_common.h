@@ -64,7 +64,14 @@ struct Trace {
   }
 };
 
-// Page-locked host buffer (staging of start vectors and witnesses).
+// Page-locked host staging memory (start vectors, witnesses). Pinning costs
+// ~0.5 ms per MB and holds the driver while it runs -- at config 4 the 200 MB
+// start-vector buffer stalls the concurrent operator build by ~0.1 s -- so
+// released buffers are kept in a small process-wide cache (ck_api.cu: at most
+// two buffers, 1 GiB in total) and the next session reuses them.
+void* pinned_acquire(size_t bytes, size_t* got_bytes);  // nullptr: allocation failed
+void pinned_release(void* p, size_t bytes);
+
 template <class T>
 struct PinnedBuf {
   T* p = nullptr;
@@ -76,20 +83,29 @@ struct PinnedBuf {
   void resize(int64_t count) {
     if (count <= n) return;
     reset();
-    if (cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count)) != cudaSuccess) {
-      cudaGetLastError();
-      p = nullptr;
-      fail(CK_ERR_OUT_OF_MEMORY, "cudaMallocHost failed");
-    }
-    n = count;
+    size_t got = 0;
+    p = static_cast<T*>(pinned_acquire(sizeof(T) * static_cast<size_t>(count), &got));
+    if (p == nullptr) fail(CK_ERR_OUT_OF_MEMORY, "cudaMallocHost failed");
+    n = static_cast<int64_t>(got / sizeof(T));
   }
   void reset() {
-    if (p) cudaFreeHost(p);
+    if (p) pinned_release(p, sizeof(T) * static_cast<size_t>(n));
     p = nullptr;
     n = 0;
   }
   T* data() { return p; }
 };
+
+// Device memory comes from the device's stream-ordered pool with the release
+// threshold lifted (ck_api.cu): an upload allocates ~14 GB and frees ~8 GB of
+// sort scratch at config 4, and plain cudaMalloc / cudaFree of that size
+// sporadically stall for 0.1-0.8 s (measured inside the A^T build). The
+// semantics of the plain calls are kept: the pointer is usable on any stream
+// when device_alloc returns, and device_free waits for the device first.
+// device_trim() hands cached memory back (before cudaMemGetInfo decisions).
+cudaError_t device_alloc(void** p, size_t bytes);
+void device_free(void* p);
+void device_trim();
 
 // Device buffer with RAII.
 template <class T>
@@ -111,16 +127,18 @@ struct DBuf {
     reset();
     n = count;
     if (count > 0) {
-      cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count));
+      cudaError_t e = device_alloc(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count));
       if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
-        fail(CK_ERR_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(sizeof(T) * count) + " bytes failed");
+        p = nullptr;
+        n = 0;
+        fail(CK_ERR_OUT_OF_MEMORY, "device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed");
       }
       CK_CUDA(e);
     }
   }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) device_free(p);
     p = nullptr;
     n = 0;
   }

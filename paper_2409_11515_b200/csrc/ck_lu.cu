@@ -811,6 +811,7 @@ static void lu_prepare(ck_lu_s* f, ck_matrix_s* m) {
   const double lb_b = (double)ceil_div(n, kLUBlock) * kLUBlock * (double)(kLUBlock + f->kl) * 8.0;
   const double aux_b = (double)ldab * (double)n / 8.0 + (double)kw * (double)ldab * 4.0 + 16.0 * n;
   size_t freeb = 0, totalb = 0;
+  device_trim();  // cached pool blocks count as free
   CK_CUDA(cudaMemGetInfo(&freeb, &totalb));
   if ((band_b + lb_b + aux_b) * 1.05 > (double)freeb)
     fail(CK_ERR_OUT_OF_MEMORY, "band LU storage (" + std::to_string((band_b + lb_b + aux_b) / 1e9) +

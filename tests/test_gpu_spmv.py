@@ -144,3 +144,21 @@ def test_adam_identical_across_column_formats(port, monkeypatch):
     assert e1.iterations == e2.iterations
     assert e1.value == e2.value
     assert np.array_equal(e1.witness, e2.witness)
+
+
+def test_cuda_errors_do_not_linger(port):
+    """A CUDA error reported by one call must not resurface in the next (the runtime's
+    per-thread last error is cleared), and pinning a pinned range again is benign."""
+    import ctypes
+    from paper_2409_11515_b200 import _lib
+    lib = _lib.load()
+    _lib.ensure_device()
+    buf = np.arange(1 << 16, dtype=np.float64)
+    assert lib.ck_host_register(buf.ctypes.data, buf.nbytes) == 0
+    assert lib.ck_host_register(buf.ctypes.data, buf.nbytes) == 0  # already registered
+    other = np.zeros(16)
+    assert lib.ck_host_unregister(ctypes.c_void_p(other.ctypes.data)) != 0  # never registered: an error...
+    a = M.laplacian2d(12)
+    x = port.random_unit_vectors(2, a.ncols)[0]
+    assert np.array_equal(ck.matvec(a, x), port.matvec(a, x))  # ...that the next call does not see
+    assert lib.ck_host_unregister(ctypes.c_void_p(buf.ctypes.data)) == 0
