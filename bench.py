@@ -515,6 +515,9 @@ def run_ours(args):
                 regs.append(arr)
         e2e_iters = args.e2e_iters
         cfg2 = configs.baseline_adam(seed, max_iter=e2e_iters)
+        # the device copy of the device-timed part is released first: the call below is a
+        # process's second norm2 of the operator (warm modules, allocator pool, pinned cache)
+        a.release_device()
         barrier()
         t0 = time.perf_counter()
         est = ck.norm2(a2, cfg2)  # upload (A, A^T build) + x0 + loop + witness check + D2H
