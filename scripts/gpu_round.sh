@@ -20,3 +20,5 @@ ncu --set full --clock-control none --import-source on -k regex:'k_apply|k_trans
   python bench.py --config 5 --steps 10 --warmup 3 --no-e2e --no-cpu > $O/${TAG}_ncu_full_c5.log 2>&1
 ls -la $O
 CK_TRACE=1 python scripts/trace_e2e.py 4 > $O/${TAG}_trace_e2e_c4.txt 2>&1
+python bench.py --partition --steps 100 --warmup 5 --no-cpu --no-e2e > $O/${TAG}_bench_partition_ws1.json 2> $O/${TAG}_part.err; tail -c 400 $O/${TAG}_bench_partition_ws1.json
+python __graft_entry__.py > $O/${TAG}_smoke.txt 2>&1; tail -1 $O/${TAG}_smoke.txt
