@@ -138,8 +138,10 @@ def bytes_per_iteration(nnz: int, n: int, R: int = 1, col_format: int = 0):
     # A^T, y (8), x m v delta (32) and writes x m v delta (32). Wide: 24 nnz + 96 n
     # per column (SURVEY.md 8d B_iter); narrow: 20 nnz + 96 n. R restart columns
     # share the matrix sweeps.
-    ea = 10 if col_format & 1 else 12
-    et = 10 if col_format & 2 else 12
+    # With the pattern dictionary (bits 2 / 3) the offsets of a slice come from a small
+    # shared table (cache resident: a few hundred patterns), 8 B per stored nonzero.
+    ea = 8 if col_format & 4 else 10 if col_format & 1 else 12
+    et = 8 if col_format & 8 else 10 if col_format & 2 else 12
     return ea * nnz + 24 * n * R, et * nnz + 72 * n * R
 
 
@@ -559,7 +561,9 @@ def run_ours(args):
                        "parallelism": (f"members sharded over {world} ranks" if ensemble else
                                        f"replicas{world} (independent restart streams)"),
                        "col_format": {0: "int32", 1: "A uint16", 2: "A^T uint16",
-                                      3: "uint16 offsets"}[info["col_format"]],
+                                      3: "uint16 offsets"}[info["col_format"] & 3] +
+                                     (" from a pattern dictionary (8 B per stored entry)"
+                                      if info["col_format"] & 12 == 12 else ""),
                        "l2": f"inputs larger than L2 ({(b_apply + b_tr) / 1e9:.1f} GB moved "
                              f"per iteration vs 126 MB L2); no flush needed",
                        "sell_padding": (info["sell_entries_a"] - nnz) / max(nnz, 1)},

@@ -79,7 +79,10 @@ typedef struct {
   int32_t device;
   /* column-index format of the device layouts: bit0 = A narrow, bit1 = A^T
    * narrow (uint16 offsets from a per-slice base, 10 B per stored entry with
-   * the value; otherwise int32, 12 B). */
+   * the value; otherwise int32, 12 B); bit2 / bit3 = the narrow offsets of A /
+   * A^T come from a dictionary of repeating slice patterns (stencil operators:
+   * 8 B per stored entry from HBM). Same columns in the same order in every
+   * format. */
   int32_t col_format;
 } ck_matrix_info;
 

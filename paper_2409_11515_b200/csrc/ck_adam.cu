@@ -274,16 +274,18 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
   }
   int64_t i = (int64_t)tile0 * kTile + threadIdx.x;
   const int64_t istep = (int64_t)stride * kTile;
-  int64_t sp0 = 0, sp1 = 0;
+  int64_t sp0 = 0, sp1 = 0, po = 0;
   int L = 0, cb = 0;
   if (tile0 < tend && i < a.nr_pad) {
     sp0 = a.A.sp[i >> 5];
     sp1 = a.A.sp[(i >> 5) + 1];
     L = a.A.len[i];
     cb = slice_cbase<NW>(a.A, i >> 5);
+    po = sell_colbase(a.A, i >> 5, i, sell_rowbase(sp0, i));
   }
   for (int tile = tile0; tile < tend; tile += stride, i += istep) {
     const int64_t base = sell_rowbase(sp0, i);
+    const int64_t cbase0 = NW ? po : base;
     const int w = (int)((sp1 - sp0) >> 5);  // slice width: uniform across the warp
     const int Lc = L, cbc = cb;
     const int64_t inext = i + istep;
@@ -292,6 +294,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
       sp1 = a.A.sp[(inext >> 5) + 1];
       L = a.A.len[inext];
       cb = slice_cbase<NW>(a.A, inext >> 5);
+      po = sell_colbase(a.A, inext >> 5, inext, sell_rowbase(sp0, inext));
     }
     double2 ahead[R];
     if (WIN && tile + 1 < tend) win_load(tile + 2, ahead);  // needed by the next tile
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_apply(const __grid_constant__ Lo
       for (int j0 = 0; j0 < w; j0 += U) {
         int c[U];
         double v[U];
-        load_chunk<U, NW>(a.A, base, cbc, j0, w, c, v);
+        load_chunk<U, NW>(a.A, base, cbase0, cbc, j0, w, c, v);
         if (WIN) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -517,16 +520,18 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
   }
   const int64_t jstep = (int64_t)stride * kTile;
   int64_t j = (int64_t)tile0 * kTile + threadIdx.x;
-  int64_t sp0 = 0, sp1 = 0;
+  int64_t sp0 = 0, sp1 = 0, po = 0;
   int L = 0, cb = 0;
   if (tile0 < tend) {
     sp0 = a.AT.sp[j >> 5];
     sp1 = a.AT.sp[(j >> 5) + 1];
     L = a.AT.len[j];
     cb = slice_cbase<NW>(a.AT, j >> 5);
+    po = sell_colbase(a.AT, j >> 5, j, sell_rowbase(sp0, j));
   }
   for (int tile = tile0; tile < tend; tile += stride, j += jstep) {
     const int64_t base = sell_rowbase(sp0, j);
+    const int64_t cbase0 = NW ? po : base;
     const int w = (int)((sp1 - sp0) >> 5);
     const int Lc = L, cbc = cb;
     if (tile + stride < tend) {
@@ -535,6 +540,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
       sp1 = a.AT.sp[(jn >> 5) + 1];
       L = a.AT.len[jn];
       cb = slice_cbase<NW>(a.AT, jn >> 5);
+      po = sell_colbase(a.AT, jn >> 5, jn, sell_rowbase(sp0, jn));
     }
     double ahead[R];
     if (WIN && tile + 1 < tend) win_load(tile + 2, ahead);
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(kTile, OCC) k_transpose(const __grid_constant_
     for (int j0 = 0; j0 < w; j0 += U) {
       int c[U];
       double v[U];
-      load_chunk<U, NW>(a.AT, base, cbc, j0, w, c, v);
+      load_chunk<U, NW>(a.AT, base, cbase0, cbc, j0, w, c, v);
       if (WIN) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {

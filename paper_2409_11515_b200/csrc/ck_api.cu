@@ -699,11 +699,13 @@ void matrix_info(const ck_matrix_s* a, ck_matrix_info* info) {
   info->sell_entries_at = a->at.entries;
   auto sb = [](const Sell& s) {
     return s.slice_ptr.bytes() + s.len.bytes() + s.col.bytes() + s.col16.bytes() + s.cbase.bytes() +
+           s.ptab.bytes() + s.poff.bytes() +
            s.val.bytes() + s.perm.bytes() + s.inv.bytes();
   };
   info->device_bytes = sb(a->a) + sb(a->at);
   info->device = a->device;
-  info->col_format = (a->a.narrow ? 1 : 0) | (a->at.narrow ? 2 : 0);
+  info->col_format = (a->a.narrow ? 1 : 0) | (a->at.narrow ? 2 : 0) | (a->a.pattern ? 4 : 0) |
+                     (a->at.pattern ? 8 : 0);
 }
 }  // namespace ck
 

@@ -221,7 +221,14 @@ __device__ __forceinline__ int slice_cbase(const SellView& A, int64_t s) {
 // Column of stored entry k of slice s, either format (setup kernels; the
 // sweeps use the compile-time form in load_chunk).
 __device__ __forceinline__ int sell_col(const SellView& A, int64_t s, int64_t k) {
-  return A.narrow ? A.cbase[s] + (int)A.col16[k] : A.col[k];
+  if (!A.narrow) return A.col[k];
+  return A.cbase[s] + (int)A.col16[A.poff ? A.poff[s] + (k - A.sp[s]) : k];
+}
+
+// First column-array element of a row: its row base, or its place in the
+// slice's dictionary pattern (narrow + pattern format).
+__device__ __forceinline__ int64_t sell_colbase(const SellView& A, int64_t slice, int64_t row, int64_t rowbase) {
+  return A.poff ? A.poff[slice] + 2 * (row & 31) : rowbase;
 }
 
 // Loads U consecutive stored entries (stored positions j0..j0+U-1, j0 and U
@@ -231,9 +238,12 @@ __device__ __forceinline__ int sell_col(const SellView& A, int64_t s, int64_t k)
 // read as (column cb, value 0). Padding inside [len, w) is stored as (cb, 0.0),
 // so the gathers that follow never need a bounds check. NW selects the narrow
 // column format (cb = the slice's base column; 0 for wide).
+// cbase0: the row's first element in the column array (sell_colbase; == base
+// unless the operator uses a pattern dictionary, whose table is re-read by
+// every slice with that pattern and so is loaded through the cached path).
 template <int U, bool NW>
-__device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int cb, int j0, int w,
-                                           int* c, double* v) {
+__device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int64_t cbase0, int cb, int j0,
+                                           int w, int* c, double* v) {
   static_assert(U % 2 == 0, "chunks cover whole entry pairs");
 #pragma unroll
   for (int m = 0; m < U / 2; ++m) {
@@ -246,7 +256,8 @@ __device__ __forceinline__ void load_chunk(const SellView& A, int64_t base, int 
     v[2 * m + 1] = vv.y;
     if (NW) {
       ushort2 cc = make_ushort2(0, 0);
-      if (ok) cc = __ldcs(reinterpret_cast<const ushort2*>(A.col16 + k));
+      const ushort2* cp = reinterpret_cast<const ushort2*>(A.col16 + sell_at(cbase0, j));
+      if (ok) cc = __ldg(cp);  // one load flavour: a branch here would serialise the chunk's loads
       c[2 * m] = cb + (int)cc.x;
       c[2 * m + 1] = cb + (int)cc.y;
     } else {

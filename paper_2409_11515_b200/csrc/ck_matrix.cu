@@ -185,6 +185,74 @@ __global__ void k_narrow_cols(int64_t nrows_pad, const int64_t* __restrict__ sp,
   }
 }
 
+// ------------------------------------------------------ pattern dictionary
+// Slices with identical uint16 offset blocks share one copy (Sell::ptab). One
+// warp per slice throughout.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// Order-independent 64-bit hash of (width, offsets): a sum of mixed (index, value) words.
+__global__ void k_slice_hash(int64_t nslices, const int64_t* __restrict__ sp,
+                             const uint16_t* __restrict__ col16, uint64_t* hash, int32_t* ids) {
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  const int64_t b = sp[s], n = sp[s + 1] - b;
+  uint64_t h = 0;
+  for (int64_t k = lane; k < n; k += 32) h += mix64(((uint64_t)k << 16) | col16[b + k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if (lane == 0) {
+    hash[s] = mix64(h ^ (uint64_t)n);
+    ids[s] = (int32_t)s;
+  }
+}
+
+// Sorted by hash: a run of equal keys is a candidate group; head[i] = 1 at its first slice.
+__global__ void k_group_heads(int64_t n, const uint64_t* __restrict__ key, int32_t* head) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) head[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+// gid = inclusive scan of head: group g's representative is the slice at its head, its
+// table size that slice's block.
+__global__ void k_group_reps(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ gid,
+                             const int32_t* __restrict__ sorted_slice, const int64_t* __restrict__ sp,
+                             int32_t* rep, int64_t* gsize) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !head[i]) return;
+  const int32_t g = gid[i] - 1, s = sorted_slice[i];
+  rep[g] = s;
+  gsize[g] = sp[s + 1] - sp[s];
+}
+
+// Every slice takes its group's table offset and checks its block against the
+// representative's, element by element (a hash collision clears *ok); the
+// representative copies its block into the table.
+__global__ void k_group_assign(int64_t n, const int32_t* __restrict__ gid, const int32_t* __restrict__ sorted_slice,
+                               const int32_t* __restrict__ rep, const int64_t* __restrict__ goff,
+                               const int64_t* __restrict__ sp, const uint16_t* __restrict__ col16,
+                               int64_t* poff, uint16_t* ptab, unsigned int* bad) {
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int32_t g = gid[i] - 1, s = sorted_slice[i], r = rep[g];
+  const int64_t b = sp[s], len = sp[s + 1] - b, rb = sp[r], off = goff[g];
+  if (lane == 0) poff[s] = off;
+  if (s == r) {
+    for (int64_t k = lane; k < len; k += 32) ptab[off + k] = col16[b + k];
+  } else {
+    bool same = sp[r + 1] - rb == len;
+    if (same)
+      for (int64_t k = lane; k < len; k += 32) same = same && col16[b + k] == col16[rb + k];
+    if (!same) atomicOr(bad, 1u);
+  }
+}
+
 // ------------------------------------------------------ standalone kernels
 // One thread per permuted row; entries summed in stored order with unfused
 // multiply/add, i.e. exactly matvec's arithmetic (sparse.hpp:221-223).
@@ -204,7 +272,7 @@ __global__ void __launch_bounds__(kTile) k_sell_spmv(SellView A, int64_t nrows_p
   for (int j0 = 0; j0 < w; j0 += U) {
     int c[U];
     double v[U], xg[U];
-    load_chunk<U, NW>(A, base, cb, j0, w, c, v);
+    load_chunk<U, NW>(A, base, sell_colbase(A, row >> 5, row, base), cb, j0, w, c, v);
 #pragma unroll
     for (int u = 0; u < U; ++u) xg[u] = __ldg(x + c[u]);
 #pragma unroll
@@ -304,6 +372,64 @@ double device_norm(const double* v, int64_t n, double* scratch, cudaStream_t st)
   CK_CUDA(cudaMemcpyAsync(&out, scratch + 3 * kNormParts, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaStreamSynchronize(st));
   return out;
+}
+
+// Pattern dictionary of a narrow operator (Sell::ptab): adopted when the distinct
+// slice patterns take at most 1/8 of the stored entries and 64 MB (stencil
+// operators: a few hundred patterns; CK_SELL_PATTERN=0 keeps the per-entry offsets).
+static void build_patterns(Sell& s, cudaStream_t st) {
+  const char* e = std::getenv("CK_SELL_PATTERN");
+  if (e && e[0] == '0') return;
+  const int64_t ns = s.nrows_pad / kSlice;
+  if (ns < 64 || s.entries < 4096) return;
+  DBuf<uint64_t> key(ns), key_sorted(ns);
+  DBuf<int32_t> ids(ns), sorted_slice(ns), head(ns), gid(ns);
+  k_slice_hash<<<grid_for(ns * 32), 256, 0, st>>>(ns, s.slice_ptr.p, s.col16.p, key.p, ids.p);
+  size_t tb = 0;
+  CK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key_sorted.p, ids.p, sorted_slice.p, ns, 0, 64, st));
+  {
+    DBuf<unsigned char> tmp((int64_t)std::max<size_t>(tb, 1));
+    CK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key_sorted.p, ids.p, sorted_slice.p, ns, 0, 64, st));
+    k_group_heads<<<grid_for(ns), 256, 0, st>>>(ns, key_sorted.p, head.p);
+    CK_CUDA(cudaStreamSynchronize(st));
+  }
+  CK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, head.p, gid.p, ns, st));
+  int32_t ngroups = 0;
+  {
+    DBuf<unsigned char> tmp((int64_t)std::max<size_t>(tb, 1));
+    CK_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, head.p, gid.p, ns, st));
+    CK_CUDA(cudaMemcpyAsync(&ngroups, gid.p + (ns - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+  }
+  if (ngroups <= 0 || (int64_t)ngroups * 8 > ns) return;  // too many distinct patterns to pay
+  DBuf<int32_t> rep(ngroups);
+  DBuf<int64_t> gsize(ngroups + 1), goff(ngroups + 1);
+  CK_CUDA(cudaMemsetAsync(gsize.p, 0, sizeof(int64_t) * (ngroups + 1), st));
+  k_group_reps<<<grid_for(ns), 256, 0, st>>>(ns, head.p, gid.p, sorted_slice.p, s.slice_ptr.p, rep.p, gsize.p);
+  CK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, gsize.p, goff.p, ngroups + 1, st));
+  int64_t total = 0;
+  {
+    DBuf<unsigned char> tmp((int64_t)std::max<size_t>(tb, 1));
+    CK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, gsize.p, goff.p, ngroups + 1, st));
+    CK_CUDA(cudaMemcpyAsync(&total, goff.p + ngroups, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK_CUDA(cudaStreamSynchronize(st));
+  }
+  if (total <= 0 || total * 8 > s.entries || total * 2 > (int64_t(64) << 20)) return;
+  DBuf<uint16_t> ptab(total);
+  DBuf<int64_t> poff(ns);
+  DBuf<unsigned int> bad(1);
+  CK_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned int), st));
+  k_group_assign<<<grid_for(ns * 32), 256, 0, st>>>(ns, gid.p, sorted_slice.p, rep.p, goff.p, s.slice_ptr.p,
+                                                    s.col16.p, poff.p, ptab.p, bad.p);
+  CK_CUDA(cudaGetLastError());
+  unsigned int h_bad = 0;
+  CK_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) return;  // a hash collision: keep the per-entry offsets
+  s.ptab = std::move(ptab);
+  s.poff = std::move(poff);
+  s.col16.reset();
+  s.pattern = true;
 }
 
 void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* h_rp,
@@ -453,6 +579,7 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
         CK_CUDA(cudaStreamSynchronize(st));
         s.col.reset();
         s.narrow = true;
+        build_patterns(s, st);
       } else {
         s.cbase.reset();
       }
