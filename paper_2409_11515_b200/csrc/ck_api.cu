@@ -321,7 +321,7 @@ PinnedCache& pinned_cache() {
   static PinnedCache* c = new PinnedCache();
   return *c;
 }
-constexpr size_t kPinnedCacheBuffers = 2;
+constexpr size_t kPinnedCacheBuffers = 6;  // staging chunks of pageable uploads + start-vector buffers
 constexpr size_t kPinnedCacheBytes = size_t(1) << 30;
 }  // namespace
 

@@ -68,7 +68,7 @@ struct Trace {
 // ~0.5 ms per MB and holds the driver while it runs -- at config 4 the 200 MB
 // start-vector buffer stalls the concurrent operator build by ~0.1 s -- so
 // released buffers are kept in a small process-wide cache (ck_api.cu: at most
-// two buffers, 1 GiB in total) and the next session reuses them.
+// six buffers, 1 GiB in total) and the next session reuses them.
 void* pinned_acquire(size_t bytes, size_t* got_bytes);  // nullptr: allocation failed
 void pinned_release(void* p, size_t bytes);
 

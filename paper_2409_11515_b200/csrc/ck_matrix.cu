@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <thread>
 #include <vector>
 
 #include "ck_common.h"
@@ -374,6 +376,53 @@ double device_norm(const double* v, int64_t n, double* scratch, cudaStream_t st)
   return out;
 }
 
+// Host -> device copy of a caller's array. Pinned (or registered) memory goes
+// straight to cudaMemcpyAsync. Pageable memory -- what a numpy / std::vector
+// caller passes -- is staged by the library itself: the runtime's own pageable
+// path copies through one internal buffer on one thread (6-12 GB/s measured
+// here); two 32 MB pinned chunks from the staging cache, filled by four host
+// threads while the previous chunk is on the link, keep the copy near the host's
+// memcpy rate. Returns with the source fully consumed.
+static void h2d_upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  constexpr size_t kChunk = size_t(32) << 20;
+  if (pinned || bytes < 2 * kChunk || std::getenv("CK_NO_STAGED_UPLOAD")) {
+    CK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    if (!pinned) CK_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  constexpr int kBufs = 2, kThreads = 4;
+  PinnedBuf<unsigned char> buf[kBufs];
+  cudaEvent_t done[kBufs];
+  for (int b = 0; b < kBufs; ++b) {
+    buf[b].resize((int64_t)kChunk);
+    CK_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+  }
+  const unsigned char* sp = static_cast<const unsigned char*>(src);
+  unsigned char* dp = static_cast<unsigned char*>(dst);
+  int64_t i = 0;
+  for (size_t off = 0; off < bytes; off += kChunk, ++i) {
+    const int b = (int)(i % kBufs);
+    const size_t len = std::min(kChunk, bytes - off);
+    if (i >= kBufs) CK_CUDA(cudaEventSynchronize(done[b]));  // the chunk this buffer held has left
+    const size_t part = (len + kThreads - 1) / kThreads;
+    std::thread th[kThreads - 1];
+    for (int t = 1; t < kThreads; ++t) {
+      const size_t lo = std::min(len, t * part), hi = std::min(len, lo + part);
+      th[t - 1] = std::thread([=, &buf] { if (hi > lo) std::memcpy(buf[b].p + lo, sp + off + lo, hi - lo); });
+    }
+    std::memcpy(buf[b].p, sp + off, std::min(len, part));
+    for (auto& t : th) t.join();
+    CK_CUDA(cudaMemcpyAsync(dp + off, buf[b].p, len, cudaMemcpyHostToDevice, st));
+    CK_CUDA(cudaEventRecord(done[b], st));
+  }
+  CK_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < kBufs; ++b) cudaEventDestroy(done[b]);
+}
+
 // Pattern dictionary of a narrow operator (Sell::ptab): adopted when the distinct
 // slice patterns take at most 1/8 of the stored entries and 64 MB (stencil
 // operators: a few hundred patterns; CK_SELL_PATTERN=0 keeps the per-entry offsets).
@@ -454,10 +503,10 @@ void matrix_upload(ck_matrix_s* m, int64_t nrows, int64_t ncols, const int64_t* 
   DBuf<int64_t> rp(nrows + 1);
   DBuf<int32_t> ci(std::max<int64_t>(nnz, 1));
   DBuf<double> va(std::max<int64_t>(nnz, 1));
-  CK_CUDA(cudaMemcpyAsync(rp.p, h_rp, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice, st));
+  h2d_upload(rp.p, h_rp, sizeof(int64_t) * (nrows + 1), st);
   if (nnz > 0) {
-    CK_CUDA(cudaMemcpyAsync(ci.p, h_ci, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
-    CK_CUDA(cudaMemcpyAsync(va.p, h_va, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+    h2d_upload(ci.p, h_ci, sizeof(int32_t) * nnz, st);
+    h2d_upload(va.p, h_va, sizeof(double) * nnz, st);
   }
   tr.mark("alloc + H2D", st);
   DBuf<unsigned int> flags(1);
