@@ -134,18 +134,20 @@ struct RingFeed {
   __device__ __forceinline__ void finish(DenseRing& R) const { R.count += (uint32_t)nb; }
 };
 
-// 32 products in four independent chains, merged in a fixed order; the
-// coefficients of this thread's row at cf[c * ld].
+// 32 products in eight independent chains of four (the block step is one
+// dependent chain per thread: fp64 FMA latency, not issue, bounds it), merged
+// in a fixed order; the coefficients of this thread's row at cf[c * ld].
 __device__ __forceinline__ double dense_dot32(const double* cf, int64_t ld, const double* h) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double a[8];
 #pragma unroll
-  for (int c = 0; c < 32; c += 4) {
-    a0 = __fma_rn(cf[c * ld], h[c], a0);
-    a1 = __fma_rn(cf[(c + 1) * ld], h[c + 1], a1);
-    a2 = __fma_rn(cf[(c + 2) * ld], h[c + 2], a2);
-    a3 = __fma_rn(cf[(c + 3) * ld], h[c + 3], a3);
+  for (int k = 0; k < 8; ++k) a[k] = __dmul_rn(cf[k * ld], h[k]);
+#pragma unroll
+  for (int c = 8; c < 32; c += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __fma_rn(cf[(c + k) * ld], h[c + k], a[k]);
   }
-  return __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+  return __dadd_rn(__dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3])),
+                   __dadd_rn(__dadd_rn(a[4], a[5]), __dadd_rn(a[6], a[7])));
 }
 
 // Forward push sweep (L forward with PERM, U^T forward without): window rows
@@ -275,27 +277,23 @@ static __device__ void dense_lt_backward(const DenseView& d, double* x, double* 
     if (p < P) {
       // inputs k' = p * 32 + kk of this part; coefficient (k', c) at cf[k' * 32 + c]
       const int kmax = W - p * 32 < 32 ? W - p * 32 : 32;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       const double* cp = cf + (int64_t)p * 32 * 32 + c;
       const double* ip = in + p * 32;
+      double acc;
       if (kmax == 32) {
+        acc = dense_dot32(cp, 32, ip);
+      } else {  // the window's last, partial part: same chain assignment, missing terms are zeros
+        double a[8];
 #pragma unroll
-        for (int kk = 0; kk < 32; kk += 4) {
-          a0 = __fma_rn(cp[kk * 32], ip[kk], a0);
-          a1 = __fma_rn(cp[(kk + 1) * 32], ip[kk + 1], a1);
-          a2 = __fma_rn(cp[(kk + 2) * 32], ip[kk + 2], a2);
-          a3 = __fma_rn(cp[(kk + 3) * 32], ip[kk + 3], a3);
+        for (int k = 0; k < 8; ++k) a[k] = 0.0;
+        for (int kk = 0; kk < kmax; ++kk) {
+          const double t = __dmul_rn(cp[kk * 32], ip[kk]);
+          a[kk & 7] = kk < 8 ? t : __fma_rn(cp[kk * 32], ip[kk], a[kk & 7]);
         }
-      } else {
-        for (int kk = 0; kk < kmax; ++kk) {  // same chain assignment as the unrolled form
-          const double t = cp[kk * 32];
-          if ((kk & 3) == 0) a0 = __fma_rn(t, ip[kk], a0);
-          if ((kk & 3) == 1) a1 = __fma_rn(t, ip[kk], a1);
-          if ((kk & 3) == 2) a2 = __fma_rn(t, ip[kk], a2);
-          if ((kk & 3) == 3) a3 = __fma_rn(t, ip[kk], a3);
-        }
+        acc = __dadd_rn(__dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3])),
+                        __dadd_rn(__dadd_rn(a[4], a[5]), __dadd_rn(a[6], a[7])));
       }
-      part[p * 32 + c] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+      part[p * 32 + c] = acc;
     }
     __syncthreads();
     if (tid < W) {
