@@ -68,9 +68,12 @@ struct DenseRing {
   uint64_t* bar;         // [ns] mbarriers
   int ns;                // stages in use
   int64_t stage;         // doubles per stage (>= 32 * max(wl, wu))
-  // blocks streamed so far (same in every thread): the stages are used round
-  // robin across sweeps, so a stage's mbarrier phase is (count / ns) & 1
-  uint32_t count;
+  // the stage the next block arrives in and every stage's mbarrier phase
+  // parity (bit s; same in every thread): the stages are used round robin
+  // across sweeps, and a runtime modulo per block would sit on the critical path
+  int cur;
+  uint32_t pbits;
+  __device__ __forceinline__ void advance() { cur = cur + 1 == ns ? 0 : cur + 1; }
 };
 
 // Shared memory of a dense CTA in doubles: window buffers, L^T partials, ring.
@@ -118,20 +121,29 @@ struct RingFeed {
   const double* C;
   int first, step, nb;
   uint32_t bytes;
-  __device__ __forceinline__ void issue(const DenseRing& R, int k) const {
-    if (threadIdx.x == 0 && k < nb)
-      ring_issue(R, (int)((R.count + k) % R.ns), C + (int64_t)(first + k * step) * (bytes / 8), bytes);
+  // one thread requests block k of the sweep into stage s
+  __device__ __forceinline__ void issue(const DenseRing& R, int k, int s) const {
+    if (threadIdx.x == 0 && k < nb) ring_issue(R, s, C + (int64_t)(first + k * step) * (bytes / 8), bytes);
   }
   // every stage is free here: the previous sweep waited for all it issued
   __device__ __forceinline__ void start(const DenseRing& R) const {
-    for (int k = 0; k < R.ns; ++k) issue(R, k);
+    int s = R.cur;
+    for (int k = 0; k < R.ns; ++k) {
+      issue(R, k, s);
+      s = s + 1 == R.ns ? 0 : s + 1;
+    }
   }
-  __device__ __forceinline__ const double* wait(const DenseRing& R, int k) const {
-    const uint32_t g = R.count + (uint32_t)k;
-    ring_wait(R, (int)(g % R.ns), (g / R.ns) & 1u);
-    return R.buf + (int64_t)(g % R.ns) * R.stage;
+  // the current block's data (stage R.cur)
+  __device__ __forceinline__ const double* wait(DenseRing& R) const {
+    ring_wait(R, R.cur, (R.pbits >> R.cur) & 1u);
+    R.pbits ^= 1u << R.cur;
+    return R.buf + (int64_t)R.cur * R.stage;
   }
-  __device__ __forceinline__ void finish(DenseRing& R) const { R.count += (uint32_t)nb; }
+  // after the block's barrier: its stage takes block k + ns, the ring moves on
+  __device__ __forceinline__ void next(DenseRing& R, int k) const {
+    issue(R, k + R.ns, R.cur);
+    R.advance();
+  }
 };
 
 // 32 products in eight independent chains of four (the block step is one
@@ -175,30 +187,30 @@ __device__ void dense_forward(const DenseView& d, const double* __restrict__ C, 
       const int64_t g = J + W + (tid - W);
       fresh = g < n ? x[g] : 0.0;
     }
-    const double* cf = feed.wait(R, blk);
+    // where this thread's value goes in the next window (the next block's
+    // interchange folded in): requested before the block's data is waited for,
+    // a global load here would sit on the block step's critical path
+    int pos = tid < W ? tid - 32 : W - 32 + (tid - W);
+    if (PERM && more && tid >= 32 && tid < W + 32) pos = d.pinv[(int64_t)(blk + 1) * d.wl + pos];
+    const double* cf = feed.wait(R);
     if (tid < W) {
       const double acc = dense_dot32(cf + tid, W, in);
       if (tid < 32) {
         if (J + tid < n) x[J + tid] = acc;  // head rows are final
       } else if (more) {
-        const int q = tid - 32;
-        const int pos = PERM ? d.pinv[(int64_t)(blk + 1) * d.wl + q] : q;
         CK_DASSERT(pos >= 0 && pos < W);
         out[pos] = __dadd_rn(in[tid], acc);
       }
     } else if (tid < W + 32 && more) {
-      const int q = W - 32 + (tid - W);
-      const int pos = PERM ? d.pinv[(int64_t)(blk + 1) * d.wl + q] : q;
       CK_DASSERT(pos >= 0 && pos < W);
       out[pos] = fresh;
     }
     __syncthreads();
-    feed.issue(R, blk + R.ns);  // the stage just read is free again
+    feed.next(R, blk);  // the stage just read is free again
     double* t = in;
     in = out;
     out = t;
   }
-  feed.finish(R);
 }
 
 // U backward: window rows [J - kv, J + 32), head = positions [kv, kv + 32).
@@ -228,7 +240,7 @@ static __device__ void dense_u_backward(const DenseView& d, double* x, double* w
       const int64_t g = J - 32 - kv + (tid - W);
       fresh = g >= 0 ? x[g] : 0.0;
     }
-    const double* cf = feed.wait(R, k);
+    const double* cf = feed.wait(R);
     if (tid < W) {
       const double acc = dense_dot32(cf + tid, W, in + kv);
       if (tid >= kv) {
@@ -241,12 +253,11 @@ static __device__ void dense_u_backward(const DenseView& d, double* x, double* w
       out[tid - W] = fresh;
     }
     __syncthreads();
-    feed.issue(R, k + R.ns);
+    feed.next(R, k);
     double* t = in;
     in = out;
     out = t;
   }
-  feed.finish(R);
 }
 
 // L^T backward: window rows [J, J + wl); the 32 head outputs are reductions
@@ -273,7 +284,9 @@ static __device__ void dense_lt_backward(const DenseView& d, double* x, double* 
     const bool more = blk > 0;
     double fresh = 0.0;
     if (more && tid < 32) fresh = x[J - 32 + tid];  // rows entering above (J >= 32 here)
-    const double* cf = feed.wait(R, k);
+    // the inverse interchange's target of this thread's row, requested ahead of the wait
+    const int pos = tid < W ? d.psrc[(int64_t)blk * d.wl + tid] : 0;  // q -> psrc[q]
+    const double* cf = feed.wait(R);
     if (p < P) {
       // inputs k' = p * 32 + kk of this part; coefficient (k', c) at cf[k' * 32 + c]
       const int kmax = W - p * 32 < 32 ? W - p * 32 : 32;
@@ -304,7 +317,6 @@ static __device__ void dense_lt_backward(const DenseView& d, double* x, double* 
       } else {
         v = in[tid];
       }
-      const int pos = d.psrc[(int64_t)blk * d.wl + tid];  // inverse interchange: q -> psrc[q]
       CK_DASSERT(pos >= 0 && pos < W);
       if (more && pos < kl) {
         out[pos + 32] = v;
@@ -314,12 +326,11 @@ static __device__ void dense_lt_backward(const DenseView& d, double* x, double* 
     }
     if (more && tid < 32) out[tid] = fresh;
     __syncthreads();
-    feed.issue(R, k + R.ns);
+    feed.next(R, k);
     double* t = in;
     in = out;
     out = t;
   }
-  feed.finish(R);
 }
 
 // x := U^-1 L^-1 P x  (transpose: x := P^T L^-T U^-T x), one CTA of
@@ -355,7 +366,8 @@ __device__ __forceinline__ DenseRing dense_ring(const DenseView& d, double* dyn,
   R.stage = dense_ring_stage(d.wl, d.wu);
   const int64_t fit = ((int64_t)(dyn_bytes / sizeof(double)) - 8) / R.stage;
   R.ns = (int)(fit < kDenseStagesMax ? fit : kDenseStagesMax);
-  R.count = 0;
+  R.cur = 0;
+  R.pbits = 0;
   ring_init(R);
   return R;
 }
