@@ -123,7 +123,10 @@ struct RingFeed {
   uint32_t bytes;
   // one thread requests block k of the sweep into stage s
   __device__ __forceinline__ void issue(const DenseRing& R, int k, int s) const {
-    if (threadIdx.x == 0 && k < nb) ring_issue(R, s, C + (int64_t)(first + k * step) * (bytes / 8), bytes);
+    // the issuer sits in the last warp, which owns no window row for all but the widest
+    // bands: the copy's address arithmetic stays off the head rows' warp
+    if (threadIdx.x == kDenseThreads - 32 && k < nb)
+      ring_issue(R, s, C + (int64_t)(first + k * step) * (bytes / 8), bytes);
   }
   // every stage is free here: the previous sweep waited for all it issued
   __device__ __forceinline__ void start(const DenseRing& R) const {
