@@ -354,8 +354,10 @@ __device__ __forceinline__ void clu_push_ring_head(const Clu& C, const Ring* rin
 }
 
 // Rows [lo, hi) of share k out of `size` of the row range [m0, m1).
+// (32-bit arithmetic: the range is at most a band width, k < 16 -- a 64-bit
+// division is ~100 instructions on every helper's path, twice per block)
 __device__ __forceinline__ int64_t clu_cut(int64_t m0, int64_t m1, int k, int size) {
-  return m0 + ((m1 - m0) * k) / size;
+  return m0 + (int64_t)(((uint32_t)(m1 - m0) * (uint32_t)k) / (uint32_t)size);
 }
 
 // Helper: the coefficients of a share, cf[c * (hi - lo) + (m - lo)] = coef(m, c)
