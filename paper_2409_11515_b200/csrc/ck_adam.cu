@@ -1186,12 +1186,13 @@ void session_init_common(ck_session_s* s, const ck_adam_cfg* cfg, const uint64_t
   pinned();
   tr.mark("remaining columns", st);
   push_state(s);
-  // chunk length: about 4 ms of device work per host round trip, 4..256 steps
+  // chunk length: about 4 ms of device work per host round trip, 16..256 steps (a finished
+  // column's kernels return at once, so a chunk that overshoots the end costs launches only)
   // bytes_per_step < 0: a fixed chunk of -bytes_per_step steps (latency-bound
   // loops, where streamed bytes say nothing about the step time)
   const int steps = bytes_per_step < 0
                         ? (int)-bytes_per_step
-                        : (int)std::min(256.0, std::max(4.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
+                        : (int)std::min(256.0, std::max(16.0, 4e-3 * 6.0e12 / std::max(bytes_per_step, 1.0)));
   build_graph(s, steps);
   tr.mark("graph capture", st);
 }
