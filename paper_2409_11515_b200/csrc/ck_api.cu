@@ -330,8 +330,11 @@ void* pinned_acquire(size_t bytes, size_t* got_bytes) {
     PinnedCache& c = pinned_cache();
     std::lock_guard<std::mutex> lk(c.mu);
     int best = -1;
-    for (int i = 0; i < (int)c.free_list.size(); ++i)  // smallest cached buffer that fits
-      if (c.free_list[i].second >= bytes && (best < 0 || c.free_list[i].second < c.free_list[best].second))
+    // smallest cached buffer that fits, but none more than twice the request: a 32 MB
+    // staging chunk must not take the 200 MB start-vector buffer out of the cache
+    for (int i = 0; i < (int)c.free_list.size(); ++i)
+      if (c.free_list[i].second >= bytes && c.free_list[i].second <= 2 * bytes &&
+          (best < 0 || c.free_list[i].second < c.free_list[best].second))
         best = i;
     if (best >= 0) {
       void* p = c.free_list[best].first;
