@@ -76,6 +76,9 @@ static double two_norm_seq(const double* v, int64_t n) {
   return amax * std::sqrt(s);
 }
 
+// Host cores random_unit_vector_host leaves free on the calling thread's behalf.
+static thread_local int tl_rng_reserve_cores = 0;
+
 template <class F>
 static void parallel_for(int64_t n, F&& f) {
   unsigned hw = std::max(1u, std::thread::hardware_concurrency());
@@ -183,7 +186,10 @@ void random_unit_vector_host(void* engine, int64_t n, double* out,
   buf[0].resize((size_t)(2 * std::min(n, kBlock)));
   buf[1].resize(buf[0].size());
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const int64_t nthr = std::min<int64_t>(hw, 64);
+  // a background draw (ck_start_vector_prefetch) leaves cores to the thread that is
+  // uploading and building the operator meanwhile: with every core taken, that thread's
+  // launches and stream waits sporadically stalled for 0.3-0.8 s
+  const int64_t nthr = std::max<int64_t>(1, std::min<int64_t>((int64_t)hw - tl_rng_reserve_cores, 64));
   // bulk draws from 2^15 words on (text state round trip ~0.1 ms)
   std::unique_ptr<Mt64Bulk> bulk;
   if (n >= (int64_t(1) << 14) && Mt64Bulk::verified()) {
@@ -427,6 +433,7 @@ extern "C" ck_status ck_start_vector_prefetch(uint64_t seed, int64_t n) {
     CK_CUDA(cudaGetDevice(&pf->device));
     StartPrefetch* p = pf.get();
     pf->th = std::thread([p] {
+      tl_rng_reserve_cores = 3;
       try {
         // The pinned buffer is pinned after the draw, not alongside it: pinning
         // 8n bytes holds the driver for ~0.1 s and stalls whatever upload call
