@@ -503,10 +503,15 @@ def run_ours(args):
             traffic = None
     roofline = {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": dom["frac"], "traffic": traffic, "traffic_source": traffic_src, "kernel": dom["name"],
+                # the two kernels of a step take ~50% each; which one is the longer changes with
+                # the SM clock the power cap leaves: k_apply (L1 data pipe bound) or k_transpose
+                # (DRAM bound). step_frac is the whole step's algorithmic bytes over its time.
+                "step_frac": None,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "bytes_per_launch": dom["bytes"]}
     iter_bytes = b_apply + b_tr
     step_eff_gbs = iter_bytes / (ms_total / args.steps / 1000.0) / 1e9
+    roofline["step_frac"] = step_eff_gbs / peak
 
     # ---- e2e: the public API call a user makes, from host buffers ----
     e2e = None
